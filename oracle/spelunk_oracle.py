@@ -1,0 +1,785 @@
+"""CPU oracle for the range-analysis hot path -- TEST INFRASTRUCTURE ONLY.
+
+This module is a numpy (FP64) restatement of the reference algorithms in
+`/root/reference/pkg/src/spelunk` (arXiv 2202.02444, "Spelunking the Deep").
+It exists so that the CUDA path can be checked on the GPU box, where the
+reference itself is absent.  Only `tests/`, `__graft_entry__.smoke()` and the
+`cpu_baseline` / `--impl reference` legs of `bench.py` may import it, and only
+as the checker or the timed CPU baseline -- never as a product code path.
+
+Parity status: PINNED.  `tests/golden/make_golden.py` runs the unmodified
+reference in the build container and commits its outputs under
+`tests/golden/`; `tests/test_oracle_golden.py` checks this module against
+every vector (bounds to 1e-12, point values bit-exact, tree labels / ray hits
+/ mesh triangle sets exactly).
+
+Layout differs from the reference on purpose: affine state is kept per box as
+base (b, m), coef (b, m, n_sym), err (b, m) rather than the reference's
+(n_sym, b, m) ping-pong slabs, so sums run in a different order and results
+agree to the last few ulps, which the reference itself allows
+(range_core.py:552-553).
+"""
+
+from __future__ import annotations
+
+import json
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+TWO_PI = 2.0 * np.pi
+ACTIVATIONS = ("relu", "elu", "sin", "tanh", "identity")
+
+
+# ---------------------------------------------------------------------------
+# Network  (network.py:29-116 types, :236-313 schema, :143-183 evaluation)
+
+
+@dataclass
+class OracleNet:
+    """Flat op list: ("dense", W (out,in), b) or ("act", kind)."""
+
+    input_dim: int
+    ops: list
+
+    @property
+    def widths(self):
+        out = [self.input_dim]
+        for op in self.ops:
+            if op[0] == "dense":
+                out.append(op[1].shape[0])
+        return out
+
+
+def net_from_json_doc(doc: dict) -> OracleNet:
+    """Weight-file schema of network.py:236-287 (validation is the package's job)."""
+    ops = []
+    for entry in doc["layers"]:
+        if entry["type"] == "dense":
+            ops.append(
+                (
+                    "dense",
+                    np.asarray(entry["weights"], dtype=np.float64),
+                    np.asarray(entry["bias"], dtype=np.float64),
+                )
+            )
+        else:
+            ops.append(("act", str(entry["kind"])))
+    return OracleNet(int(doc["input_dim"]), ops)
+
+
+def load_net(path) -> OracleNet:
+    with open(path, "r", encoding="utf-8") as f:
+        return net_from_json_doc(json.load(f))
+
+
+def as_oracle_net(net) -> OracleNet:
+    """Accept an OracleNet, a weight-file path/dict, or any NetworkSpec-like
+    object whose .layers hold objects with .weights/.bias or enum activations."""
+    if isinstance(net, OracleNet):
+        return net
+    if isinstance(net, dict):
+        return net_from_json_doc(net)
+    if isinstance(net, (str, bytes)) or hasattr(net, "__fspath__"):
+        return load_net(net)
+    ops = []
+    for layer in net.layers:
+        if hasattr(layer, "weights"):
+            ops.append(
+                (
+                    "dense",
+                    np.asarray(layer.weights, dtype=np.float64),
+                    np.asarray(layer.bias, dtype=np.float64),
+                )
+            )
+        else:
+            ops.append(("act", str(getattr(layer, "value", layer))))
+    return OracleNet(int(net.input_dim), ops)
+
+
+def _act_value(x, kind):
+    """Pointwise activations (network.py:149-160)."""
+    if kind == "relu":
+        return np.maximum(x, 0.0)
+    if kind == "elu":
+        return np.where(x >= 0.0, x, np.expm1(np.minimum(x, 0.0)))
+    if kind == "sin":
+        return np.sin(x)
+    if kind == "tanh":
+        return np.tanh(x)
+    if kind == "identity":
+        return x
+    raise ValueError(kind)
+
+
+def eval_points(net, xs) -> np.ndarray:
+    """Deterministic FP64 point evaluation (network.py:163-183).
+
+    Uses the same fixed-order einsum contraction as the reference so values
+    are bit-identical to `eval_batch` (pinned by the golden test).
+    """
+    net = as_oracle_net(net)
+    x = np.asarray(xs, dtype=np.float64)
+    if x.size == 0:
+        return np.zeros(0)
+    for op in net.ops:
+        if op[0] == "dense":
+            x = np.einsum("nk,mk->nm", x, op[1], optimize=False) + op[2]
+        else:
+            x = _act_value(x, op[1])
+    return x[:, 0]
+
+
+def eval_points_blas(net, xs) -> np.ndarray:
+    """BLAS forward pass (network.py:196-222); last-ulp differences allowed."""
+    net = as_oracle_net(net)
+    x = np.asarray(xs, dtype=np.float64)
+    for op in net.ops:
+        if op[0] == "dense":
+            x = x @ op[1].T + op[2]
+        else:
+            x = _act_value(x, op[1])
+    return x[:, 0]
+
+
+# ---------------------------------------------------------------------------
+# Linearisation rules (range_core.py:213-349).  Each affine rule returns
+# (alpha, beta, gamma) with |h(x) - alpha x - beta| <= gamma on [lo, hi];
+# each interval rule returns the exact image of [lo, hi].
+
+
+def _relu_linear(lo, hi):
+    # range_core.py:213-231: Chebyshev secant on straddling lanes
+    width = hi - lo
+    on = lo >= 0.0
+    off = hi <= 0.0
+    mixed = ~(on | off)
+    slope = hi / np.where(mixed, width, 1.0)
+    alpha = np.where(mixed, slope, np.where(on, 1.0, 0.0))
+    beta = np.where(mixed, -slope * lo * 0.5, 0.0)
+    gamma = beta.copy()
+    flat = width == 0.0
+    if flat.any():
+        a0 = np.where(lo > 0.0, 1.0, 0.0)
+        alpha = np.where(flat, a0, alpha)
+        beta = np.where(flat, np.maximum(lo, 0.0) - a0 * lo, beta)
+        gamma = np.where(flat, 0.0, gamma)
+    return alpha, beta, gamma
+
+
+def _elu_value(x):
+    return np.where(x >= 0.0, x, np.expm1(np.minimum(x, 0.0)))
+
+
+def _elu_linear(lo, hi):
+    # range_core.py:238-264: secant slope, tangent point x* = ln(alpha)
+    width = hi - lo
+    flat = width == 0.0
+    on = lo >= 0.0
+    f_lo = _elu_value(lo)
+    f_hi = _elu_value(hi)
+    alpha = np.where(on, 1.0, (f_hi - f_lo) / np.where(flat, 1.0, width))
+    under = alpha <= 0.0
+    log_arg = np.where(under | on, 1.0, alpha)
+    top = f_lo - alpha * lo
+    bottom = (alpha - 1.0) - alpha * np.log(log_arg)
+    beta = np.where(on, 0.0, (top + bottom) * 0.5)
+    gamma = np.where(on, 0.0, (top - bottom) * 0.5)
+    if under.any():
+        alpha = np.where(under, 0.0, alpha)
+        beta = np.where(under, (f_lo + f_hi) * 0.5, beta)
+        gamma = np.where(under, (f_hi - f_lo) * 0.5, gamma)
+    if flat.any():
+        a0 = np.where(lo >= 0.0, 1.0, np.exp(np.minimum(lo, 0.0)))
+        alpha = np.where(flat, a0, alpha)
+        beta = np.where(flat, f_lo - a0 * lo, beta)
+        gamma = np.where(flat, 0.0, gamma)
+    return alpha, np.asarray(beta), np.maximum(gamma, 0.0)
+
+
+def cos_range(lo, hi):
+    """Range of cos over [lo, hi] by modular extremum detection (range_core.py:267-274)."""
+    c_lo, c_hi = np.cos(lo), np.cos(hi)
+    peak = np.floor(hi / TWO_PI) * TWO_PI >= lo
+    trough = np.floor((hi - np.pi) / TWO_PI) * TWO_PI + np.pi >= lo
+    return (
+        np.where(trough, -1.0, np.minimum(c_lo, c_hi)),
+        np.where(peak, 1.0, np.maximum(c_lo, c_hi)),
+    )
+
+
+def _sin_linear(lo, hi):
+    # range_core.py:277-294: slope = mid of cos range, extremes at the ends
+    # or at the first two 2pi-translates of +-arccos(alpha) at/after lo
+    c_min, c_max = cos_range(lo, hi)
+    alpha = (c_min + c_max) * 0.5
+    e = np.arccos(np.clip(alpha, -1.0, 1.0))
+    xs = [lo, hi]
+    for root in (e, -e):
+        first = root + TWO_PI * np.ceil((lo - root) / TWO_PI)
+        xs.append(np.clip(first, lo, hi))
+        xs.append(np.clip(first + TWO_PI, lo, hi))
+    rem = np.stack([np.sin(x) - alpha * x for x in xs])
+    top, bottom = rem.max(axis=0), rem.min(axis=0)
+    return alpha, (top + bottom) * 0.5, (top - bottom) * 0.5
+
+
+def _tanh_linear(lo, hi):
+    # range_core.py:297-317
+    width = hi - lo
+    flat = width == 0.0
+    f_lo, f_hi = np.tanh(lo), np.tanh(hi)
+    alpha = np.where(flat, 1.0 - f_lo * f_lo, (f_hi - f_lo) / np.where(flat, 1.0, width))
+    with np.errstate(divide="ignore"):
+        x_star = np.arctanh(np.clip(np.sqrt(np.clip(1.0 - alpha, 0.0, 1.0)), 0.0, 1.0))
+    xs = [lo, hi, np.clip(x_star, lo, hi), np.clip(-x_star, lo, hi)]
+    rem = np.stack([np.tanh(x) - alpha * x for x in xs])
+    top, bottom = rem.max(axis=0), rem.min(axis=0)
+    beta = (top + bottom) * 0.5
+    gamma = (top - bottom) * 0.5
+    if flat.any():
+        beta = np.where(flat, f_lo - alpha * lo, beta)
+        gamma = np.where(flat, 0.0, gamma)
+    return alpha, beta, np.maximum(gamma, 0.0)
+
+
+def _identity_linear(lo, hi):
+    return np.ones_like(lo), np.zeros_like(lo), np.zeros_like(lo)
+
+
+def _sin_image(lo, hi):
+    # range_core.py:338-345
+    s_lo, s_hi = np.sin(lo), np.sin(hi)
+    peak = np.floor((hi - 0.5 * np.pi) / TWO_PI) * TWO_PI + 0.5 * np.pi >= lo
+    trough = np.floor((hi + 0.5 * np.pi) / TWO_PI) * TWO_PI - 0.5 * np.pi >= lo
+    return (
+        np.where(trough, -1.0, np.minimum(s_lo, s_hi)),
+        np.where(peak, 1.0, np.maximum(s_lo, s_hi)),
+    )
+
+
+LINEAR_RULES = {
+    "relu": _relu_linear,
+    "elu": _elu_linear,
+    "sin": _sin_linear,
+    "tanh": _tanh_linear,
+    "identity": _identity_linear,
+}
+
+IMAGE_RULES = {
+    "relu": lambda lo, hi: (np.maximum(lo, 0.0), np.maximum(hi, 0.0)),
+    "elu": lambda lo, hi: (_elu_value(lo), _elu_value(hi)),
+    "sin": _sin_image,
+    "tanh": lambda lo, hi: (np.tanh(lo), np.tanh(hi)),
+    "identity": lambda lo, hi: (lo, hi),
+}
+
+
+# ---------------------------------------------------------------------------
+# Policies (range_core.py:104-165)
+
+
+def parse_policy(policy):
+    """Return (kind, n_keep); accepts strings or CondensationPolicy-like objects."""
+    if not isinstance(policy, str):
+        kind = getattr(policy.kind, "value", policy.kind)
+        return str(kind), getattr(policy, "n_keep", None)
+    name = policy.strip().lower()
+    if name.startswith("affine-truncate"):
+        return "affine-truncate", int(name.partition(":")[2])
+    if name in ("interval", "affine-fixed", "affine-full"):
+        return name, None
+    raise ValueError(f"unknown policy {policy!r}")
+
+
+# ---------------------------------------------------------------------------
+# Batched bound evaluation (range_core.py:547-642)
+
+
+def interval_bounds(net, centers, axes):
+    """Centre/radius interval propagation over the axis-aligned hull
+    (range_core.py:625-642)."""
+    net = as_oracle_net(net)
+    c = np.asarray(centers, dtype=np.float64)
+    r = np.abs(np.asarray(axes, dtype=np.float64)).sum(axis=1)
+    for op in net.ops:
+        if op[0] == "dense":
+            w = op[1]
+            c = c @ w.T + op[2]
+            r = r @ np.abs(w.T)
+        else:
+            lo, hi = IMAGE_RULES[op[1]](c - r, c + r)
+            c = (lo + hi) * 0.5
+            r = (hi - lo) * 0.5
+    return c[:, 0] - r[:, 0], c[:, 0] + r[:, 0]
+
+
+def affine_bounds(net, centers, axes, policy="affine-fixed"):
+    """Affine-arithmetic bound of the network over oriented boxes
+    (range_core.py:547-622; Alg. 1 of the paper).
+
+    centers (b, d), axes (b, s, d) with zero rows as padding.  State per box:
+    base (b, m), coef (b, m, n_sym), err (b, m) >= 0.
+    """
+    net = as_oracle_net(net)
+    kind, n_keep = parse_policy(policy)
+    if kind == "interval":
+        return interval_bounds(net, centers, axes)
+    base = np.array(centers, dtype=np.float64)
+    ax = np.asarray(axes, dtype=np.float64)
+    coef = np.ascontiguousarray(np.swapaxes(ax, 1, 2))  # (b, d, s)
+    err = np.zeros_like(base)
+    for op in net.ops:
+        if op[0] == "dense":
+            w = op[1]
+            base = base @ w.T + op[2]
+            coef = np.matmul(w[None, :, :], coef)
+            err = err @ np.abs(w.T)
+            continue
+        if op[1] == "identity":
+            continue
+        r = np.abs(coef).sum(axis=2) + err
+        alpha, beta, gamma = LINEAR_RULES[op[1]](base - r, base + r)
+        base = alpha * base + beta
+        coef = coef * alpha[:, :, None]
+        if kind == "affine-fixed":
+            err = np.abs(alpha) * err + gamma
+            continue
+        err = np.abs(alpha) * err
+        b, m = base.shape
+        fresh = np.zeros((b, m, m))
+        idx = np.arange(m)
+        fresh[:, idx, idx] = gamma
+        coef = np.concatenate([coef, fresh], axis=2)
+        if kind == "affine-truncate" and coef.shape[2] > n_keep:
+            coef, err = _truncate_rows(coef, err, n_keep)
+    r = np.abs(coef[:, 0, :]).sum(axis=1) + err[:, 0]
+    return base[:, 0] - r, base[:, 0] + r
+
+
+def _truncate_rows(coef, err, n_keep):
+    """Per box keep the n_keep symbols of largest L1 norm (ties -> lower
+    index, kept symbols stay in order) and fold the rest into err
+    (range_core.py:604-619)."""
+    mag = np.abs(coef)
+    norms = mag.sum(axis=1)  # (b, n)
+    order = np.argsort(-norms, axis=1, kind="stable")
+    keep = np.sort(order[:, :n_keep], axis=1)
+    drop = np.sort(order[:, n_keep:], axis=1)
+    folded = np.take_along_axis(mag, drop[:, None, :], axis=2).sum(axis=2)
+    kept = np.take_along_axis(coef, keep[:, None, :], axis=2)
+    return kept, err + folded
+
+
+def bound_batch(net, centers, axes, policy="affine-fixed", chunk=None):
+    """range_bound_batch equivalent; optional chunking like spatial.py:38."""
+    centers = np.asarray(centers, dtype=np.float64)
+    axes = np.asarray(axes, dtype=np.float64)
+    if chunk is None or len(centers) <= chunk:
+        return affine_bounds(net, centers, axes, policy)
+    lo = np.empty(len(centers))
+    hi = np.empty(len(centers))
+    for s in range(0, len(centers), chunk):
+        lo[s : s + chunk], hi[s : s + chunk] = affine_bounds(
+            net, centers[s : s + chunk], axes[s : s + chunk], policy
+        )
+    return lo, hi
+
+
+def sign_labels(lo, hi):
+    """+1 POSITIVE (lo > 0), -1 NEGATIVE (hi < 0), 0 UNKNOWN (range_core.py:504-509)."""
+    lo = np.asarray(lo)
+    hi = np.asarray(hi)
+    return np.where(lo > 0.0, 1, np.where(hi < 0.0, -1, 0)).astype(np.int8)
+
+
+# ---------------------------------------------------------------------------
+# k-d tree, breadth first (spatial.py:172-289)
+
+
+def _cube_axes(lo, hi):
+    n, d = lo.shape
+    axes = np.zeros((n, d, d))
+    i = np.arange(d)
+    axes[:, i, i] = (hi - lo) / 2.0
+    return axes
+
+
+def bound_aabbs(net, los, his, policy, chunk=4096):
+    """spatial.py:172-186: centres (lo+hi)/2, diagonal half-extent axes."""
+    return bound_batch(net, (los + his) / 2.0, _cube_axes(los, his), policy, chunk)
+
+
+def split_widest(los, his):
+    """spatial.py:189-199: halve on the widest axis (ties to the lowest);
+    result is [all low halves; all high halves]."""
+    n = los.shape[0]
+    rows = np.arange(n)
+    ax = np.argmax(his - los, axis=1)
+    mid = 0.5 * (los[rows, ax] + his[rows, ax])
+    low_hi = his.copy()
+    low_hi[rows, ax] = mid
+    high_lo = los.copy()
+    high_lo[rows, ax] = mid
+    return np.concatenate([los, high_lo]), np.concatenate([low_hi, his])
+
+
+def face_centres(los, his):
+    """spatial.py:202-211: (n, 2d, d) face-centre points."""
+    n, d = los.shape
+    c = (los + his) / 2.0
+    h = (his - los) / 2.0
+    pts = np.repeat(c[:, None, :], 2 * d, axis=1)
+    for i in range(d):
+        pts[:, 2 * i, i] = c[:, i] - h[:, i]
+        pts[:, 2 * i + 1, i] = c[:, i] + h[:, i]
+    return pts
+
+
+def tree_levels(net, lo, hi, policy="affine-fixed", delta=0.001, max_depth=None):
+    """Breadth-first k-d tree (spatial.py:214-289) as flat per-level arrays.
+
+    Level k+1 holds the low children of level k's split nodes (in order) then
+    the high children, exactly like the reference's level arrays.  Returns a
+    list of dicts: lo, hi (n, d) FP64; label int8 (+1/-1/0); split bool;
+    face int8 (+1/-1 annotation on tiny UNKNOWN leaves, 0 = none);
+    parent int64 (index into the previous level, -1 for the root).
+    """
+    net = as_oracle_net(net)
+    lo = np.asarray(lo, dtype=np.float64)
+    hi = np.asarray(hi, dtype=np.float64)
+    if max_depth is not None and max_depth > 60:
+        raise ValueError("DepthOverflow")
+    d = lo.shape[0]
+    stop = delta / np.sqrt(d)
+    los, his = lo[None, :].copy(), hi[None, :].copy()
+    parent = np.array([-1], dtype=np.int64)
+    levels = []
+    depth = 0
+    while True:
+        blo, bhi = bound_aabbs(net, los, his, policy)
+        label = sign_labels(blo, bhi)
+        unknown = label == 0
+        face = np.zeros(len(los), dtype=np.int8)
+        if max_depth is not None:
+            split = unknown & (depth < max_depth)
+        else:
+            small = unknown & (np.max(his - los, axis=1) < stop)
+            split = unknown & ~small
+            if small.any():
+                idx = np.flatnonzero(small)
+                vals = eval_points(net, face_centres(los[idx], his[idx]).reshape(-1, d))
+                vals = vals.reshape(len(idx), -1)
+                neg = np.any(vals < 0.0, axis=1)
+                pos = np.any(vals >= 0.0, axis=1)
+                face[idx] = np.where(neg & pos, 0, np.where(neg, -1, 1))
+        levels.append(
+            dict(lo=los, hi=his, label=label, split=split, face=face, parent=parent,
+                 bound_lo=blo, bound_hi=bhi)
+        )
+        if not split.any():
+            break
+        sidx = np.flatnonzero(split)
+        los, his = split_widest(los[split], his[split])
+        parent = np.concatenate([sidx, sidx])
+        depth += 1
+    return levels
+
+
+def node_keys(levels):
+    """Path keys per level: root = 1, low child = 2k, high child = 2k + 1."""
+    keys = [np.array([1], dtype=np.int64)]
+    for lv in levels[1:]:
+        k = len(lv["parent"]) // 2
+        pk = keys[-1][lv["parent"]]
+        bit = np.concatenate([np.zeros(k, np.int64), np.ones(k, np.int64)])
+        keys.append(pk * 2 + bit)
+    return keys
+
+
+# ---------------------------------------------------------------------------
+# Range-marching ray caster (rays.py:88-138) and pinhole camera (camera.py)
+
+
+@dataclass(frozen=True)
+class MarchParams:
+    """rays.py:48-71 defaults."""
+
+    t_max: float = 10.0
+    sigma0: float | None = None
+    eta_plus: float = 1.5
+    eta_minus: float = 0.5
+    delta: float = 0.001
+    safety: float = 0.98
+
+    @property
+    def s0(self):
+        return self.t_max / 10.0 if self.sigma0 is None else self.sigma0
+
+
+def march(net, origins, dirs, params=MarchParams(), policy="affine-fixed",
+          t_init=None, sigma_init=None):
+    """Lock-step adaptive range-march; returns (hit bool, t FP64, steps)."""
+    net = as_oracle_net(net)
+    origins = np.asarray(origins, dtype=np.float64)
+    dirs = np.asarray(dirs, dtype=np.float64)
+    n = len(origins)
+    t = np.zeros(n) if t_init is None else np.array(t_init, dtype=np.float64)
+    sig = np.full(n, params.s0) if sigma_init is None else np.array(sigma_init, dtype=np.float64)
+    steps = np.zeros(n)
+    hit = np.zeros(n, dtype=bool)
+    t_hit = np.full(n, np.inf)
+    if n == 0:
+        return hit, t_hit, steps
+    f0 = eval_points(net, origins)
+    surf = f0 == 0.0
+    hit[surf] = True
+    t_hit[surf] = 0.0
+    inside0 = f0 < 0.0
+    live = np.flatnonzero(~surf & (t < params.t_max))
+    while live.size:
+        p, r, tl = origins[live], dirs[live], t[live]
+        probe = eval_points(net, p + (tl + params.delta)[:, None] * r)
+        steps[live] += 1.0
+        crossed = (probe < 0.0) != inside0[live]
+        hit[live[crossed]] = True
+        t_hit[live[crossed]] = t[live[crossed]]
+        keep = ~crossed
+        live = live[keep]
+        if live.size == 0:
+            break
+        p, r, tl = p[keep], r[keep], tl[keep]
+        sl = sig[live]
+        centre = p + (tl + sl / 2.0)[:, None] * r
+        axis = ((sl / 2.0)[:, None] * r)[:, None, :]
+        blo, bhi = bound_batch(net, centre, axis, policy)
+        ok = (blo > 0.0) | (bhi < 0.0)
+        sig[live] = np.where(ok, sl * params.eta_plus, sl * params.eta_minus)
+        t[live] = tl + np.maximum(params.safety * np.where(ok, sl, 0.0), params.delta)
+        live = live[t[live] < params.t_max]
+    return hit, t_hit, steps
+
+
+def camera_frame(position, look_at, up):
+    """camera.py:39-49: (forward, right, true_up)."""
+    pos = np.asarray(position, dtype=np.float64)
+    fwd = np.asarray(look_at, dtype=np.float64) - pos
+    fwd = fwd / np.linalg.norm(fwd)
+    right = np.cross(fwd, np.asarray(up, dtype=np.float64))
+    right = right / np.linalg.norm(right)
+    return fwd, right, np.cross(right, fwd)
+
+
+def pixel_dirs(position, look_at, up, vertical_fov, width, height):
+    """camera.py:68-92: unit directions (height, width, 3), row 0 on top."""
+    fwd, right, tup = camera_frame(position, look_at, up)
+    half_h = math.tan(math.radians(vertical_fov) / 2.0)
+    half_w = half_h * width / height
+    u = ((np.arange(width, dtype=np.float64) + 0.5) / width * 2.0 - 1.0) * half_w
+    v = (1.0 - (np.arange(height, dtype=np.float64) + 0.5) / height * 2.0) * half_h
+    d = fwd[None, None, :] + u[None, :, None] * right[None, None, :] + v[:, None, None] * tup[None, None, :]
+    return d / np.linalg.norm(d, axis=2, keepdims=True)
+
+
+# ---------------------------------------------------------------------------
+# Marching-cubes tables (mc_tables.py:24-105): generated, not the classic table
+
+MC_CORNERS = np.array(
+    [[0, 0, 0], [1, 0, 0], [1, 1, 0], [0, 1, 0], [0, 0, 1], [1, 0, 1], [1, 1, 1], [0, 1, 1]],
+    dtype=np.int64,
+)
+MC_EDGES = ((0, 1), (1, 2), (2, 3), (3, 0), (4, 5), (5, 6), (6, 7), (7, 4),
+            (0, 4), (1, 5), (2, 6), (3, 7))
+# faces as corner cycles, counter-clockwise seen from outside
+MC_FACES = ((0, 3, 2, 1), (4, 5, 6, 7), (0, 1, 5, 4), (3, 7, 6, 2), (0, 4, 7, 3), (1, 2, 6, 5))
+
+
+def _edge_of(a, b):
+    for e, (p, q) in enumerate(MC_EDGES):
+        if (p, q) == (a, b) or (q, p) == (a, b):
+            return e
+    raise KeyError((a, b))
+
+
+def _face_links(inside, cyc):
+    """Directed isoline links (exit edge -> entry edge) on one face; an
+    ambiguous face isolates each inside corner (mc_tables.py:54-69)."""
+    sgn = [inside[c] for c in cyc]
+    side = [_edge_of(cyc[i], cyc[(i + 1) % 4]) for i in range(4)]
+    outs = [i for i in range(4) if sgn[i] and not sgn[(i + 1) % 4]]
+    ins = [i for i in range(4) if not sgn[i] and sgn[(i + 1) % 4]]
+    if not outs:
+        return []
+    if len(outs) == 1:
+        return [(side[outs[0]], side[ins[0]])]
+    return [(side[p], side[(p - 1) % 4]) for p in range(4) if sgn[p]]
+
+
+def _case_triangles(case):
+    inside = [bool((case >> i) & 1) for i in range(8)]
+    succ = {}
+    for cyc in MC_FACES:
+        for a, b in _face_links(inside, cyc):
+            succ[a] = b
+    out = []
+    todo = set(succ)
+    while todo:
+        first = min(todo)
+        ring = [first]
+        todo.discard(first)
+        cur = succ[first]
+        while cur != first:
+            ring.append(cur)
+            todo.discard(cur)
+            cur = succ[cur]
+        for i in range(1, len(ring) - 1):
+            out.append((ring[0], ring[i + 1], ring[i]))  # reversed fan
+    return tuple(out)
+
+
+MC_TRIANGLES = tuple(_case_triangles(c) for c in range(256))
+
+
+# ---------------------------------------------------------------------------
+# Hierarchical marching cubes (meshing.py:23-169)
+
+
+def grid_axis(lo, hi, n_cells):
+    """np.linspace(lo, hi, n+1): i*step + lo, last entry forced to hi."""
+    return np.linspace(lo, hi, n_cells + 1)
+
+
+def edge_key(ia, ib, n_pts):
+    """Global grid edge id: (linear index of the lower corner) * 3 + axis."""
+    a = np.asarray(ia)
+    b = np.asarray(ib)
+    low = np.minimum(a, b)
+    ax = int(np.flatnonzero(a != b)[0])
+    lin = (int(low[0]) * n_pts + int(low[1])) * n_pts + int(low[2])
+    return lin * 3 + ax
+
+
+class _Builder:
+    """Edge-keyed vertex dedup (meshing.py:29-66)."""
+
+    def __init__(self, coords):
+        self.coords = coords
+        self.n_pts = len(coords[0])
+        self.ids = {}
+        self.verts = []
+        self.keys = []
+        self.tris = []
+
+    def _vid(self, cell, e, vals):
+        a, b = MC_EDGES[e]
+        ia = tuple(int(cell[k] + MC_CORNERS[a][k]) for k in range(3))
+        ib = tuple(int(cell[k] + MC_CORNERS[b][k]) for k in range(3))
+        key = (ia, ib) if ia <= ib else (ib, ia)
+        v = self.ids.get(key)
+        if v is None:
+            fa, fb = vals[a], vals[b]
+            t = (0.0 - fa) / (fb - fa)
+            pa = np.array([self.coords[k][ia[k]] for k in range(3)])
+            pb = np.array([self.coords[k][ib[k]] for k in range(3)])
+            v = len(self.verts)
+            self.verts.append(pa + t * (pb - pa))
+            self.keys.append(edge_key(ia, ib, self.n_pts))
+            self.ids[key] = v
+        return v
+
+    def cell(self, cell, vals):
+        case = sum(1 << c for c in range(8) if vals[c] < 0.0)
+        for tri in MC_TRIANGLES[case]:
+            self.tris.append(tuple(self._vid(cell, e, vals) for e in tri))
+
+    def result(self):
+        if not self.verts:
+            return np.zeros((0, 3)), np.zeros((0, 3), np.int64), np.zeros(0, np.int64)
+        return np.stack(self.verts), np.array(self.tris, np.int64), np.array(self.keys, np.int64)
+
+
+def _polygonize(builder, vals, origin):
+    neg = vals < 0.0
+    nx, ny, nz = (s - 1 for s in vals.shape)
+    case = np.zeros((nx, ny, nz), dtype=np.int32)
+    for c, (dx, dy, dz) in enumerate(MC_CORNERS):
+        case |= neg[dx : dx + nx, dy : dy + ny, dz : dz + nz].astype(np.int32) << c
+    for i, j, k in np.argwhere((case != 0) & (case != 255)):
+        cv = [vals[i + dx, j + dy, k + dz] for dx, dy, dz in MC_CORNERS]
+        builder.cell((origin[0] + i, origin[1] + j, origin[2] + k), cv)
+
+
+def _grid_values(net, coords, rng):
+    (i0, i1), (j0, j1), (k0, k1) = rng
+    g = np.stack(
+        np.meshgrid(coords[0][i0 : i1 + 1], coords[1][j0 : j1 + 1], coords[2][k0 : k1 + 1],
+                    indexing="ij"),
+        axis=-1,
+    )
+    return eval_points(net, g.reshape(-1, 3)).reshape(g.shape[:3])
+
+
+def mesh_blocks(net, lo, hi, m, dense_levels=3, policy="affine-fixed"):
+    """Surviving index-range blocks of the hierarchical prune (meshing.py:134-163)."""
+    net = as_oracle_net(net)
+    n = 2 ** m
+    coords = [grid_axis(lo[k], hi[k], n) for k in range(3)]
+
+    def survivors(blocks):
+        if not blocks:
+            return []
+        b = np.asarray(blocks, dtype=np.int64)  # (nb, 3, 2)
+        wlo = np.stack([coords[k][b[:, k, 0]] for k in range(3)], axis=1)
+        whi = np.stack([coords[k][b[:, k, 1]] for k in range(3)], axis=1)
+        axes = _cube_axes(wlo, whi)
+        blo, bhi = bound_batch(net, (wlo + whi) / 2.0, axes, policy)
+        return [blk for blk, a, z in zip(blocks, blo, bhi) if a <= 0.0 <= z]
+
+    blocks = [((0, n), (0, n), (0, n))]
+    for _ in range(3 * (m - dense_levels)):
+        blocks = survivors(blocks)
+        nxt = []
+        for blk in blocks:
+            size = [blk[k][1] - blk[k][0] for k in range(3)]
+            ax = int(np.argmax(size))
+            cut = blk[ax][0] + size[ax] // 2
+            a = list(blk)
+            b = list(blk)
+            a[ax] = (blk[ax][0], cut)
+            b[ax] = (cut, blk[ax][1])
+            nxt.extend((tuple(a), tuple(b)))
+        blocks = nxt
+    return survivors(blocks), coords
+
+
+def mesh_extract(net, lo, hi, m, dense_levels=3, policy="affine-fixed"):
+    """Hierarchical extraction; returns (vertices, triangles, vertex_edge_keys)."""
+    net = as_oracle_net(net)
+    blocks, coords = mesh_blocks(net, lo, hi, m, dense_levels, policy)
+    builder = _Builder(coords)
+    for blk in blocks:
+        vals = _grid_values(net, coords, blk)
+        _polygonize(builder, vals, (blk[0][0], blk[1][0], blk[2][0]))
+    return builder.result()
+
+
+def mesh_extract_dense(net, lo, hi, m):
+    """meshing.py:100-108 brute force."""
+    net = as_oracle_net(net)
+    n = 2 ** m
+    coords = [grid_axis(lo[k], hi[k], n) for k in range(3)]
+    builder = _Builder(coords)
+    _polygonize(builder, _grid_values(net, coords, ((0, n), (0, n), (0, n))), (0, 0, 0))
+    return builder.result()
+
+
+def triangle_key_set(triangles, vertex_keys):
+    """Triangles as edge-key triples, rotated so the smallest key leads
+    (winding preserved); a multiset-free canonical form for comparisons."""
+    out = []
+    for t in np.asarray(triangles):
+        k = [int(vertex_keys[i]) for i in t]
+        r = k.index(min(k))
+        out.append(tuple(k[r:] + k[:r]))
+    return sorted(out)

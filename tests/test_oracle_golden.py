@@ -1,0 +1,127 @@
+"""Pin the CPU oracle to vectors produced by the unmodified reference
+(tests/golden/make_golden.py).  CPU only."""
+
+import numpy as np
+import pytest
+
+from oracle import spelunk_oracle as orc
+from tests.conftest import golden_group
+
+POLICIES = ["interval", "affine-fixed", "affine-full", "affine-truncate:8", "affine-truncate:16"]
+
+
+def test_rules_match_reference(golden):
+    lo, hi = golden["rules/lo"], golden["rules/hi"]
+    for kind in ("relu", "elu", "sin", "tanh"):
+        with np.errstate(all="ignore"):
+            a, b, g = orc.LINEAR_RULES[kind](lo, hi)
+            il, ih = orc.IMAGE_RULES[kind](lo, hi)
+        np.testing.assert_array_equal(a, golden[f"rules/{kind}/alpha"])
+        np.testing.assert_array_equal(b, golden[f"rules/{kind}/beta"])
+        np.testing.assert_array_equal(g, golden[f"rules/{kind}/gamma"])
+        np.testing.assert_array_equal(il, golden[f"rules/{kind}/ilo"])
+        np.testing.assert_array_equal(ih, golden[f"rules/{kind}/ihi"])
+
+
+def test_point_eval_bit_exact(golden, net_paths):
+    for name, path in net_paths.items():
+        net = orc.load_net(path)
+        got = orc.eval_points(net, golden[f"eval/{name}/x"])
+        np.testing.assert_array_equal(got, golden[f"eval/{name}/f"])
+
+
+@pytest.mark.parametrize("policy", POLICIES)
+def test_bounds_match_reference(golden, net_paths, policy):
+    for name, path in net_paths.items():
+        net = orc.load_net(path)
+        c = golden[f"bounds/{name}/centers"]
+        a = golden[f"bounds/{name}/axes"]
+        lo, hi = orc.bound_batch(net, c, a, policy)
+        want_lo = golden[f"bounds/{name}/{policy}/lo"]
+        want_hi = golden[f"bounds/{name}/{policy}/hi"]
+        scale = np.maximum(1.0, np.maximum(np.abs(want_lo), np.abs(want_hi)))
+        assert np.max(np.abs(lo - want_lo) / scale) <= 1e-12, name
+        assert np.max(np.abs(hi - want_hi) / scale) <= 1e-12, name
+
+
+TREES = {
+    "box_d8_fixed": ("box", dict(policy="affine-fixed", max_depth=8)),
+    "box_conv_full": ("box", dict(policy="affine-full", delta=0.1)),
+    "relu_sdf_d10_fixed": ("relu_sdf", dict(policy="affine-fixed", max_depth=10)),
+    "relu_sdf_d7_interval": ("relu_sdf", dict(policy="interval", max_depth=7)),
+    "relu4x32_d9_fixed": ("relu4x32", dict(policy="affine-fixed", max_depth=9)),
+    "elu_sdf_conv_trunc": ("elu_sdf", dict(policy="affine-truncate:8", delta=0.15)),
+}
+
+
+def golden_tree(golden, tag):
+    g = golden_group(golden, f"tree/{tag}")
+    n = 1 + max(int(k.split("/")[0]) for k in g)
+    return [{f: g[f"{i}/{f}"] for f in ("keys", "lo", "hi", "sign", "face")} for i in range(n)]
+
+
+@pytest.mark.parametrize("tag", sorted(TREES))
+def test_tree_matches_reference(golden, net_paths, tag):
+    netname, kw = TREES[tag]
+    levels = orc.tree_levels(orc.load_net(net_paths[netname]), -np.ones(3), np.ones(3), **kw)
+    keys = orc.node_keys(levels)
+    want = golden_tree(golden, tag)
+    assert len(levels) == len(want)
+    for lv, k, w in zip(levels, keys, want):
+        order = np.argsort(k)
+        worder = np.argsort(w["keys"])
+        np.testing.assert_array_equal(k[order], w["keys"][worder])
+        np.testing.assert_array_equal(lv["label"][order], w["sign"][worder])
+        np.testing.assert_array_equal(lv["face"][order], w["face"][worder])
+        np.testing.assert_array_equal(lv["lo"][order], w["lo"][worder])
+        np.testing.assert_array_equal(lv["hi"][order], w["hi"][worder])
+
+
+@pytest.mark.parametrize("netname", ["box", "relu_sdf", "sin3x48"])
+@pytest.mark.parametrize("policy", ["affine-fixed", "interval", "affine-truncate:8"])
+def test_march_matches_reference(golden, net_paths, netname, policy):
+    net = orc.load_net(net_paths[netname])
+    p = orc.MarchParams(t_max=4.0)
+    hit, t, steps = orc.march(net, golden[f"rays/{netname}/origins"], golden[f"rays/{netname}/dirs"], p, policy)
+    np.testing.assert_array_equal(hit, golden[f"rays/{netname}/{policy}/hit"])
+    np.testing.assert_array_equal(t, golden[f"rays/{netname}/{policy}/t"])
+    np.testing.assert_array_equal(steps, golden[f"rays/{netname}/{policy}/steps"])
+
+
+def test_camera_and_march(golden, net_paths):
+    dirs = orc.pixel_dirs([1.6, 1.2, 2.0], [0, 0, 0], [0, 1, 0], 40.0, 24, 16)
+    np.testing.assert_array_equal(dirs, golden["camera/dirs"])
+    d = dirs.reshape(-1, 3)
+    o = np.broadcast_to(np.array([1.6, 1.2, 2.0]), d.shape)
+    hit, t, steps = orc.march(orc.load_net(net_paths["relu_sdf"]), o, d, orc.MarchParams(), "affine-fixed")
+    np.testing.assert_array_equal(hit, golden["camera/relu_sdf/hit"])
+    np.testing.assert_array_equal(t, golden["camera/relu_sdf/t"])
+    np.testing.assert_array_equal(steps, golden["camera/relu_sdf/steps"])
+
+
+def test_mc_tables(golden):
+    flat = [(c, *tri) for c in range(256) for tri in orc.MC_TRIANGLES[c]]
+    np.testing.assert_array_equal(np.array(flat), golden["mc/tri_table"])
+    assert len(flat) == 820
+
+
+MESHES = {
+    "offset_box_m5_fixed": ("offset_box", 5, "affine-fixed"),
+    "offset_box_m5_full": ("offset_box", 5, "affine-full"),
+    "relu_sdf_m5_fixed": ("relu_sdf", 5, "affine-fixed"),
+    "elu_sdf_m5_fixed": ("elu_sdf", 5, "affine-fixed"),
+}
+
+
+@pytest.mark.parametrize("tag", sorted(MESHES))
+def test_mesh_matches_reference(golden, net_paths, tag):
+    netname, m, pol = MESHES[tag]
+    v, t, _ = orc.mesh_extract(orc.load_net(net_paths[netname]), -np.ones(3), np.ones(3), m, 3, pol)
+    np.testing.assert_array_equal(v, golden[f"mesh/{tag}/vertices"])
+    np.testing.assert_array_equal(t, golden[f"mesh/{tag}/triangles"])
+
+
+def test_dense_mesh_matches_reference(golden, net_paths):
+    v, t, _ = orc.mesh_extract_dense(orc.load_net(net_paths["relu_sdf"]), -np.ones(3), np.ones(3), 5)
+    np.testing.assert_array_equal(v, golden["mesh/relu_sdf_m5_dense/vertices"])
+    np.testing.assert_array_equal(t, golden["mesh/relu_sdf_m5_dense/triangles"])
