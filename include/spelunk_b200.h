@@ -1,0 +1,152 @@
+/*
+ * spelunk_b200 -- C ABI of the B200 (sm_100a) range-analysis hot path.
+ *
+ * Drop-in boundary for the reference package `spelunk` (arXiv 2202.02444
+ * reference at /root/reference/pkg/src/spelunk).  The reference has no FFI;
+ * its de-facto operator boundary is a handful of Python functions, and each
+ * entry point below replaces one of them (file:line in the reference):
+ *
+ *   spk_net_create / spk_net_destroy  <- NetworkSpec / DenseLayer /
+ *                                        ActivationKind (network.py:29-116),
+ *                                        load_network (network.py:236-287)
+ *   spk_bound_batch                   <- range_bound_batch (range_core.py:547-622)
+ *                                        and interval_forward_batch (:625-642)
+ *   spk_bound_aabb                    <- _classify_corners (spatial.py:172-186)
+ *   spk_eval_batch                    <- eval_batch (network.py:163-183)
+ *   spk_bound_batch_host              <- range_bound_batch called with host
+ *                                        (NumPy) arrays, copies included
+ *   spk_tree_build                    <- build_spatial_tree (spatial.py:214-289)
+ *   spk_march                         <- _march_arrays (rays.py:88-138)
+ *   spk_mesh_blocks / spk_mesh_cells  <- extract_mesh (meshing.py:111-169)
+ *
+ * Conventions: plain pointers and sizes, no torch types.  "Device" pointers
+ * are CUDA device (or managed) memory owned by the caller; calls are
+ * asynchronous on `stream` (a cudaStream_t passed as void*, NULL = legacy
+ * default stream) and keep no pointer after returning.  FP64 in / FP64 out,
+ * like the reference; `precision` selects the arithmetic the kernels run in
+ * (SPK_FP32: FP32 FFMA with directed rounding on the error terms -- sound;
+ * SPK_FP64: same algorithm in FP64).  Every function returns an SPK_* status;
+ * spk_last_error() gives a thread-local message.  Handles are immutable after
+ * creation and may be shared across threads; all entry points are reentrant.
+ */
+#ifndef SPELUNK_B200_H
+#define SPELUNK_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes; the Python layer maps them onto the reference's exception
+ * taxonomy (errors.py:4-73) */
+enum {
+  SPK_OK = 0,
+  SPK_ERR_DIMENSION = 1,         /* DimensionMismatch */
+  SPK_ERR_UNSUPPORTED_ACT = 2,   /* UnsupportedActivation */
+  SPK_ERR_INVALID_PARAMETER = 3, /* InvalidParameter */
+  SPK_ERR_DEPTH_OVERFLOW = 4,    /* DepthOverflow */
+  SPK_ERR_CUDA = 5,              /* SpelunkError (CUDA runtime failure) */
+  SPK_ERR_UNSUPPORTED_SHAPE = 6, /* SpelunkError (layer width / s beyond the compiled kernels) */
+  SPK_ERR_OUT_OF_MEMORY = 7      /* SpelunkError */
+};
+
+/* network op codes (ActivationKind, network.py:29-34) */
+enum {
+  SPK_OP_DENSE = 0,
+  SPK_OP_RELU = 1,
+  SPK_OP_ELU = 2,
+  SPK_OP_SIN = 3,
+  SPK_OP_TANH = 4,
+  SPK_OP_IDENTITY = 5
+};
+
+/* condensation policies (range_core.py:104-145) */
+enum {
+  SPK_POLICY_INTERVAL = 0,
+  SPK_POLICY_AFFINE_FIXED = 1,
+  SPK_POLICY_AFFINE_FULL = 2,
+  SPK_POLICY_AFFINE_TRUNCATE = 3
+};
+
+enum { SPK_FP32 = 0, SPK_FP64 = 1 };
+
+/* sign classes (range_core.py:42-45, 504-509) */
+enum { SPK_NEGATIVE = -1, SPK_UNKNOWN = 0, SPK_POSITIVE = 1 };
+
+typedef struct spk_net spk_net;
+typedef struct spk_tree spk_tree;
+
+const char* spk_last_error(void);
+int spk_version(void);
+/* number of SMs of the current device, or -1 */
+int spk_device_sm_count(void);
+
+/* Upload a network once.  op_kind[i] is SPK_OP_*; for dense ops
+ * op_out_dim[i] is the output width and `params` holds, for every dense op
+ * in order, W (out x in, row-major: W[i][j] multiplies input j into output
+ * i, network.py:38-66) followed by b (out).  Validation matches
+ * NetworkSpec.__post_init__ (network.py:86-107). */
+int spk_net_create(int input_dim, int n_ops, const int* op_kind, const int* op_out_dim,
+                   const double* params, int64_t n_params, int device, spk_net** out);
+int spk_net_destroy(spk_net* net);
+/* widest layer, number of dense layers, and sum_l m_in*m_out (FLOP model) */
+int spk_net_info(const spk_net* net, int* max_width, int* n_dense, int64_t* macs);
+
+/* Bound the network over n oriented boxes (device pointers).
+ * centers: n x d; axes: n x s x d (all-zero rows are padding,
+ * range_core.py:550-551).  lo/hi: n doubles; cls: n int8 (SPK_POSITIVE /
+ * SPK_NEGATIVE / SPK_UNKNOWN) or NULL.  policy SPK_POLICY_*; n_keep for
+ * truncate (>=1). */
+int spk_bound_batch(const spk_net* net, int policy, int n_keep, int precision, int64_t n,
+                    int s, const double* centers, const double* axes, double* lo, double* hi,
+                    int8_t* cls, void* stream);
+
+/* Same for axis-aligned boxes given by corners (n x d each): centre
+ * (lo+hi)/2 and half-extents (hi-lo)/2 in FP64 exactly as
+ * spatial.py:181-183 does. */
+int spk_bound_aabb(const spk_net* net, int policy, int n_keep, int precision, int64_t n,
+                   const double* box_lo, const double* box_hi, double* lo, double* hi,
+                   int8_t* cls, void* stream);
+
+/* C5 sweep: n cubes generated on device from (seed, index): centres
+ * uniform in [-1,1]^d (splitmix64 stream), half-extent
+ * `half` on every axis.  first_index offsets the stream (for sharding). */
+int spk_bound_random_cubes(const spk_net* net, int policy, int n_keep, int precision,
+                           int64_t n, int64_t first_index, uint64_t seed, double half,
+                           double* lo, double* hi, int8_t* cls, void* stream);
+
+/* Point evaluation (device pointers): xs n x d -> out n. */
+int spk_eval_batch(const spk_net* net, int precision, int64_t n, const double* xs,
+                   double* out, void* stream);
+
+/* Host-pointer variant of spk_bound_batch: pageable or pinned host arrays;
+ * the library stages chunks through pinned buffers on two streams so the
+ * copies overlap the kernels, and returns when lo/hi/cls are written. */
+int spk_bound_batch_host(const spk_net* net, int policy, int n_keep, int precision, int64_t n,
+                         int s, const double* centers, const double* axes, double* lo,
+                         double* hi, int8_t* cls);
+
+/* K5: breadth-first k-d tree (build_spatial_tree, spatial.py:214-289).
+ * root_lo/root_hi: host arrays of d doubles.  max_depth >= 0: fixed-depth
+ * mode (UNKNOWN nodes split while depth < max_depth, <= 60 else
+ * SPK_ERR_DEPTH_OVERFLOW); max_depth < 0: convergence mode, UNKNOWN nodes
+ * split until their widest extent drops below delta/sqrt(d) and such leaves
+ * get the face-centre sign annotation.  The result lives in device memory,
+ * one array set per level: level k+1 = [low children ; high children] of
+ * level k's split nodes, in order (the reference's layout). */
+int spk_tree_build(const spk_net* net, int policy, int n_keep, int precision, const double* root_lo,
+                   const double* root_hi, int max_depth, double delta, void* stream, spk_tree** out);
+int spk_tree_destroy(spk_tree* tree);
+int spk_tree_info(const spk_tree* tree, int* n_levels, int64_t* n_nodes, int64_t* bound_evals);
+/* device pointers of one level (valid until spk_tree_destroy): AABB corners
+ * (n x d), the bound, the sign label (+1/-1/0), the face-sign annotation
+ * (+1/-1, 0 = none) and the parent index into the previous level (-1). */
+int spk_tree_level(const spk_tree* tree, int level, int64_t* n, const double** lo, const double** hi,
+                   const double** bound_lo, const double** bound_hi, const int8_t** label,
+                   const int8_t** face, const int64_t** parent);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPELUNK_B200_H */

@@ -1,0 +1,44 @@
+"""paper_2202_02444_b200 -- B200-native (sm_100a) range analysis of neural
+implicit MLPs: the hot path of arXiv 2202.02444 ("Spelunking the Deep").
+
+Drop-in for the reference package `spelunk`'s bound-evaluation,
+spatial-hierarchy, ray-cast and mesh-extraction entry points; every compute
+call goes through the in-tree CUDA library `_spk.so` (include/spelunk_b200.h).
+There is no CPU fallback.
+"""
+
+from . import errors
+from .network import (
+    ActivationKind,
+    DenseLayer,
+    NetworkSpec,
+    build_box_oracle,
+    box_sdf,
+    count_evals,
+    eval_batch,
+    eval_scalar,
+    load_network,
+    save_network,
+)
+from .range_core import (
+    AFFINE_FIXED,
+    AFFINE_FULL,
+    INTERVAL_ONLY,
+    CondensationPolicy,
+    Interval,
+    PolicyKind,
+    QueryBox,
+    SignClass,
+    affine_truncate,
+    bound_aabb,
+    bound_random_cubes,
+    classify,
+    interval_forward,
+    interval_forward_batch,
+    parse_policy,
+    range_bound,
+    range_bound_batch,
+    sign_classes,
+)
+
+__version__ = "0.1.0"

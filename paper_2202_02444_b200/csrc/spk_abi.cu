@@ -1,0 +1,396 @@
+// C-ABI implementation (include/spelunk_b200.h): network upload, argument
+// validation mirroring the reference's exceptions, dispatch to the fused
+// kernels, and the host-pointer pipelined path.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "spk_kernels.cuh"
+#include "spk_abi_internal.h"
+
+namespace spk {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(SPK_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+int sm_count_for(int device) {
+  static std::mutex mu;
+  static std::vector<int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  if ((int)cache.size() <= device) cache.resize(device + 1, 0);
+  if (cache[device] == 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+    cache[device] = v;
+  }
+  return cache[device];
+}
+
+DeviceGuard::DeviceGuard(int dev) {
+  cudaGetDevice(&prev_);
+  if (prev_ != dev) cudaSetDevice(dev);
+  dev_ = dev;
+}
+DeviceGuard::~DeviceGuard() {
+  if (prev_ != dev_) cudaSetDevice(prev_);
+}
+
+static const int kMmaxChoices[] = {32, 64, 128, 256, 512};
+
+template <typename T>
+static int kt_for(int mmax) {
+  switch (mmax) {
+    case 32: return KTOf<T, 32>::KT;
+    case 64: return KTOf<T, 64>::KT;
+    case 128: return KTOf<T, 128>::KT;
+    case 256: return KTOf<T, 256>::KT;
+    default: return KTOf<T, 512>::KT;
+  }
+}
+
+template <typename T>
+static int sub_for(int mmax) {
+  switch (mmax) {
+    case 32: return KTOf<T, 32>::SUB;
+    case 64: return KTOf<T, 64>::SUB;
+    case 128: return KTOf<T, 128>::SUB;
+    case 256: return KTOf<T, 256>::SUB;
+    default: return KTOf<T, 512>::SUB;
+  }
+}
+
+template <typename T>
+static T round_up_to(double x) {
+  T t = (T)x;
+  if ((double)t < x) t = std::nextafter(t, (T)INFINITY);
+  return t;
+}
+
+// Build the device program for one precision (lazily, once per net).
+template <typename T>
+int build_device_net(spk_net* net, DevNet<T>& dn) {
+  const bool fp32 = sizeof(T) == 4;
+  const int mmax = net->mmax;
+  const int KT = kt_for<T>(mmax);
+  const int tile = KT * mmax;
+  NetDev<T> nd;
+  std::memset(&nd, 0, sizeof(nd));
+  nd.d = net->input_dim;
+  nd.n_pre = (int)net->pre_acts.size();
+  for (int i = 0; i < nd.n_pre; ++i) nd.pre_act[i] = net->pre_acts[i];
+  nd.n_layers = (int)net->layers.size();
+
+  std::vector<T> tiles;
+  std::vector<T> small;   // narrow W, biases, bias errors (offsets patched later)
+  struct Offs { size_t w = 0, b = 0, be = 0; };
+  std::vector<Offs> offs(net->layers.size());
+  std::vector<double> gam(net->layers.size());
+  for (size_t l = 0; l < net->layers.size(); ++l) {
+    const HostLayer& L = net->layers[l];
+    const bool narrow = L.m_out <= NARROW_MAX;
+    int n_eff;
+    if (narrow) {
+      n_eff = (L.m_in + 31) / 32 + 6;
+    } else {
+      const int nt = (L.m_in + KT - 1) / KT;
+      const int sub = sub_for<T>(mmax);
+      n_eff = std::min(sub, L.m_in) + (L.m_in + sub - 1) / sub + 1;
+      for (int t = 0; t < nt; ++t) {
+        for (int kk = 0; kk < KT; ++kk) {
+          const int k = t * KT + kk;
+          for (int i = 0; i < mmax; ++i) {
+            T v = T(0);
+            if (k < L.m_in && i < L.m_out) v = (T)L.W[(size_t)i * L.m_in + k];
+            tiles.push_back(v);
+          }
+        }
+      }
+    }
+    // + u for FP32: W and b are rounded from FP64 to T, |dW| <= u|W|, so the
+    // certified function is the reference's FP64 network.
+    gam[l] = gamma_n_host(n_eff, fp32) + (fp32 ? 5.9604644775390625e-8 * (1.0 + 1e-6) : 0.0);
+    if (narrow) {
+      offs[l].w = small.size();
+      for (size_t q = 0; q < L.W.size(); ++q) small.push_back((T)L.W[q]);
+    }
+    offs[l].b = small.size();
+    for (int i = 0; i < L.m_out; ++i) small.push_back((T)L.b[i]);
+    offs[l].be = small.size();
+    for (int i = 0; i < L.m_out; ++i) {
+      // |b_i| enters the FMA chain exactly once; its share of the rounding
+      // budget plus an underflow guard, rounded up.
+      const double be = gam[l] * std::fabs((double)(T)L.b[i]) * (1.0 + 1e-6) +
+                        (fp32 ? 1e-37 : 1e-300) * (L.m_in + 2);
+      small.push_back(round_up_to<T>(be));
+    }
+    while (small.size() % 4) small.push_back(T(0));
+  }
+  T* d_tiles = nullptr;
+  T* d_small = nullptr;
+  cudaError_t e;
+  if (!tiles.empty()) {
+    e = cudaMalloc(&d_tiles, tiles.size() * sizeof(T));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(tiles)");
+    e = cudaMemcpy(d_tiles, tiles.data(), tiles.size() * sizeof(T), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(tiles)");
+  }
+  e = cudaMalloc(&d_small, std::max<size_t>(small.size(), 4) * sizeof(T));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(small)");
+  e = cudaMemcpy(d_small, small.data(), small.size() * sizeof(T), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(small)");
+
+  nd.wtiles = d_tiles;
+  nd.tiles_per_pass = (int)(tiles.size() / (size_t)tile);
+  nd.gamma_first = round_up_to<T>(gam.empty() ? 0.0 : gam[0]);
+  for (size_t l = 0; l < net->layers.size(); ++l) {
+    const HostLayer& L = net->layers[l];
+    LayerDev<T>& D = nd.L[l];
+    D.m_in = L.m_in;
+    D.m_out = L.m_out;
+    D.narrow = L.m_out <= NARROW_MAX;
+    D.ntiles = D.narrow ? 0 : (L.m_in + KT - 1) / KT;
+    D.n_act = (int)L.acts.size();
+    for (int a = 0; a < D.n_act; ++a) D.act[a] = L.acts[a];
+    D.w = D.narrow ? d_small + offs[l].w : nullptr;
+    D.bias = d_small + offs[l].b;
+    D.berr = d_small + offs[l].be;
+    D.gamma_next = (l + 1 < net->layers.size()) ? round_up_to<T>(gam[l + 1]) : T(0);
+  }
+  dn.nd = nd;
+  dn.tiles = d_tiles;
+  dn.small = d_small;
+  dn.ready = true;
+  return SPK_OK;
+}
+
+template <typename T>
+int get_dev(spk_net* net, const NetDev<T>** out) {
+  DevNet<T>& dn = net->dev<T>();
+  std::lock_guard<std::mutex> lk(net->mu);
+  if (!dn.ready) {
+    DeviceGuard g(net->device);
+    int rc = build_device_net<T>(net, dn);
+    if (rc != SPK_OK) return rc;
+  }
+  *out = &dn.nd;
+  return SPK_OK;
+}
+template int get_dev<float>(spk_net*, const NetDev<float>**);
+template int get_dev<double>(spk_net*, const NetDev<double>**);
+
+template <typename T>
+cudaError_t dispatch_any(int mmax, int mode, int S, const NetDev<T>& nd, const BoxInput& in,
+                         const BoundOutput& out, long long n, int sm, cudaStream_t st) {
+  switch (mmax) {
+    case 32: return dispatch_bound<T, 32>(mode, S, nd, in, out, n, sm, st);
+    case 64: return dispatch_bound<T, 64>(mode, S, nd, in, out, n, sm, st);
+    case 128: return dispatch_bound<T, 128>(mode, S, nd, in, out, n, sm, st);
+    case 256: return dispatch_bound<T, 256>(mode, S, nd, in, out, n, sm, st);
+    default: return dispatch_bound<T, 512>(mode, S, nd, in, out, n, sm, st);
+  }
+}
+
+int run_pass(const spk_net* cnet, int mode, int S, int precision, const BoxInput& in,
+             const BoundOutput& out, long long n, cudaStream_t st) {
+  spk_net* net = const_cast<spk_net*>(cnet);
+  DeviceGuard g(net->device);
+  const int sm = sm_count_for(net->device);
+  if (sm <= 0) return fail(SPK_ERR_CUDA, "no CUDA device");
+  cudaError_t e;
+  if (precision == SPK_FP64) {
+    const NetDev<double>* nd;
+    int rc = get_dev<double>(net, &nd);
+    if (rc) return rc;
+    e = dispatch_any<double>(net->mmax, mode, S, *nd, in, out, n, sm, st);
+  } else {
+    const NetDev<float>* nd;
+    int rc = get_dev<float>(net, &nd);
+    if (rc) return rc;
+    e = dispatch_any<float>(net->mmax, mode, S, *nd, in, out, n, sm, st);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return SPK_OK;
+}
+
+static int check_policy(int policy, int n_keep, int* mode) {
+  switch (policy) {
+    case SPK_POLICY_INTERVAL: *mode = MODE_INTERVAL; return SPK_OK;
+    case SPK_POLICY_AFFINE_FIXED: *mode = MODE_AFFINE; return SPK_OK;
+    case SPK_POLICY_AFFINE_TRUNCATE:
+      if (n_keep < 1) return fail(SPK_ERR_INVALID_PARAMETER, "affine-truncate requires n_keep >= 1");
+      *mode = -SPK_POLICY_AFFINE_TRUNCATE;
+      return SPK_OK;
+    case SPK_POLICY_AFFINE_FULL: *mode = -SPK_POLICY_AFFINE_FULL; return SPK_OK;
+    default: return fail(SPK_ERR_INVALID_PARAMETER, "unknown policy");
+  }
+}
+
+}  // namespace spk
+
+using namespace spk;
+
+extern "C" {
+
+const char* spk_last_error(void) { return g_last_error.c_str(); }
+int spk_version(void) { return 100; }
+
+int spk_device_sm_count(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  return sm_count_for(dev);
+}
+
+int spk_net_create(int input_dim, int n_ops, const int* op_kind, const int* op_out_dim,
+                   const double* params, int64_t n_params, int device, spk_net** out) {
+  if (!out) return fail(SPK_ERR_INVALID_PARAMETER, "null output handle");
+  *out = nullptr;
+  if (input_dim < 1) return fail(SPK_ERR_DIMENSION, "input_dim must be >= 1");
+  auto net = std::make_unique<spk_net>();
+  net->input_dim = input_dim;
+  net->device = device;
+  int dim = input_dim;
+  int64_t off = 0;
+  int max_w = input_dim;
+  for (int i = 0; i < n_ops; ++i) {
+    const int k = op_kind[i];
+    if (k == SPK_OP_DENSE) {
+      HostLayer L;
+      L.m_in = dim;
+      L.m_out = op_out_dim[i];
+      if (L.m_out < 1) return fail(SPK_ERR_DIMENSION, "dense layer needs >= 1 output");
+      const int64_t nw = (int64_t)L.m_in * L.m_out;
+      if (off + nw + L.m_out > n_params) return fail(SPK_ERR_DIMENSION, "params shorter than layer shapes");
+      L.W.assign(params + off, params + off + nw);
+      off += nw;
+      L.b.assign(params + off, params + off + L.m_out);
+      off += L.m_out;
+      for (double v : L.W) if (!std::isfinite(v)) return fail(SPK_ERR_INVALID_PARAMETER, "non-finite weight");
+      for (double v : L.b) if (!std::isfinite(v)) return fail(SPK_ERR_INVALID_PARAMETER, "non-finite bias");
+      dim = L.m_out;
+      max_w = std::max(max_w, std::max(L.m_in, L.m_out));
+      net->layers.push_back(std::move(L));
+    } else if (k >= SPK_OP_RELU && k <= SPK_OP_IDENTITY) {
+      auto& acts = net->layers.empty() ? net->pre_acts : net->layers.back().acts;
+      if ((int)acts.size() >= MAX_ACTS) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "too many consecutive activations");
+      acts.push_back(k);
+    } else {
+      return fail(SPK_ERR_UNSUPPORTED_ACT, "unknown op kind");
+    }
+  }
+  if (net->layers.empty()) return fail(SPK_ERR_DIMENSION, "network has no dense layers");
+  if (dim != 1) return fail(SPK_ERR_DIMENSION, "final layer must output 1 value");
+  if ((int)net->layers.size() > MAX_LAYERS) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "too many dense layers");
+  if (off != n_params) return fail(SPK_ERR_DIMENSION, "params longer than layer shapes");
+  net->mmax = 0;
+  for (int m : kMmaxChoices) {
+    if (m >= max_w) { net->mmax = m; break; }
+  }
+  if (net->mmax == 0) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "layer width above 512");
+  net->max_width = max_w;
+  for (auto& L : net->layers) net->macs += (int64_t)L.m_in * L.m_out;
+  *out = net.release();
+  return SPK_OK;
+}
+
+int spk_net_destroy(spk_net* net) {
+  if (!net) return SPK_OK;
+  {
+    DeviceGuard g(net->device);
+    if (net->f32.ready) { cudaFree(net->f32.tiles); cudaFree(net->f32.small); }
+    if (net->f64.ready) { cudaFree(net->f64.tiles); cudaFree(net->f64.small); }
+  }
+  delete net;
+  return SPK_OK;
+}
+
+int spk_net_info(const spk_net* net, int* max_width, int* n_dense, int64_t* macs) {
+  if (!net) return fail(SPK_ERR_INVALID_PARAMETER, "null net");
+  if (max_width) *max_width = net->max_width;
+  if (n_dense) *n_dense = (int)net->layers.size();
+  if (macs) *macs = net->macs;
+  return SPK_OK;
+}
+
+int spk_bound_batch(const spk_net* net, int policy, int n_keep, int precision, int64_t n, int s,
+                    const double* centers, const double* axes, double* lo, double* hi, int8_t* cls,
+                    void* stream) {
+  if (!net) return fail(SPK_ERR_INVALID_PARAMETER, "null net");
+  int mode;
+  if (int rc = check_policy(policy, n_keep, &mode)) return rc;
+  if (s < 0) return fail(SPK_ERR_DIMENSION, "axes must be (n, s, d)");
+  if (n < 0) return fail(SPK_ERR_DIMENSION, "negative batch");
+  if (n == 0) return SPK_OK;
+  if (mode < 0) return launch_symbolic(net, -mode, n_keep, precision, n, s, centers, axes, lo, hi, cls,
+                                       (cudaStream_t)stream);
+  if (s > 3 && mode == MODE_AFFINE) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "more than 3 box axes");
+  BoxInput in{IN_BOXES, s, centers, axes, 0, 0, 0.0};
+  BoundOutput o{lo, hi, cls};
+  if (mode == MODE_INTERVAL) {
+    // interval only needs the hull: pass all s axes through the radius sum
+    in.s = s;
+    if (s > 3) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "more than 3 box axes");
+  }
+  return run_pass(net, mode, s, precision, in, o, n, (cudaStream_t)stream);
+}
+
+int spk_bound_aabb(const spk_net* net, int policy, int n_keep, int precision, int64_t n,
+                   const double* box_lo, const double* box_hi, double* lo, double* hi, int8_t* cls,
+                   void* stream) {
+  if (!net) return fail(SPK_ERR_INVALID_PARAMETER, "null net");
+  int mode;
+  if (int rc = check_policy(policy, n_keep, &mode)) return rc;
+  if (net->input_dim > 3) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "AABB path supports d <= 3");
+  if (n <= 0) return n < 0 ? fail(SPK_ERR_DIMENSION, "negative batch") : SPK_OK;
+  if (mode < 0) return launch_symbolic_aabb(net, -mode, n_keep, precision, n, box_lo, box_hi, lo, hi, cls,
+                                            (cudaStream_t)stream);
+  BoxInput in{IN_AABB, net->input_dim, box_lo, box_hi, 0, 0, 0.0};
+  BoundOutput o{lo, hi, cls};
+  return run_pass(net, mode, net->input_dim, precision, in, o, n, (cudaStream_t)stream);
+}
+
+int spk_bound_random_cubes(const spk_net* net, int policy, int n_keep, int precision, int64_t n,
+                           int64_t first_index, uint64_t seed, double half, double* lo, double* hi,
+                           int8_t* cls, void* stream) {
+  if (!net) return fail(SPK_ERR_INVALID_PARAMETER, "null net");
+  int mode;
+  if (int rc = check_policy(policy, n_keep, &mode)) return rc;
+  if (mode < 0) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "random cubes: interval / affine-fixed only");
+  if (net->input_dim > 3) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "random cubes support d <= 3");
+  if (!(half >= 0.0)) return fail(SPK_ERR_INVALID_PARAMETER, "half-extent must be >= 0");
+  if (n <= 0) return SPK_OK;
+  BoxInput in{IN_RANDOM, net->input_dim, nullptr, nullptr, (long long)first_index, seed, half};
+  BoundOutput o{lo, hi, cls};
+  return run_pass(net, mode, net->input_dim, precision, in, o, n, (cudaStream_t)stream);
+}
+
+int spk_eval_batch(const spk_net* net, int precision, int64_t n, const double* xs, double* out,
+                   void* stream) {
+  if (!net) return fail(SPK_ERR_INVALID_PARAMETER, "null net");
+  if (n <= 0) return n < 0 ? fail(SPK_ERR_DIMENSION, "negative batch") : SPK_OK;
+  BoxInput in{IN_POINTS, 0, xs, nullptr, 0, 0, 0.0};
+  BoundOutput o{out, nullptr, nullptr};
+  return run_pass(net, MODE_POINT, 0, precision, in, o, n, (cudaStream_t)stream);
+}
+
+int spk_bound_batch_host(const spk_net* net, int policy, int n_keep, int precision, int64_t n, int s,
+                         const double* centers, const double* axes, double* lo, double* hi,
+                         int8_t* cls) {
+  if (!net) return fail(SPK_ERR_INVALID_PARAMETER, "null net");
+  if (n <= 0) return n < 0 ? fail(SPK_ERR_DIMENSION, "negative batch") : SPK_OK;
+  return host_pipeline(net, policy, n_keep, precision, n, s, centers, axes, lo, hi, cls);
+}
+
+}  // extern "C"

@@ -1,0 +1,79 @@
+// Internal host-side types shared by the C-ABI translation units.
+#pragma once
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+#include "spk_pass.cuh"
+
+namespace spk {
+
+struct HostLayer {
+  int m_in = 0, m_out = 0;
+  std::vector<double> W;  // m_out x m_in row-major
+  std::vector<double> b;
+  std::vector<int> acts;  // activations after this dense layer
+};
+
+template <typename T>
+struct DevNet {
+  bool ready = false;
+  NetDev<T> nd;
+  T* tiles = nullptr;
+  T* small = nullptr;
+};
+
+struct BoxInput;
+struct BoundOutput;
+
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* where);
+int sm_count_for(int device);
+
+class DeviceGuard {
+ public:
+  explicit DeviceGuard(int dev);
+  ~DeviceGuard();
+ private:
+  int prev_ = 0, dev_ = 0;
+};
+
+int run_pass(const struct ::spk_net* net, int mode, int S, int precision, const BoxInput& in,
+             const BoundOutput& out, long long n, cudaStream_t st);
+
+// affine-truncate / affine-full (symbol-carrying policies), spk_symbolic.cu
+int launch_symbolic(const struct ::spk_net* net, int policy, int n_keep, int precision, long long n, int s,
+                    const double* centers, const double* axes, double* lo, double* hi, int8_t* cls,
+                    cudaStream_t st);
+int launch_symbolic_aabb(const struct ::spk_net* net, int policy, int n_keep, int precision, long long n,
+                         const double* box_lo, const double* box_hi, double* lo, double* hi, int8_t* cls,
+                         cudaStream_t st);
+
+// host-pointer pipeline, spk_host.cu
+int host_pipeline(const struct ::spk_net* net, int policy, int n_keep, int precision, long long n, int s,
+                  const double* centers, const double* axes, double* lo, double* hi, int8_t* cls);
+
+}  // namespace spk
+
+struct spk_net {
+  int input_dim = 0;
+  int device = 0;
+  int mmax = 0;
+  int max_width = 0;
+  int64_t macs = 0;
+  std::vector<int> pre_acts;
+  std::vector<spk::HostLayer> layers;
+  std::mutex mu;
+  spk::DevNet<float> f32;
+  spk::DevNet<double> f64;
+  template <typename T> spk::DevNet<T>& dev();
+};
+template <> inline spk::DevNet<float>& spk_net::dev<float>() { return f32; }
+template <> inline spk::DevNet<double>& spk_net::dev<double>() { return f64; }
+
+namespace spk {
+template <typename T>
+int get_dev(::spk_net* net, const NetDev<T>** out);
+}

@@ -1,0 +1,159 @@
+// Persistent bound / point-evaluation kernels built on spk_pass.cuh and
+// their host launchers.  Instantiated per (precision, MMAX) in
+// spk_inst_*.cu so nvcc compiles them in parallel.
+#pragma once
+#include <mutex>
+#include "spk_pass.cuh"
+
+namespace spk {
+
+enum InputKind : int { IN_BOXES = 0, IN_AABB = 1, IN_RANDOM = 2, IN_POINTS = 3 };
+
+struct BoxInput {
+  int kind;
+  int s;                   // axes per box (IN_BOXES)
+  const double* a;         // centres / AABB lo / points
+  const double* b;         // axes / AABB hi
+  long long first;         // IN_RANDOM: stream offset
+  unsigned long long seed; // IN_RANDOM
+  double half;             // IN_RANDOM: cube half-extent
+};
+
+struct BoundOutput {
+  double* lo;   // bounds (or point values)
+  double* hi;   // may be null for points
+  int8_t* cls;  // may be null
+};
+
+// splitmix64 finaliser; the C5 box stream.
+SPK_DEV unsigned long long mix64(unsigned long long z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+SPK_DEV double random_coord(unsigned long long seed, long long idx, int k, int d) {
+  const unsigned long long z = mix64(seed + 0x9E3779B97F4A7C15ull * (unsigned long long)(idx * d + k + 1));
+  return (double)(z >> 11) * 0x1.0p-53 * 2.0 - 1.0;
+}
+
+template <typename T, int C, int MMAX, int MODE>
+__global__ void __launch_bounds__(NT, 1)
+    bound_kernel(const NetDev<T> net, const BoxInput in, const BoundOutput out, const long long n) {
+  using CF = Cfg<T, C, MMAX>;
+  constexpr int NB = CF::NB, CP = CF::CP;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* X = reinterpret_cast<T*>(smem_raw);
+  T* Wst = X + CF::XS;
+  T* NBUF = Wst + NSTAGE * CF::TILE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(NBUF + CF::NBUF);
+  const int tid = threadIdx.x;
+  const int d = net.d;
+
+  const long long nbt = (n + NB - 1) / NB;
+  const long long mine = blockIdx.x < nbt ? (nbt - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if (tid == 0) {
+    for (int s = 0; s < NSTAGE; ++s) mbar_init(&full[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  WRing<T, C, MMAX> ring{Wst, full, net.wtiles, net.tiles_per_pass, mine * net.tiles_per_pass, 0};
+  if (net.tiles_per_pass > 0) ring.prologue(tid);
+
+  for (long long tile = blockIdx.x; tile < nbt; tile += gridDim.x) {
+    const long long g0 = tile * NB;
+    // ---- inputs -> X rows [0, d); zeros elsewhere
+    for (int q = tid; q < MMAX * NB; q += NT) {
+      const int k = q / NB, b = q % NB;
+      const long long gb = g0 + b;
+      T packed[CP];
+#pragma unroll
+      for (int c = 0; c < CP; ++c) packed[c] = T(0);
+      if (k < d && gb < n) {
+        State<T, C, MODE> st;
+        double centre;
+        double ax[3] = {0.0, 0.0, 0.0};
+        int n_ax = 0;
+        if (in.kind == IN_BOXES || in.kind == IN_POINTS) {
+          centre = in.a[gb * d + k];
+          if (in.kind == IN_BOXES) {
+            n_ax = in.s < 3 ? in.s : 3;
+            for (int j = 0; j < n_ax; ++j) ax[j] = in.b[(gb * in.s + j) * d + k];
+          }
+        } else if (in.kind == IN_AABB) {
+          const double l = in.a[gb * d + k], h = in.b[gb * d + k];
+          centre = (l + h) / 2.0;  // spatial.py:182-183, exact halving
+          n_ax = d < 3 ? d : 3;
+          if (k < 3) ax[k] = (h - l) / 2.0;
+        } else {
+          centre = random_coord(in.seed, in.first + gb, k, d);
+          n_ax = d < 3 ? d : 3;
+          if (k < 3) ax[k] = in.half;
+        }
+        input_state<T, C, MODE>(centre, ax, n_ax, 1, st);
+        for (int a = 0; a < net.n_pre; ++a) apply_act<T, C, MODE>(st, net.pre_act[a]);
+        pack_next<T, C, MODE>(st, net.gamma_first, packed);
+      }
+      T* dst = X + ((size_t)k * NB + b) * CP;
+#pragma unroll
+      for (int c = 0; c < CP; ++c) dst[c] = packed[c];
+    }
+    __syncthreads();
+
+    auto emit = [&](int b, const State<T, C, MODE>& st) {
+      const long long gb = g0 + b;
+      if (gb >= n) return;
+      double lo, hi;
+      final_bounds<T, C, MODE>(st, lo, hi);
+      out.lo[gb] = lo;
+      if (out.hi) out.hi[gb] = hi;
+      if (out.cls) out.cls[gb] = (int8_t)(lo > 0.0 ? 1 : (hi < 0.0 ? -1 : 0));
+    };
+    run_layers<T, C, MMAX, MODE>(net, X, NBUF, ring, tid, emit);
+  }
+}
+
+// ------------------------------------------------------------- launchers
+template <typename T, int C, int MMAX, int MODE>
+cudaError_t launch_bound(const NetDev<T>& net, const BoxInput& in, const BoundOutput& out, long long n,
+                         int sm_count, cudaStream_t stream) {
+  using CF = Cfg<T, C, MMAX>;
+  auto kfn = bound_kernel<T, C, MMAX, MODE>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  if (n <= 0) return cudaSuccess;
+  const long long nbt = (n + CF::NB - 1) / CF::NB;
+  const int grid = (int)(nbt < sm_count ? nbt : sm_count);
+  kfn<<<grid, NT, CF::SMEM, stream>>>(net, in, out, n);
+  return cudaGetLastError();
+}
+
+// Per-(T, MMAX) dispatch on mode and S; defined in spk_inst_<T>_<MMAX>.cu.
+template <typename T, int MMAX>
+cudaError_t dispatch_bound(int mode, int S, const NetDev<T>& net, const BoxInput& in,
+                           const BoundOutput& out, long long n, int sm_count, cudaStream_t stream);
+
+template <typename T, int MMAX>
+struct KTOf {
+  static constexpr int KT = Cfg<T, 1, MMAX>::KT;
+  static constexpr int SUB = Cfg<T, 1, MMAX>::SUB;
+};
+
+#define SPK_DEFINE_DISPATCH(T, MMAX)                                                                  \
+  template <>                                                                                         \
+  cudaError_t dispatch_bound<T, MMAX>(int mode, int S, const NetDev<T>& net, const BoxInput& in,       \
+                                      const BoundOutput& out, long long n, int sm, cudaStream_t st) { \
+    if (mode == MODE_POINT) return launch_bound<T, 1, MMAX, MODE_POINT>(net, in, out, n, sm, st);      \
+    if (mode == MODE_INTERVAL) return launch_bound<T, 2, MMAX, MODE_INTERVAL>(net, in, out, n, sm, st); \
+    switch (S) {                                                                                      \
+      case 0: return launch_bound<T, 2, MMAX, MODE_AFFINE>(net, in, out, n, sm, st);                  \
+      case 1: return launch_bound<T, 3, MMAX, MODE_AFFINE>(net, in, out, n, sm, st);                  \
+      case 2: return launch_bound<T, 4, MMAX, MODE_AFFINE>(net, in, out, n, sm, st);                  \
+      default: return launch_bound<T, 5, MMAX, MODE_AFFINE>(net, in, out, n, sm, st);                 \
+    }                                                                                                 \
+  }
+
+}  // namespace spk

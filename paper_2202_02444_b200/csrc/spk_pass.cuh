@@ -1,0 +1,468 @@
+// Fused all-layer network pass over a tile of boxes (the K1/K2/K4 kernels).
+//
+// One CTA owns NB boxes for the whole network.  Their state lives in shared
+// memory as X[k][box][c]: for point evaluation c = {x}; for interval
+// arithmetic c = {centre, v}; for affine-fixed c = {base, A_1..A_S, v},
+// where v = e + gamma*(|base| + sum|A|) is the error channel pre-inflated by
+// the rounding budget of the next dense layer.  A dense layer is then ONE
+// contraction of W against all C columns of all NB boxes:
+//     base' = W base + b,   A' = W A   (FFMA, round-to-nearest)
+//     e'    = |W| v + berr               (FFMA.RP with |W| operand modifier)
+// which is exactly the reference's per-layer GEMM (range_core.py:573-582)
+// with the error GEMV folded in, plus a rigorous FP32 rounding budget.  The
+// epilogue applies the activation rule (range_core.py:583-603) and the
+// affine-fixed fold, and writes the next layer's X in place.  The final
+// dense layer (width 1) is a warp reduction that emits lo/hi (and the sign
+// class).  W streams from L2 through a 3-stage cp.async.bulk (TMA bulk copy)
+// + mbarrier ring of KT x MMAX tiles, so the layer loop never waits on HBM.
+//
+// Register tile per thread: TI consecutive output neurons x TB boxes x C
+// columns; all C columns of one (neuron, box) pair are owned by one thread,
+// which lets the activation rule run straight out of registers.
+#pragma once
+#include "spk_common.cuh"
+#include "spk_rules.cuh"
+
+namespace spk {
+
+constexpr int MAX_LAYERS = 24;
+constexpr int MAX_ACTS = 4;
+constexpr int NT = 256;         // threads per CTA
+constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reduction path
+constexpr int NSTAGE = 3;       // W tile ring depth
+
+enum Mode : int { MODE_POINT = 0, MODE_INTERVAL = 1, MODE_AFFINE = 2 };
+
+template <typename T>
+struct LayerDev {
+  int m_in, m_out;
+  int narrow;
+  int ntiles;
+  int n_act;
+  int act[MAX_ACTS];
+  const T* w;        // narrow layers: W row-major (m_out x m_in)
+  const T* bias;     // m_out
+  const T* berr;     // m_out: rounding budget of the bias term, rounded up
+  T gamma_next;      // rounding budget factor of the NEXT dense layer (0 after the last)
+};
+
+template <typename T>
+struct NetDev {
+  int d;
+  int n_layers;
+  int n_pre;
+  int pre_act[MAX_ACTS];
+  T gamma_first;
+  int tiles_per_pass;
+  const T* wtiles;   // generic layers' k-tiles, each KT x MMAX (row k = column k of W)
+  LayerDev<T> L[MAX_LAYERS];
+};
+
+template <typename T, int C, int MMAX>
+struct Cfg {
+  static constexpr int TI = sizeof(T) == 4 ? 8 : 4;
+  static constexpr int TB = C == 1 ? (sizeof(T) == 4 ? 8 : 4) : (C == 2 ? 4 : 2);
+  static constexpr int CP = C == 1 ? 1 : (C == 2 ? 2 : (C <= 4 ? 4 : ((C + 1) / 2) * 2));
+  static constexpr int NG = MMAX / TI;
+  static constexpr int NBG = NT / NG;
+  static constexpr int NB = NBG * TB;
+  static constexpr int KT_RAW = 16384 / (MMAX * (int)sizeof(T));
+  static constexpr int KT = KT_RAW > MMAX ? MMAX : (KT_RAW < 1 ? 1 : KT_RAW);
+  static constexpr int SUB = sizeof(T) == 4 ? (KT < 16 ? KT : 16) : KT;  // blocked-sum length
+  static constexpr int TILE = KT * MMAX;                 // elements per W tile
+  static constexpr int XS = MMAX * NB * CP;              // elements of X
+  static constexpr int NBUF = NB * NARROW_MAX * CP;      // narrow-layer staging
+  static constexpr size_t SMEM = sizeof(T) * (size_t)(XS + NSTAGE * TILE + NBUF) + 64;
+  static_assert(NG >= 1 && NG <= NT && NT % NG == 0, "tile shape");
+  static_assert((TB * CP * sizeof(T)) % 16 == 0, "vector loads of X");
+  static_assert((TI * sizeof(T)) % 16 == 0, "vector loads of W");
+};
+
+// ------------------------------------------------------------ mbarrier/TMA
+SPK_DEV uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+SPK_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+SPK_DEV void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+SPK_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+SPK_DEV void tma_bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Ring of W tiles.  Tile g of the CTA's global sequence is tile
+// (g mod tiles_per_pass) of the network; all threads consume every tile.
+template <typename T, int C, int MMAX>
+struct WRing {
+  using CF = Cfg<T, C, MMAX>;
+  T* stages;
+  uint64_t* full;
+  const T* src;
+  int per_pass;
+  long long total;  // tiles this CTA will consume
+  long long next;   // next tile to consume
+
+  SPK_DEV void issue(long long g) const {
+    const int st = (int)(g % NSTAGE);
+    const T* s = src + (size_t)(g % per_pass) * CF::TILE;
+    tma_bulk_load(stages + (size_t)st * CF::TILE, s, CF::TILE * sizeof(T), &full[st]);
+  }
+  SPK_DEV void prologue(int tid) const {
+    if (tid == 0) {
+      for (long long g = 0; g < NSTAGE && g < total; ++g) issue(g);
+    }
+  }
+  SPK_DEV const T* acquire() const {
+    const int st = (int)(next % NSTAGE);
+    mbar_wait(&full[st], (uint32_t)((next / NSTAGE) & 1));
+    return stages + (size_t)st * CF::TILE;
+  }
+  // every thread must be past its reads of the current stage (caller syncs)
+  SPK_DEV void release(int tid) {
+    if (tid == 0 && next + NSTAGE < total) issue(next + NSTAGE);
+    ++next;
+  }
+};
+
+// --------------------------------------------------------------- epilogue
+// Per-(neuron, box) state between layers.
+template <typename T, int C, int MODE>
+struct State {
+  static constexpr int S = MODE == MODE_AFFINE ? C - 2 : 0;
+  T base;       // value / centre / affine base
+  T A[S > 0 ? S : 1];
+  T e;          // interval radius / affine error (not yet pre-inflated)
+};
+
+template <typename T, int C, int MODE>
+SPK_DEV T sum_abs_A(const State<T, C, MODE>& st) {
+  T r = T(0);
+#pragma unroll
+  for (int j = 0; j < State<T, C, MODE>::S; ++j) r = Num<T>::add_ru(r, fabs(st.A[j]));
+  return r;
+}
+
+// Apply one activation to the state (sound rules; range_core.py:583-603 for
+// affine-fixed, :639-641 for interval, network.py:149-160 for points).
+template <typename T, int C, int MODE>
+SPK_DEV void apply_act(State<T, C, MODE>& st, int act) {
+  if (act == ACT_IDENTITY) return;  // skipped, range_core.py:586-587
+  if (MODE == MODE_POINT) {
+    st.base = act_value<T>(act, st.base);
+  } else if (MODE == MODE_INTERVAL) {
+    const T lo = Num<T>::sub_rd(st.base, st.e), hi = Num<T>::add_ru(st.base, st.e);
+    T L, H;
+    interval_image<T>(act, lo, hi, L, H);
+    const T c = Num<T>::fma_rn(L, T(0.5), Num<T>::mul_rn(H, T(0.5)));
+    st.base = c;
+    st.e = fmax(Num<T>::sub_ru(H, c), Num<T>::sub_ru(c, L));
+  } else {
+    const T rA = sum_abs_A(st);
+    const T r = Num<T>::add_ru(rA, st.e);
+    const T lo = Num<T>::sub_rd(st.base, r), hi = Num<T>::add_ru(st.base, r);
+    T a, b, g;
+    const int kind = affine_rule<T>(act, lo, hi, a, b, g);
+    if (kind == 0) return;
+    if (kind == 1) {
+      st.base = T(0);
+#pragma unroll
+      for (int j = 0; j < State<T, C, MODE>::S; ++j) st.A[j] = T(0);
+      st.e = T(0);
+      return;
+    }
+    const T nb = Num<T>::fma_rn(a, st.base, b);
+#pragma unroll
+    for (int j = 0; j < State<T, C, MODE>::S; ++j) st.A[j] = Num<T>::mul_rn(a, st.A[j]);
+    const T aa = fabs(a);
+    T e = Num<T>::fma_ru(aa, st.e, g);
+    // rounding of a*base+b and of the a*A_j products
+    e = Num<T>::fma_ru(Num<T>::RHO, Num<T>::add_ru(fabs(nb), Num<T>::mul_ru(aa, rA)), e);
+    st.e = Num<T>::add_ru(e, Num<T>::TINY);
+    st.base = nb;
+  }
+}
+
+// Column values handed to the next dense layer.
+template <typename T, int C, int MODE>
+SPK_DEV void pack_next(const State<T, C, MODE>& st, T gamma_next, T* out) {
+  out[0] = st.base;
+  // v = e + gamma' (|base| + sum|A| + e): gamma' covers the next layer's
+  // FMA rounding and (FP32) the rounding of the FP64 weights to T.
+  if (MODE == MODE_INTERVAL) {
+    out[1] = Num<T>::fma_ru(gamma_next, Num<T>::add_ru(fabs(st.base), st.e), st.e);
+  } else if (MODE == MODE_AFFINE) {
+    const T rA = sum_abs_A(st);
+#pragma unroll
+    for (int j = 0; j < State<T, C, MODE>::S; ++j) out[1 + j] = st.A[j];
+    out[C - 1] = Num<T>::fma_ru(gamma_next, Num<T>::add_ru(Num<T>::add_ru(fabs(st.base), rA), st.e), st.e);
+  }
+}
+
+// Final bound of a width-1 output: lo/hi rounded outward.
+template <typename T, int C, int MODE>
+SPK_DEV void final_bounds(const State<T, C, MODE>& st, double& lo, double& hi) {
+  if (MODE == MODE_POINT) {
+    lo = hi = (double)st.base;
+  } else if (MODE == MODE_INTERVAL) {
+    lo = (double)Num<T>::sub_rd(st.base, st.e);
+    hi = (double)Num<T>::add_ru(st.base, st.e);
+  } else {
+    const T r = Num<T>::add_ru(sum_abs_A(st), st.e);
+    lo = (double)Num<T>::sub_rd(st.base, r);
+    hi = (double)Num<T>::add_ru(st.base, r);
+  }
+}
+
+// ------------------------------------------------------------ dense layers
+// Generic layer: register-tiled contraction over the W ring.  The
+// round-to-nearest columns are summed in blocks of SUB k-steps (fresh
+// partials added to the running sums), so the rounding budget is
+// gamma_{SUB + ceil(m_in/SUB) + 1} instead of gamma_{m_in + 1}.
+template <typename T, int C, int MMAX, int MODE>
+SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, MMAX>& ring, int tid,
+                           bool last, T gamma_next) {
+  using CF = Cfg<T, C, MMAX>;
+  constexpr int TI = CF::TI, TB = CF::TB, CP = CF::CP, NB = CF::NB, KT = CF::KT;
+  const int ng = tid % CF::NG, bg = tid / CF::NG;
+  const int i0 = ng * TI;
+
+  T acc[TI][TB][C];
+#pragma unroll
+  for (int ti = 0; ti < TI; ++ti) {
+    const T b0 = (i0 + ti < L.m_out) ? L.bias[i0 + ti] : T(0);
+#pragma unroll
+    for (int tb = 0; tb < TB; ++tb) {
+      acc[ti][tb][0] = b0;
+#pragma unroll
+      for (int c = 1; c < C; ++c) acc[ti][tb][c] = T(0);
+    }
+  }
+
+  for (int t = 0; t < L.ntiles; ++t) {
+    const T* __restrict__ Ws = ring.acquire();
+    const T* __restrict__ Xt = X + ((size_t)(t * KT) * NB + bg * TB) * CP;
+    // RN columns accumulate in SUB-step partial sums (blocked summation):
+    // rounding budget gamma_{SUB + ceil(m_in/SUB) + 1} instead of gamma_{m_in+1}.
+#pragma unroll 1
+    for (int k0 = 0; k0 < KT; k0 += CF::SUB) {
+      T part[TI][TB][C > 1 ? C - 1 : 1];
+#pragma unroll
+      for (int ti = 0; ti < TI; ++ti)
+#pragma unroll
+        for (int tb = 0; tb < TB; ++tb)
+#pragma unroll
+          for (int c = 0; c < (C > 1 ? C - 1 : 1); ++c) part[ti][tb][c] = T(0);
+#pragma unroll 2
+      for (int kk = k0; kk < k0 + CF::SUB; ++kk) {
+        T w[TI];
+        T x[TB * CP];
+        {
+          const float4* wp = reinterpret_cast<const float4*>(Ws + kk * MMAX + i0);
+          float4* wd = reinterpret_cast<float4*>(w);
+#pragma unroll
+          for (int q = 0; q < (int)(TI * sizeof(T) / 16); ++q) wd[q] = wp[q];
+          const float4* xp = reinterpret_cast<const float4*>(Xt + (size_t)kk * NB * CP);
+          float4* xd = reinterpret_cast<float4*>(x);
+#pragma unroll
+          for (int q = 0; q < (int)(TB * CP * sizeof(T) / 16); ++q) xd[q] = xp[q];
+        }
+#pragma unroll
+        for (int ti = 0; ti < TI; ++ti) {
+#pragma unroll
+          for (int tb = 0; tb < TB; ++tb) {
+            if (C == 1) {
+              part[ti][tb][0] = Num<T>::fma_rn(w[ti], x[tb * CP], part[ti][tb][0]);
+            } else {
+#pragma unroll
+              for (int c = 0; c < C - 1; ++c)
+                part[ti][tb][c] = Num<T>::fma_rn(w[ti], x[tb * CP + c], part[ti][tb][c]);
+              acc[ti][tb][C - 1] = Num<T>::fma_ru(fabs(w[ti]), x[tb * CP + C - 1], acc[ti][tb][C - 1]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int ti = 0; ti < TI; ++ti)
+#pragma unroll
+        for (int tb = 0; tb < TB; ++tb)
+#pragma unroll
+          for (int c = 0; c < (C > 1 ? C - 1 : 1); ++c) acc[ti][tb][c] += part[ti][tb][c];
+    }
+    __syncthreads();  // all reads of this W stage (and, on the last tile, of X) are done
+    ring.release(tid);
+  }
+
+  // epilogue: activation rules, write next X in place
+#pragma unroll
+  for (int ti = 0; ti < TI; ++ti) {
+    const int i = i0 + ti;
+    const bool valid = i < L.m_out;
+    const T be = valid ? L.berr[i] : T(0);
+#pragma unroll
+    for (int tb = 0; tb < TB; ++tb) {
+      const int b = bg * TB + tb;
+      T out[CP];
+#pragma unroll
+      for (int c = 0; c < CP; ++c) out[c] = T(0);
+      if (valid) {
+        State<T, C, MODE> st;
+        st.base = acc[ti][tb][0];
+        if (MODE == MODE_AFFINE) {
+#pragma unroll
+          for (int j = 0; j < State<T, C, MODE>::S; ++j) st.A[j] = acc[ti][tb][1 + j];
+        }
+        st.e = (MODE == MODE_POINT) ? T(0) : Num<T>::add_ru(acc[ti][tb][C - 1], be);
+        for (int a = 0; a < L.n_act; ++a) apply_act<T, C, MODE>(st, L.act[a]);
+        pack_next<T, C, MODE>(st, gamma_next, out);
+      }
+      T* dst = X + ((size_t)i * NB + b) * CP;
+#pragma unroll
+      for (int c = 0; c < CP; ++c) dst[c] = out[c];
+    }
+  }
+  __syncthreads();
+  (void)last;
+}
+
+// Narrow layer (m_out <= NARROW_MAX, e.g. the final width-1 layer): one
+// warp per (box, neuron) item, lanes stride over k, butterfly reduction.
+// Rounding budget gamma_{ceil(m_in/32) + 6}.
+template <typename T, int C, int MMAX, int MODE, class Emit>
+SPK_DEV void narrow_layer(const LayerDev<T>& L, T* __restrict__ X, T* __restrict__ NBUF, int tid,
+                          bool last, T gamma_next, Emit&& emit) {
+  using CF = Cfg<T, C, MMAX>;
+  constexpr int CP = CF::CP, NB = CF::NB, KT = CF::KT;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int items = NB * L.m_out;
+  for (int it = warp; it < items; it += NT / 32) {
+    const int b = it / L.m_out, i = it % L.m_out;
+    const T* wrow = L.w + (size_t)i * L.m_in;
+    T p[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) p[c] = T(0);
+    for (int k = lane; k < L.m_in; k += 32) {
+      const T wk = __ldg(wrow + k);
+      const T* xk = X + ((size_t)k * NB + b) * CP;
+      if (C == 1) {
+        p[0] = Num<T>::fma_rn(wk, xk[0], p[0]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < C - 1; ++c) p[c] = Num<T>::fma_rn(wk, xk[c], p[c]);
+        p[C - 1] = Num<T>::fma_ru(fabs(wk), xk[C - 1], p[C - 1]);
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const T o = __shfl_xor_sync(0xffffffffu, p[c], off);
+        p[c] = (C > 1 && c == C - 1) ? Num<T>::add_ru(p[c], o) : p[c] + o;
+      }
+    }
+    if (lane == 0) {
+      T* dst = NBUF + ((size_t)b * NARROW_MAX + i) * CP;
+#pragma unroll
+      for (int c = 0; c < C; ++c) dst[c] = p[c];
+    }
+  }
+  __syncthreads();
+  // epilogue
+  for (int it = tid; it < items; it += NT) {
+    const int b = it / L.m_out, i = it % L.m_out;
+    const T* src = NBUF + ((size_t)b * NARROW_MAX + i) * CP;
+    State<T, C, MODE> st;
+    st.base = src[0] + L.bias[i];
+    if (MODE == MODE_AFFINE) {
+#pragma unroll
+      for (int j = 0; j < State<T, C, MODE>::S; ++j) st.A[j] = src[1 + j];
+    }
+    st.e = (MODE == MODE_POINT) ? T(0) : Num<T>::add_ru(src[C - 1], L.berr[i]);
+    for (int a = 0; a < L.n_act; ++a) apply_act<T, C, MODE>(st, L.act[a]);
+    if (last) {
+      emit(b, st);
+    } else {
+      T out[CP];
+#pragma unroll
+      for (int c = 0; c < CP; ++c) out[c] = T(0);
+      pack_next<T, C, MODE>(st, gamma_next, out);
+      T* dst = X + ((size_t)i * NB + b) * CP;
+#pragma unroll
+      for (int c = 0; c < CP; ++c) dst[c] = out[c];
+    }
+  }
+  if (!last) {
+    // zero the rows a following generic layer reads beyond m_out
+    const int r_end = ((L.m_out + KT - 1) / KT) * KT;
+    const int n = (r_end - L.m_out) * NB * CP;
+    T* base = X + (size_t)L.m_out * NB * CP;
+    for (int q = tid; q < n; q += NT) base[q] = T(0);
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- the pass
+// Runs every layer for the CTA's current tile.  X rows [0, d) must hold the
+// packed input columns and rows [d, MMAX) zeros; `emit(b, state)` receives
+// each box's final width-1 state.
+template <typename T, int C, int MMAX, int MODE, class Emit>
+SPK_DEV void run_layers(const NetDev<T>& net, T* X, T* NBUF, WRing<T, C, MMAX>& ring, int tid,
+                        Emit&& emit) {
+  for (int l = 0; l < net.n_layers; ++l) {
+    const LayerDev<T>& L = net.L[l];
+    const bool last = (l == net.n_layers - 1);
+    if (L.narrow) {
+      narrow_layer<T, C, MMAX, MODE>(L, X, NBUF, tid, last, L.gamma_next, emit);
+    } else {
+      generic_layer<T, C, MMAX, MODE>(L, X, ring, tid, last, L.gamma_next);
+    }
+  }
+}
+
+// Sound FP64 -> T conversion of one input coordinate of an affine/interval
+// state.  Returns the packed columns for X given the centre coordinate and
+// the s axis components along this dimension (n_ax of them).
+template <typename T, int C, int MODE>
+SPK_DEV void input_state(double centre, const double* ax, int n_ax, int stride, State<T, C, MODE>& st) {
+  st.base = Num<T>::from_d_rn(centre);
+  if (MODE == MODE_POINT) { st.e = T(0); return; }
+  T err = conv_err<T>(centre, st.base);
+  if (MODE == MODE_INTERVAL) {
+    double r = 0.0;
+    for (int j = 0; j < n_ax; ++j) r = __dadd_ru(r, fabs(ax[j * stride]));
+    st.e = Num<T>::add_ru(Num<T>::from_d_ru(r), err);
+  } else {
+    constexpr int S = State<T, C, MODE>::S;
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      const double a = j < n_ax ? ax[j * stride] : 0.0;
+      st.A[j] = Num<T>::from_d_rn(a);
+      err = Num<T>::add_ru(err, conv_err<T>(a, st.A[j]));
+    }
+    // axes beyond the compiled S are folded into the error channel (sound)
+    for (int j = S; j < n_ax; ++j) {
+      err = Num<T>::add_ru(err, Num<T>::from_d_ru(fabs(ax[j * stride])));
+    }
+    st.e = err;
+  }
+}
+
+}  // namespace spk

@@ -1,0 +1,347 @@
+// K5: breadth-first k-d tree build (build_spatial_tree, spatial.py:214-289)
+// as a level-synchronous frontier on the device.
+//
+// Per level: (1) the fused bound kernel classifies every frontier AABB
+// (IN_AABB input, centre/half-extent formed in FP64 exactly like
+// spatial.py:181-183); (2) spk_tree_mark decides split / tiny-leaf per node
+// and counts splits per block with a warp ballot; (3) spk_tree_scatter
+// finds its block offset, ranks split nodes inside the block with a
+// ballot prefix, and writes the children: low halves at [0, K), high halves
+// at [K, 2K) -- the reference's level layout (spatial.py:285-287) -- with
+// the midpoint split on the widest axis computed in FP64 (spatial.py:189-199),
+// so child AABBs are bit-identical to the reference's.  Tiny UNKNOWN leaves
+// (convergence mode) get the 2d face-centre sign annotation
+// (spatial.py:257-265) from one point-evaluation pass.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "spk_kernels.cuh"
+#include "spk_abi_internal.h"
+
+namespace spk {
+
+constexpr int TB_THREADS = 256;
+
+struct TreeLevel {
+  long long n = 0;
+  double* lo = nullptr;      // n x d
+  double* hi = nullptr;      // n x d
+  double* blo = nullptr;     // bound lo (n)
+  double* bhi = nullptr;     // bound hi (n)
+  int8_t* label = nullptr;   // +1 / -1 / 0
+  int8_t* face = nullptr;    // face-sign annotation (+1/-1, 0 = none)
+  long long* parent = nullptr;
+};
+
+// per-node decision: flag 1 = split, 2 = tiny UNKNOWN leaf (convergence mode)
+__global__ void tree_mark_kernel(long long n, int d, const double* __restrict__ lo, const double* __restrict__ hi,
+                                 const int8_t* __restrict__ label, int depth, int max_depth, double stop_extent,
+                                 uint8_t* __restrict__ flag, int* __restrict__ block_split,
+                                 int* __restrict__ block_small) {
+  const long long i = (long long)blockIdx.x * TB_THREADS + threadIdx.x;
+  uint8_t f = 0;
+  if (i < n && label[i] == 0) {
+    if (max_depth >= 0) {
+      f = depth < max_depth ? 1 : 0;
+    } else {
+      double ext = 0.0;
+      for (int k = 0; k < d; ++k) ext = fmax(ext, hi[i * d + k] - lo[i * d + k]);
+      f = ext < stop_extent ? 2 : 1;
+    }
+  }
+  if (i < n) flag[i] = f;
+  __shared__ int ws[TB_THREADS / 32], wt[TB_THREADS / 32];
+  const unsigned bs = __ballot_sync(0xffffffffu, f == 1);
+  const unsigned bt = __ballot_sync(0xffffffffu, f == 2);
+  if ((threadIdx.x & 31) == 0) {
+    ws[threadIdx.x >> 5] = __popc(bs);
+    wt[threadIdx.x >> 5] = __popc(bt);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int a = 0, b = 0;
+    for (int w = 0; w < TB_THREADS / 32; ++w) { a += ws[w]; b += wt[w]; }
+    block_split[blockIdx.x] = a;
+    block_small[blockIdx.x] = b;
+  }
+}
+
+// Exclusive offset of this block = sum of earlier blocks' counts.
+__device__ long long block_offset(const int* __restrict__ counts, int upto) {
+  long long s = 0;
+  for (int b = threadIdx.x; b < upto; b += TB_THREADS) s += counts[b];
+  __shared__ long long red[TB_THREADS / 32];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  long long t = 0;
+  for (int w = 0; w < TB_THREADS / 32; ++w) t += red[w];
+  __syncthreads();
+  return t;
+}
+
+// Rank of this thread's flag among the block's flagged threads (ballot prefix).
+__device__ int block_rank(bool pred, int* total) {
+  __shared__ int wcount[TB_THREADS / 32];
+  const unsigned m = __ballot_sync(0xffffffffu, pred);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) wcount[w] = __popc(m);
+  __syncthreads();
+  int before = 0, all = 0;
+  for (int q = 0; q < TB_THREADS / 32; ++q) {
+    if (q < w) before += wcount[q];
+    all += wcount[q];
+  }
+  __syncthreads();
+  *total = all;
+  return before + __popc(m & ((1u << lane) - 1u));
+}
+
+__global__ void tree_scatter_kernel(long long n, int d, const double* __restrict__ lo, const double* __restrict__ hi,
+                                    const uint8_t* __restrict__ flag, const int* __restrict__ block_split,
+                                    const int* __restrict__ block_small, long long n_split,
+                                    double* __restrict__ child_lo, double* __restrict__ child_hi,
+                                    long long* __restrict__ child_parent, long long* __restrict__ small_idx) {
+  const long long i = (long long)blockIdx.x * TB_THREADS + threadIdx.x;
+  const long long off_s = block_offset(block_split, blockIdx.x);
+  const long long off_t = block_offset(block_small, blockIdx.x);
+  const uint8_t f = i < n ? flag[i] : 0;
+  int tot;
+  const int rs = block_rank(f == 1, &tot);
+  const int rt = block_rank(f == 2, &tot);
+  if (f == 2) small_idx[off_t + rt] = i;
+  if (f != 1) return;
+  const long long j = off_s + rs;
+  // widest axis, ties to the lowest index (np.argmax, spatial.py:193)
+  int ax = 0;
+  double best = -1.0;
+  for (int k = 0; k < d; ++k) {
+    const double e = hi[i * d + k] - lo[i * d + k];
+    if (e > best) { best = e; ax = k; }
+  }
+  const double mid = 0.5 * (lo[i * d + ax] + hi[i * d + ax]);
+  for (int k = 0; k < d; ++k) {
+    const double l = lo[i * d + k], h = hi[i * d + k];
+    child_lo[j * d + k] = l;
+    child_hi[j * d + k] = k == ax ? mid : h;
+    child_lo[(n_split + j) * d + k] = k == ax ? mid : l;
+    child_hi[(n_split + j) * d + k] = h;
+  }
+  child_parent[j] = i;
+  child_parent[n_split + j] = i;
+}
+
+// Face centres of tiny leaves: (m, 2d, d) points (spatial.py:202-211).
+__global__ void face_points_kernel(long long m, int d, const long long* __restrict__ idx,
+                                   const double* __restrict__ lo, const double* __restrict__ hi,
+                                   double* __restrict__ pts) {
+  const long long t = (long long)blockIdx.x * TB_THREADS + threadIdx.x;
+  if (t >= m * 2 * d) return;
+  const long long node = idx[t / (2 * d)];
+  const int face = (int)(t % (2 * d));
+  const int axis = face / 2;
+  for (int k = 0; k < d; ++k) {
+    const double l = lo[node * d + k], h = hi[node * d + k];
+    const double c = (l + h) / 2.0, half = (h - l) / 2.0;
+    double v = c;
+    if (k == axis) v = (face & 1) ? c + half : c - half;
+    pts[t * d + k] = v;
+  }
+}
+
+__global__ void face_sign_kernel(long long m, int d, const long long* __restrict__ idx,
+                                 const double* __restrict__ vals, int8_t* __restrict__ face) {
+  const long long t = (long long)blockIdx.x * TB_THREADS + threadIdx.x;
+  if (t >= m) return;
+  bool neg = false, pos = false;
+  for (int q = 0; q < 2 * d; ++q) {
+    const double v = vals[t * 2 * d + q];
+    neg |= v < 0.0;
+    pos |= v >= 0.0;
+  }
+  face[idx[t]] = (neg && pos) ? 0 : (neg ? -1 : 1);
+}
+
+}  // namespace spk
+
+struct spk_tree {
+  int d = 0;
+  int device = 0;
+  std::vector<spk::TreeLevel> levels;
+  long long bound_evals = 0;
+};
+
+namespace spk {
+
+static void free_level(TreeLevel& L) {
+  cudaFree(L.lo); cudaFree(L.hi); cudaFree(L.blo); cudaFree(L.bhi);
+  cudaFree(L.label); cudaFree(L.face); cudaFree(L.parent);
+  L = TreeLevel();
+}
+
+static int alloc_level(TreeLevel& L, long long n, int d) {
+  L.n = n;
+  const size_t m = std::max<long long>(n, 1);
+  cudaError_t e = cudaSuccess;
+  if (e == cudaSuccess) e = cudaMalloc(&L.lo, m * d * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&L.hi, m * d * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&L.blo, m * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&L.bhi, m * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&L.label, m);
+  if (e == cudaSuccess) e = cudaMalloc(&L.face, m);
+  if (e == cudaSuccess) e = cudaMalloc(&L.parent, m * sizeof(long long));
+  if (e != cudaSuccess) return cuda_fail(e, "tree level alloc");
+  return SPK_OK;
+}
+
+}  // namespace spk
+
+using namespace spk;
+
+extern "C" {
+
+int spk_tree_build(const spk_net* net, int policy, int n_keep, int precision, const double* root_lo,
+                   const double* root_hi, int max_depth, double delta, void* stream, spk_tree** out) {
+  if (!net || !out) return fail(SPK_ERR_INVALID_PARAMETER, "null argument");
+  *out = nullptr;
+  const int d = net->input_dim;
+  if (d > 3) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "tree build supports d <= 3");
+  if (!(delta > 0.0)) return fail(SPK_ERR_INVALID_PARAMETER, "delta must be positive");
+  if (max_depth > 60) return fail(SPK_ERR_DEPTH_OVERFLOW, "fixed depth exceeds 60");
+  for (int k = 0; k < d; ++k) {
+    if (!std::isfinite(root_lo[k]) || !std::isfinite(root_hi[k]) || !(root_hi[k] > root_lo[k]))
+      return fail(SPK_ERR_INVALID_PARAMETER, "bounds must be finite with positive extent");
+  }
+  DeviceGuard g(net->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  auto tree = new spk_tree();
+  tree->d = d;
+  tree->device = net->device;
+  const double stop = delta / std::sqrt((double)d);
+  int rc = SPK_OK;
+  TreeLevel cur;
+  if ((rc = alloc_level(cur, 1, d)) != SPK_OK) { delete tree; return rc; }
+  cudaMemcpyAsync(cur.lo, root_lo, d * sizeof(double), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(cur.hi, root_hi, d * sizeof(double), cudaMemcpyHostToDevice, st);
+  const long long minus1 = -1;
+  cudaMemcpyAsync(cur.parent, &minus1, sizeof(long long), cudaMemcpyHostToDevice, st);
+  cudaMemsetAsync(cur.face, 0, 1, st);
+  int* counts = nullptr;
+  uint8_t* flag = nullptr;
+  long long* small_idx = nullptr;
+  double* fpts = nullptr;
+  double* fvals = nullptr;
+  long long cap = 0, fcap = 0;
+  for (int depth = 0; rc == SPK_OK; ++depth) {
+    const long long n = cur.n;
+    rc = spk_bound_aabb(net, policy, n_keep, precision, n, cur.lo, cur.hi, cur.blo, cur.bhi, cur.label, st);
+    if (rc != SPK_OK) break;
+    tree->bound_evals += n;
+    cudaMemsetAsync(cur.face, 0, n, st);
+    const int nb = (int)((n + TB_THREADS - 1) / TB_THREADS);
+    if (n > cap) {
+      cudaFree(counts); cudaFree(flag); cudaFree(small_idx);
+      cap = std::max<long long>(n, 1024);
+      const long long nbc = (cap + TB_THREADS - 1) / TB_THREADS;
+      if (cudaMalloc(&counts, 2 * nbc * sizeof(int)) != cudaSuccess ||
+          cudaMalloc(&flag, cap) != cudaSuccess || cudaMalloc(&small_idx, cap * sizeof(long long)) != cudaSuccess) {
+        rc = fail(SPK_ERR_OUT_OF_MEMORY, "tree scratch");
+        break;
+      }
+    }
+    int* bsplit = counts;
+    int* bsmall = counts + nb;
+    tree_mark_kernel<<<nb, TB_THREADS, 0, st>>>(n, d, cur.lo, cur.hi, cur.label, depth, max_depth, stop, flag,
+                                                bsplit, bsmall);
+    // totals: sum of block counts (small launch, then one D2H)
+    long long totals[2] = {0, 0};
+    {
+      std::vector<int> hc(2 * (size_t)nb);
+      cudaError_t e = cudaMemcpyAsync(hc.data(), counts, 2 * nb * sizeof(int), cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) { rc = cuda_fail(e, "tree level"); break; }
+      for (int b = 0; b < nb; ++b) { totals[0] += hc[b]; totals[1] += hc[nb + b]; }
+    }
+    const long long k = totals[0], m = totals[1];
+    TreeLevel next;
+    if (k > 0 && (rc = alloc_level(next, 2 * k, d)) != SPK_OK) break;
+    tree_scatter_kernel<<<nb, TB_THREADS, 0, st>>>(n, d, cur.lo, cur.hi, flag, bsplit, bsmall, k, next.lo, next.hi,
+                                                   next.parent, small_idx);
+    if (m > 0) {
+      if (m * 2 * d > fcap) {
+        cudaFree(fpts); cudaFree(fvals);
+        fcap = m * 2 * d;
+        if (cudaMalloc(&fpts, fcap * d * sizeof(double)) != cudaSuccess ||
+            cudaMalloc(&fvals, fcap * sizeof(double)) != cudaSuccess) {
+          rc = fail(SPK_ERR_OUT_OF_MEMORY, "face points");
+          break;
+        }
+      }
+      const long long np = m * 2 * d;
+      face_points_kernel<<<(int)((np + TB_THREADS - 1) / TB_THREADS), TB_THREADS, 0, st>>>(m, d, small_idx, cur.lo,
+                                                                                             cur.hi, fpts);
+      rc = spk_eval_batch(net, precision, np, fpts, fvals, st);
+      if (rc != SPK_OK) break;
+      face_sign_kernel<<<(int)((m + TB_THREADS - 1) / TB_THREADS), TB_THREADS, 0, st>>>(m, d, small_idx, fvals,
+                                                                                          cur.face);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { rc = cuda_fail(e, "tree kernels"); break; }
+    tree->levels.push_back(cur);
+    cur = TreeLevel();
+    if (k == 0) break;
+    cur = next;
+  }
+  if (cur.lo) free_level(cur);
+  cudaFree(counts); cudaFree(flag); cudaFree(small_idx); cudaFree(fpts); cudaFree(fvals);
+  if (rc == SPK_OK) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "tree sync");
+  }
+  if (rc != SPK_OK) {
+    for (auto& L : tree->levels) free_level(L);
+    delete tree;
+    return rc;
+  }
+  *out = tree;
+  return SPK_OK;
+}
+
+int spk_tree_destroy(spk_tree* tree) {
+  if (!tree) return SPK_OK;
+  DeviceGuard g(tree->device);
+  for (auto& L : tree->levels) free_level(L);
+  delete tree;
+  return SPK_OK;
+}
+
+int spk_tree_info(const spk_tree* tree, int* n_levels, int64_t* n_nodes, int64_t* bound_evals) {
+  if (!tree) return fail(SPK_ERR_INVALID_PARAMETER, "null tree");
+  long long total = 0;
+  for (auto& L : tree->levels) total += L.n;
+  if (n_levels) *n_levels = (int)tree->levels.size();
+  if (n_nodes) *n_nodes = total;
+  if (bound_evals) *bound_evals = tree->bound_evals;
+  return SPK_OK;
+}
+
+int spk_tree_level(const spk_tree* tree, int level, int64_t* n, const double** lo, const double** hi,
+                   const double** bound_lo, const double** bound_hi, const int8_t** label, const int8_t** face,
+                   const int64_t** parent) {
+  if (!tree || level < 0 || level >= (int)tree->levels.size())
+    return fail(SPK_ERR_INVALID_PARAMETER, "bad tree level");
+  const TreeLevel& L = tree->levels[level];
+  if (n) *n = L.n;
+  if (lo) *lo = L.lo;
+  if (hi) *hi = L.hi;
+  if (bound_lo) *bound_lo = L.blo;
+  if (bound_hi) *bound_hi = L.bhi;
+  if (label) *label = L.label;
+  if (face) *face = L.face;
+  if (parent) *parent = reinterpret_cast<const int64_t*>(L.parent);
+  return SPK_OK;
+}
+
+}  // extern "C"

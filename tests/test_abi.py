@@ -1,0 +1,55 @@
+"""CPU-side checks of the C-ABI boundary: the in-tree library loads and
+exports every entry point include/spelunk_b200.h declares; network upload
+validation maps onto the reference's exceptions.  No kernels run here."""
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2202_02444_b200 import _lib, errors
+from paper_2202_02444_b200.network import DeviceNet, NetworkSpec, DenseLayer, load_network
+
+HEADER = Path(__file__).resolve().parents[1] / "include" / "spelunk_b200.h"
+
+
+def declared_functions():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"\b(spk_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    names = declared_functions()
+    assert len(names) >= 10
+    for name in names:
+        assert hasattr(lib, name), name
+
+
+def test_bindings_cover_header():
+    assert set(declared_functions()) <= set(_lib.SIGNATURES)
+
+
+def test_net_create_validates(net_paths):
+    lib = _lib.load()
+    dn = DeviceNet(load_network(net_paths["relu4x32"]), 0)
+    assert dn.max_width == 32 and dn.n_dense == 5 and dn.macs == 3 * 32 + 3 * 32 * 32 + 32
+    # final width must be 1 (network.py:106-107)
+    bad = np.zeros((2, 3))
+    import ctypes as C
+
+    kinds = np.array([_lib.OP_DENSE], np.int32)
+    outs = np.array([2], np.int32)
+    params = np.zeros(8)
+    h = C.c_void_p()
+    st = lib.spk_net_create(3, 1, kinds.ctypes.data, outs.ctypes.data, params.ctypes.data, 8, 0, C.byref(h))
+    assert st == _lib.ERR_DIM
+    with pytest.raises(errors.DimensionMismatch):
+        _lib.check(st)
+
+
+def test_width_limit_reported():
+    net = NetworkSpec(3, (DenseLayer(np.zeros((600, 3)), np.zeros(600)), DenseLayer(np.zeros((1, 600)), np.zeros(1))))
+    with pytest.raises(errors.DeviceError):
+        DeviceNet(net, 0)
