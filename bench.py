@@ -1,0 +1,479 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 range-analysis hot path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Headline workload (BASELINE.json configs[1], "C2"): k-d tree build to depth
+18 over [-1,1]^3 with affine-fixed bounds on a random-init (torch-uniform,
+seed 0) 3->8x256->1 ReLU MLP.  A step is one full tree build; `value` is
+affine box bounds per second (tree nodes bounded / step time, whole job).
+At N > 1 the frontier below a redundant top cut is split across ranks (one
+process per GPU, no collective in the build): total work is fixed, so
+scaling is "strong".  `extra` carries the C5 throughput sweep point
+(16M on-device cubes, 8x256, one launch) and C1 (4x32, 64^3 grid).
+
+Timing: W untimed warm-up steps, then K steps, each bracketed by a barrier
+and torch.cuda.synchronize(), timed with CUDA events on the launching
+stream; the max over ranks is taken.  L2 (126 MB) is flushed by writing a
+256 MB buffer before every timed step.  SM clocks and throttle reasons are
+sampled with nvidia-smi during the timed region.
+
+--impl reference times the reference's own CPU algorithm (the pinned NumPy
+oracle port, oracle/spelunk_oracle.py; the reference itself is pure Python
+and cannot travel to the GPU box) on all host cores: P processes with one
+BLAS thread each bound 4096-box chunks of the same depth-18 level
+(spatial.py:172-186 calls range_bound_batch in 4096-box chunks).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "affine box bounds/sec (8x256 MLP)"
+UNIT = "boxes/s"
+DEPTH = 18
+CHUNK = 4096
+
+
+# --------------------------------------------------------------------------- CPU legs
+def _cpu_worker(args):
+    """One single-BLAS-thread process bounding its share of boxes (oracle port)."""
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    net_doc, centers, axes, reps = args
+    try:
+        from threadpoolctl import threadpool_limits
+
+        lim = threadpool_limits(1)
+    except Exception:  # pragma: no cover
+        lim = None
+    from oracle import spelunk_oracle as orc
+
+    net = orc.net_from_json_doc(net_doc)
+    orc.bound_batch(net, centers[:64], axes[:64], "affine-fixed")  # warm
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        for s in range(0, len(centers), CHUNK):
+            orc.bound_batch(net, centers[s : s + CHUNK], axes[s : s + CHUNK], "affine-fixed")
+    dt = time.perf_counter() - t0
+    del lim
+    return len(centers) * reps, dt
+
+
+class CpuPool:
+    def __init__(self, procs):
+        import multiprocessing as mp
+
+        os.environ["OPENBLAS_NUM_THREADS"] = "1"
+        os.environ["OMP_NUM_THREADS"] = "1"
+        self.procs = procs
+        self.pool = mp.get_context("spawn").Pool(procs)
+
+    def run(self, net_doc, centers, axes, per_proc, reps=1):
+        parts = []
+        for p in range(self.procs):
+            sl = slice(p * per_proc, (p + 1) * per_proc)
+            parts.append((net_doc, centers[sl], axes[sl], reps))
+        t0 = time.perf_counter()
+        res = self.pool.map(_cpu_worker, parts)
+        wall = time.perf_counter() - t0
+        boxes = sum(r[0] for r in res)
+        busy = max(r[1] for r in res)
+        return boxes, busy, wall
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def level18_boxes():
+    """The depth-18 level of the C2 tree when every node is UNKNOWN (the
+    random-init case): the 64^3 grid of cubes of half 1/64."""
+    from paper_2202_02444_b200 import synth
+
+    return synth.grid_cubes(64)
+
+
+def cpu_info():
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model, os.cpu_count() or 1
+
+
+def run_reference(args, rank):
+    """--impl reference: the reference algorithm on the host cores."""
+    if rank != 0:
+        return None
+    from paper_2202_02444_b200 import network, synth
+
+    net = synth.config_net("C2")
+    doc = network.network_to_doc(net)
+    centers, axes = level18_boxes()
+    model, cores = cpu_info()
+    pool = CpuPool(cores)
+    per_proc = CHUNK
+    rng = np.random.default_rng(0)
+    sel = rng.permutation(len(centers))[: per_proc * cores]
+    c, a = centers[sel], axes[sel]
+    for _ in range(args.warmup):
+        pool.run(doc, c, a, per_proc)
+    tot_boxes, tot_time = 0, 0.0
+    for _ in range(args.steps):
+        boxes, busy, wall = pool.run(doc, c, a, per_proc)
+        tot_boxes += boxes
+        tot_time += wall
+    pool.close()
+    value = tot_boxes / tot_time
+    sample = (f"{cores} procs x 1 BLAS thread, each one {CHUNK}-box chunk of the depth-18 level per step "
+              f"(range_bound_batch chunking of spatial.py:38); CPU {model}")
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * tot_time / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": "C2 k-d tree depth 18, 8x256 ReLU (torch-uniform seed 0), affine-fixed; "
+                               "reference arm bounds the depth-18 level in 4096-box chunks",
+                   "flush": "n/a (CPU)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+# --------------------------------------------------------------------------- GPU helpers
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (recipe's clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[3:7]):
+                if flag.lower() in ("active", "1", "yes"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def physical_gpu_index(local_rank):
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        ids = [v.strip() for v in vis.split(",") if v.strip()]
+        if local_rank < len(ids) and ids[local_rank].isdigit():
+            return int(ids[local_rank])
+    return local_rank
+
+
+def timed(fn, torch, flush, barrier):
+    """Barrier + sync, flush L2, CUDA-event time of fn() on the current stream."""
+    barrier()
+    torch.cuda.synchronize()
+    flush()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    out = fn()
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    return e0.elapsed_time(e1) / 1e3, out
+
+
+def load_traffic():
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except ValueError:
+            return {}
+    return {}
+
+
+# --------------------------------------------------------------------------- main GPU arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    import paper_2202_02444_b200 as sp
+    from paper_2202_02444_b200 import _lib, spatial, synth
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.cuda.current_device()
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+
+        def barrier():
+            tdist.barrier()
+    else:
+        def barrier():
+            return None
+
+    flush_buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def flush():
+        flush_buf.fill_(1.0)
+
+    net = synth.config_net("C2")
+    dn = sp.network.device_net(net, dev)
+    flop_box = 2.0 * (3 + 2) * dn.macs  # affine-fixed, s = 3
+    bounds = spatial.AABB(-np.ones(3), np.ones(3))
+
+    def step():
+        if world == 1:
+            return spatial.build_spatial_tree_arrays(net, bounds, policy=sp.AFFINE_FIXED, max_depth=DEPTH,
+                                                     precision="fp32", to_host=False)
+        return spatial.build_spatial_tree_sharded(net, bounds, DEPTH, sp.AFFINE_FIXED, rank, world,
+                                                  precision="fp32", to_host=False)
+
+    def useful_units(arr):
+        """Tree nodes this rank contributes, each node of the unsharded tree once."""
+        if "top_levels" in arr.meta:  # sharded: own sub-tree below the cut (+ the top, on rank 0)
+            own = arr.n_nodes - len(arr.levels[0])
+            return own + (arr.meta["top_nodes"] if rank == 0 else 0)
+        return arr.n_nodes if rank == 0 else 0
+
+    for _ in range(args.warmup):
+        timed(step, torch, flush, barrier)
+
+    times, launches, kernel_ms, kernel_boxes, units_local = [], 0, 0.0, 0, 0
+    clock = ClockSampler(physical_gpu_index(local_rank))
+    with clock:
+        for _ in range(args.steps):
+            dt, arr = timed(step, torch, flush, barrier)
+            times.append(dt)
+            launches += arr.launches
+            kernel_ms += arr.bound_ms
+            kernel_boxes += arr.bound_evals
+            units_local += useful_units(arr)
+    step_time = np.array(times)
+    if dist:
+        import torch.distributed as tdist
+
+        t = torch.tensor([step_time.sum(), float(units_local)], dtype=torch.float64, device=dev)
+        tmax = t.clone()
+        tdist.all_reduce(tmax[:1], op=tdist.ReduceOp.MAX)
+        tdist.all_reduce(t[1:], op=tdist.ReduceOp.SUM)
+        total_time, units = float(tmax[0]), float(t[1])
+    else:
+        total_time, units = float(step_time.sum()), float(units_local)
+    value = units / total_time
+
+    if rank != 0:
+        return None
+
+    # ---- roofline of the dominant kernel (fused bound kernel, FFMA-bound)
+    import ctypes as C
+
+    pk = C.c_double()
+    _lib.call("spk_ffma_peak", 20000, C.byref(pk), torch.cuda.current_stream().cuda_stream)
+    peak_tf = pk.value / 1e12
+    achieved_tf = kernel_boxes * flop_box / (kernel_ms / 1e3) / 1e12
+    traffic = load_traffic().get("C2_bound_kernel_bytes_per_launch")
+
+    # ---- extra workloads (single GPU, rank 0): C5 16M cubes and C1 grid
+    extra = {}
+    extra["C5_8x256_16M"] = bench_c5(torch, sp, synth, "C5_256", 16 << 20, flush, peak_tf)
+    extra["C1_4x32_64cubed"] = bench_c1(torch, sp, synth, flush, peak_tf)
+
+    # ---- e2e through the public API (host arrays out)
+    e2e = bench_e2e_tree(torch, sp, spatial, net, bounds, args)
+
+    # ---- CPU baseline: oracle port on the host cores, bounded sample
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        cpu = cpu_baseline(sp)
+
+    ck = clock.summary()
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total_time / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+        "config": {"workload": "C2: k-d tree build to depth 18 over [-1,1]^3, affine-fixed, 3->8x256->1 ReLU "
+                               "random-init (torch-uniform, seed 0); 524,287 node bounds per build",
+                   "global_batch": int(units / args.steps), "parallelism": f"frontier-sharded x{world}",
+                   "flush": "L2 flushed (256 MB write) before every timed step",
+                   "certified_fraction": None},
+        "roofline": {"bound": "fp32", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": achieved_tf / peak_tf, "traffic": traffic,
+                     "kernel": "spk::bound_kernel<float,5,256,AFFINE> (all tree levels)",
+                     "flop_per_box": flop_box,
+                     "peak_source": "measured FFMA probe (spk_ffma_peak) on this GPU at run time",
+                     "kernel_ms_per_step": kernel_ms / args.steps},
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "gpu_launches": int(launches / args.steps),
+        "clocks": ck,
+        "extra": extra,
+    }
+
+
+def bench_c5(torch, sp, synth, tag, n, flush, peak_tf):
+    net = synth.config_net(tag)
+    dn = sp.network.device_net(net)
+    lo = torch.empty(n, dtype=torch.float64, device="cuda")
+    hi = torch.empty(n, dtype=torch.float64, device="cuda")
+    cls = torch.empty(n, dtype=torch.int8, device="cuda")
+    out = (lo, hi, cls)
+    run = lambda: sp.bound_random_cubes(net, n, seed=1, half=1.0 / 64, out=out)
+    run()
+    ts = []
+    for _ in range(3):
+        dt, _ = timed(run, torch, flush, lambda: None)
+        ts.append(dt)
+    dt = float(np.median(ts))
+    flop = 2.0 * 5 * dn.macs
+    cert = float((cls != 0).float().mean().item())
+    return {"boxes": n, "boxes_per_s": n / dt, "ms": dt * 1e3, "tflops": n * flop / dt / 1e12,
+            "frac_of_ffma_peak": n * flop / dt / 1e12 / peak_tf, "certified_fraction": cert,
+            "half_extent": 1 / 64}
+
+
+def bench_c1(torch, sp, synth, flush, peak_tf):
+    net = synth.config_net("C1")
+    dn = sp.network.device_net(net)
+    c, a = synth.grid_cubes(64)
+    ct = torch.from_numpy(c).cuda()
+    at = torch.from_numpy(a).cuda()
+    run = lambda: sp.range_bound_batch(net, ct, at, sp.AFFINE_FIXED, return_class=True)
+    run()
+    ts = []
+    for _ in range(5):
+        dt, res = timed(run, torch, flush, lambda: None)
+        ts.append(dt)
+    dt = float(np.median(ts))
+    n = len(c)
+    flop = 2.0 * 5 * dn.macs
+    cert = float((res[2] != 0).float().mean().item())
+    return {"boxes": n, "boxes_per_s": n / dt, "ms": dt * 1e3, "tflops": n * flop / dt / 1e12,
+            "frac_of_ffma_peak": n * flop / dt / 1e12 / peak_tf, "certified_fraction": cert}
+
+
+def bench_e2e_tree(torch, sp, spatial, net, bounds, args):
+    """Public API, host arrays out: build_spatial_tree_arrays(to_host=True)."""
+    arr = spatial.build_spatial_tree_arrays(net, bounds, policy=sp.AFFINE_FIXED, max_depth=DEPTH, to_host=True)
+    ts = []
+    for _ in range(max(1, min(args.steps, 3))):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        arr = spatial.build_spatial_tree_arrays(net, bounds, policy=sp.AFFINE_FIXED, max_depth=DEPTH, to_host=True)
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    dt = float(np.median(ts))
+    n = arr.n_nodes
+    d2h = sum(l.lo.nbytes + l.hi.nbytes + l.bound_lo.nbytes + l.bound_hi.nbytes + l.label.nbytes +
+              l.face.nbytes + l.parent.nbytes for l in arr.levels)
+    return {"value": n / dt, "unit": UNIT, "h2d_bytes_per_step": 48, "d2h_bytes_per_step": int(d2h),
+            "api": "build_spatial_tree_arrays(net, AABB([-1]*3,[1]*3), policy=AFFINE_FIXED, max_depth=18, "
+                   "to_host=True)", "ms": dt * 1e3}
+
+
+def cpu_baseline(sp):
+    from paper_2202_02444_b200 import network, synth
+
+    net = synth.config_net("C2")
+    doc = network.network_to_doc(net)
+    centers, axes = level18_boxes()
+    model, cores = cpu_info()
+    per_proc = 2 * CHUNK
+    sel = np.random.default_rng(1).permutation(len(centers))[: per_proc * cores]
+    pool = CpuPool(cores)
+    pool.run(doc, centers[sel][: cores * 64], axes[sel][: cores * 64], 64)  # spawn + import warm-up
+    boxes, busy, wall = pool.run(doc, centers[sel], axes[sel], per_proc)
+    pool.close()
+    return {"value": boxes / wall, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{boxes} depth-18 boxes ({cores} procs x {per_proc}, 4096-box chunks, 1 BLAS thread each), "
+                      f"affine-fixed 8x256, oracle port of range_bound_batch; CPU {model}; wall {wall:.1f}s"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        line = run_reference(args, rank)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    line = run_ours(args, rank, world, local_rank)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as tdist
+
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

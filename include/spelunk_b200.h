@@ -81,6 +81,9 @@ const char* spk_last_error(void);
 int spk_version(void);
 /* number of SMs of the current device, or -1 */
 int spk_device_sm_count(void);
+/* measured FP32 FFMA throughput of the current device (FLOP/s), the
+ * roofline denominator of the FFMA-bound bound kernels */
+int spk_ffma_peak(int iters, double* flops_per_s, void* stream);
 
 /* Upload a network once.  op_kind[i] is SPK_OP_*; for dense ops
  * op_out_dim[i] is the output width and `params` holds, for every dense op
@@ -128,17 +131,26 @@ int spk_bound_batch_host(const spk_net* net, int policy, int n_keep, int precisi
                          double* hi, int8_t* cls);
 
 /* K5: breadth-first k-d tree (build_spatial_tree, spatial.py:214-289).
- * root_lo/root_hi: host arrays of d doubles.  max_depth >= 0: fixed-depth
+ * root_lo/root_hi: host arrays of n_roots x d doubles (one root for the
+ * reference call; a frontier slice at start_depth when the build is sharded
+ * across GPUs -- depths, and so the fixed-depth cut, count from start_depth).
+ * max_depth >= 0: fixed-depth
  * mode (UNKNOWN nodes split while depth < max_depth, <= 60 else
  * SPK_ERR_DEPTH_OVERFLOW); max_depth < 0: convergence mode, UNKNOWN nodes
  * split until their widest extent drops below delta/sqrt(d) and such leaves
  * get the face-centre sign annotation.  The result lives in device memory,
  * one array set per level: level k+1 = [low children ; high children] of
  * level k's split nodes, in order (the reference's layout). */
-int spk_tree_build(const spk_net* net, int policy, int n_keep, int precision, const double* root_lo,
-                   const double* root_hi, int max_depth, double delta, void* stream, spk_tree** out);
+int spk_tree_build(const spk_net* net, int policy, int n_keep, int precision, int64_t n_roots,
+                   const double* root_lo, const double* root_hi, int start_depth, int max_depth,
+                   double delta, void* stream, spk_tree** out);
 int spk_tree_destroy(spk_tree* tree);
 int spk_tree_info(const spk_tree* tree, int* n_levels, int64_t* n_nodes, int64_t* bound_evals);
+/* copy one level into caller buffers (host or device, any may be NULL) */
+int spk_tree_level_copy(const spk_tree* tree, int level, double* lo, double* hi, double* bound_lo,
+                        double* bound_hi, int8_t* label, int8_t* face, int64_t* parent);
+/* kernels launched by the build and CUDA-event time spent in its bound kernels */
+int spk_tree_stats(const spk_tree* tree, int64_t* launches, double* bound_ms);
 /* device pointers of one level (valid until spk_tree_destroy): AABB corners
  * (n x d), the bound, the sign label (+1/-1/0), the face-sign annotation
  * (+1/-1, 0 = none) and the parent index into the previous level (-1). */

@@ -45,6 +45,7 @@ SIGNATURES = {
     "spk_last_error": ([], C.c_char_p),
     "spk_version": ([], i32),
     "spk_device_sm_count": ([], i32),
+    "spk_ffma_peak": ([i32, vp, vp], i32),
     "spk_net_create": ([i32, i32, vp, vp, vp, i64, i32, vp], i32),
     "spk_net_destroy": ([vp], i32),
     "spk_net_info": ([vp, vp, vp, vp], i32),
@@ -53,7 +54,9 @@ SIGNATURES = {
     "spk_bound_random_cubes": ([vp, i32, i32, i32, i64, i64, u64, f64, vp, vp, vp, vp], i32),
     "spk_eval_batch": ([vp, i32, i64, vp, vp, vp], i32),
     "spk_bound_batch_host": ([vp, i32, i32, i32, i64, i32, vp, vp, vp, vp, vp], i32),
-    "spk_tree_build": ([vp, i32, i32, i32, vp, vp, i32, f64, vp, vp], i32),
+    "spk_tree_build": ([vp, i32, i32, i32, i64, vp, vp, i32, i32, f64, vp, vp], i32),
+    "spk_tree_stats": ([vp, vp, vp], i32),
+    "spk_tree_level_copy": ([vp, i32, vp, vp, vp, vp, vp, vp, vp], i32),
     "spk_tree_destroy": ([vp], i32),
     "spk_tree_info": ([vp, vp, vp, vp], i32),
     "spk_tree_level": ([vp, i32, vp, vp, vp, vp, vp, vp, vp, vp], i32),

@@ -75,6 +75,10 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = True) ->
     jobs = jobs or max(1, min(len(sources), os.cpu_count() or 4))
     with ThreadPoolExecutor(max_workers=jobs) as pool:
         objs = list(pool.map(lambda s: _compile(s, force), sources))
+    keep = {o.name for o in objs}
+    for stale in OBJDIR.glob("*.o"):
+        if stale.name not in keep:
+            stale.unlink()
     newest = max(o.stat().st_mtime for o in objs)
     if LIB.exists() and LIB.stat().st_mtime >= newest and not force:
         if verbose:

@@ -394,3 +394,54 @@ int spk_bound_batch_host(const spk_net* net, int policy, int n_keep, int precisi
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// FP32 FFMA throughput probe: the roofline denominator for the FFMA-bound
+// bound kernels, measured on the box at its current clocks (bench.py).
+namespace spk {
+__global__ void __launch_bounds__(256) ffma_probe_kernel(float* out, int iters, float seed, float mp, float cp) {
+  // 16 independent FFMA chains per thread with register operands (a = a*b + c);
+  // b and c are the same registers for every chain, the classic peak probe.
+  float a[16], b, c;
+  asm volatile("mov.f32 %0, %1;" : "=f"(b) : "f"(mp));
+  asm volatile("mov.f32 %0, %1;" : "=f"(c) : "f"(cp));
+#pragma unroll
+  for (int j = 0; j < 16; ++j) a[j] = seed + j * 1e-3f + threadIdx.x * 1e-7f;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) a[j] = fmaf(a[j], b, c);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) s += a[j];
+  if (s == 12345.678f) out[0] = s;  // keep the chains alive
+}
+}  // namespace spk
+
+extern "C" int spk_ffma_peak(int iters, double* flops_per_s, void* stream) {
+  using namespace spk;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int sm = sm_count_for(dev);
+  if (sm <= 0) return fail(SPK_ERR_CUDA, "no CUDA device");
+  float* out = nullptr;
+  if (cudaMalloc(&out, sizeof(float)) != cudaSuccess) return fail(SPK_ERR_OUT_OF_MEMORY, "probe");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int blocks = sm * 8, threads = 256;
+  ffma_probe_kernel<<<blocks, threads, 0, st>>>(out, 64, 1.0f, 0.9999f, 1e-6f);  // warm-up
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, st);
+  ffma_probe_kernel<<<blocks, threads, 0, st>>>(out, iters, 1.0f, 0.9999f, 1e-6f);
+  cudaEventRecord(e1, st);
+  cudaError_t e = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  if (e != cudaSuccess) return cuda_fail(e, "ffma probe");
+  *flops_per_s = 2.0 * 16.0 * (double)iters * blocks * threads / (ms * 1e-3);
+  return SPK_OK;
+}

@@ -66,16 +66,25 @@ struct Cfg {
   static constexpr int NG = MMAX / TI;
   static constexpr int NBG = NT / NG;
   static constexpr int NB = NBG * TB;
-  static constexpr int KT_RAW = 16384 / (MMAX * (int)sizeof(T));
+  static constexpr int KT_RAW = 32768 / (MMAX * (int)sizeof(T));
   static constexpr int KT = KT_RAW > MMAX ? MMAX : (KT_RAW < 1 ? 1 : KT_RAW);
-  static constexpr int SUB = sizeof(T) == 4 ? (KT < 16 ? KT : 16) : KT;  // blocked-sum length
+  static constexpr int SUB = sizeof(T) == 4 ? 16 : 1 << 20;  // blocked-sum length (FP32)
   static constexpr int TILE = KT * MMAX;                 // elements per W tile
-  static constexpr int XS = MMAX * NB * CP;              // elements of X
+  // X row stride (elements): 16-byte aligned rows, and an odd number of
+  // 16-byte units per row so the epilogue's vector stores spread over banks
+  static constexpr int RS0 = ((NB * CP * (int)sizeof(T) + 15) / 16) * 16 / (int)sizeof(T);
+  static constexpr int RS = ((RS0 * (int)sizeof(T) / 16) % 2 == 1) ? RS0 : RS0 + 16 / (int)sizeof(T);
+  static constexpr int XS = MMAX * RS;                   // elements of X
+  // a thread's TI neurons: TI/G groups of G consecutive neurons (G = one
+  // 16-byte vector); group q of neuron-group ng starts at q*NG*G + ng*G, so
+  // a warp's vector loads of a W row are contiguous (bank-conflict free)
+  static constexpr int G = 16 / (int)sizeof(T);
   static constexpr int NBUF = NB * NARROW_MAX * CP;      // narrow-layer staging
   static constexpr size_t SMEM = sizeof(T) * (size_t)(XS + NSTAGE * TILE + NBUF) + 64;
   static_assert(NG >= 1 && NG <= NT && NT % NG == 0, "tile shape");
   static_assert((TB * CP * sizeof(T)) % 16 == 0, "vector loads of X");
   static_assert((TI * sizeof(T)) % 16 == 0, "vector loads of W");
+  SPK_DEV static int neuron(int ng, int ti) { return (ti / G) * (NG * G) + ng * G + (ti % G); }
 };
 
 // ------------------------------------------------------------ mbarrier/TMA
@@ -243,12 +252,12 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
   using CF = Cfg<T, C, MMAX>;
   constexpr int TI = CF::TI, TB = CF::TB, CP = CF::CP, NB = CF::NB, KT = CF::KT;
   const int ng = tid % CF::NG, bg = tid / CF::NG;
-  const int i0 = ng * TI;
 
   T acc[TI][TB][C];
 #pragma unroll
   for (int ti = 0; ti < TI; ++ti) {
-    const T b0 = (i0 + ti < L.m_out) ? L.bias[i0 + ti] : T(0);
+    const int i = CF::neuron(ng, ti);
+    const T b0 = (i < L.m_out) ? L.bias[i] : T(0);
 #pragma unroll
     for (int tb = 0; tb < TB; ++tb) {
       acc[ti][tb][0] = b0;
@@ -257,72 +266,97 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
     }
   }
 
-  for (int t = 0; t < L.ntiles; ++t) {
-    const T* __restrict__ Ws = ring.acquire();
-    const T* __restrict__ Xt = X + ((size_t)(t * KT) * NB + bg * TB) * CP;
-    // RN columns accumulate in SUB-step partial sums (blocked summation):
-    // rounding budget gamma_{SUB + ceil(m_in/SUB) + 1} instead of gamma_{m_in+1}.
-#pragma unroll 1
-    for (int k0 = 0; k0 < KT; k0 += CF::SUB) {
-      T part[TI][TB][C > 1 ? C - 1 : 1];
+  // RN columns accumulate in SUB-step partial sums (blocked summation, the
+  // blocks may span W tiles): rounding budget gamma_{SUB + ceil(m_in/SUB) + 1}
+  // instead of gamma_{m_in + 1}.  The RU error column needs no blocking.
+  constexpr int CR = C > 1 ? C - 1 : 1;
+  constexpr int SUBIN = KT < CF::SUB ? KT : CF::SUB;
+  T part[TI][TB][CR];
 #pragma unroll
-      for (int ti = 0; ti < TI; ++ti)
+  for (int ti = 0; ti < TI; ++ti)
 #pragma unroll
-        for (int tb = 0; tb < TB; ++tb)
+    for (int tb = 0; tb < TB; ++tb)
 #pragma unroll
-          for (int c = 0; c < (C > 1 ? C - 1 : 1); ++c) part[ti][tb][c] = T(0);
-#pragma unroll 2
-      for (int kk = k0; kk < k0 + CF::SUB; ++kk) {
-        T w[TI];
-        T x[TB * CP];
-        {
-          const float4* wp = reinterpret_cast<const float4*>(Ws + kk * MMAX + i0);
-          float4* wd = reinterpret_cast<float4*>(w);
+      for (int c = 0; c < CR; ++c) part[ti][tb][c] = T(0);
+  int since = 0;
+  auto flush = [&]() {
 #pragma unroll
-          for (int q = 0; q < (int)(TI * sizeof(T) / 16); ++q) wd[q] = wp[q];
-          const float4* xp = reinterpret_cast<const float4*>(Xt + (size_t)kk * NB * CP);
-          float4* xd = reinterpret_cast<float4*>(x);
+    for (int ti = 0; ti < TI; ++ti)
 #pragma unroll
-          for (int q = 0; q < (int)(TB * CP * sizeof(T) / 16); ++q) xd[q] = xp[q];
+      for (int tb = 0; tb < TB; ++tb)
+#pragma unroll
+        for (int c = 0; c < CR; ++c) {
+          acc[ti][tb][c] += part[ti][tb][c];
+          part[ti][tb][c] = T(0);
         }
+  };
+
+  // fragment loads for one k-step (W: TI values, X: TB*CP values)
+  auto load_frag = [&](const T* __restrict__ Ws, const T* __restrict__ Xt, int kk, T* w, T* x) {
+    float4* wd = reinterpret_cast<float4*>(w);
 #pragma unroll
-        for (int ti = 0; ti < TI; ++ti) {
+    for (int q = 0; q < TI / CF::G; ++q)
+      wd[q] = *reinterpret_cast<const float4*>(Ws + kk * MMAX + q * (CF::NG * CF::G) + ng * CF::G);
+    const float4* xp = reinterpret_cast<const float4*>(Xt + (size_t)kk * CF::RS);
+    float4* xd = reinterpret_cast<float4*>(x);
 #pragma unroll
-          for (int tb = 0; tb < TB; ++tb) {
-            if (C == 1) {
-              part[ti][tb][0] = Num<T>::fma_rn(w[ti], x[tb * CP], part[ti][tb][0]);
-            } else {
+    for (int q = 0; q < (int)(TB * CP * sizeof(T) / 16); ++q) xd[q] = xp[q];
+  };
+  auto fma_step = [&](const T* w, const T* x) {
 #pragma unroll
-              for (int c = 0; c < C - 1; ++c)
-                part[ti][tb][c] = Num<T>::fma_rn(w[ti], x[tb * CP + c], part[ti][tb][c]);
-              acc[ti][tb][C - 1] = Num<T>::fma_ru(fabs(w[ti]), x[tb * CP + C - 1], acc[ti][tb][C - 1]);
-            }
-          }
+    for (int ti = 0; ti < TI; ++ti) {
+#pragma unroll
+      for (int tb = 0; tb < TB; ++tb) {
+        if (C == 1) {
+          part[ti][tb][0] = Num<T>::fma_rn(w[ti], x[tb * CP], part[ti][tb][0]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < C - 1; ++c)
+            part[ti][tb][c] = Num<T>::fma_rn(w[ti], x[tb * CP + c], part[ti][tb][c]);
+          acc[ti][tb][C - 1] = Num<T>::fma_ru(fabs(w[ti]), x[tb * CP + C - 1], acc[ti][tb][C - 1]);
         }
       }
-#pragma unroll
-      for (int ti = 0; ti < TI; ++ti)
-#pragma unroll
-        for (int tb = 0; tb < TB; ++tb)
-#pragma unroll
-          for (int c = 0; c < (C > 1 ? C - 1 : 1); ++c) acc[ti][tb][c] += part[ti][tb][c];
+    }
+  };
+
+  for (int t = 0; t < L.ntiles; ++t) {
+    const T* __restrict__ Ws = ring.acquire();
+    const T* __restrict__ Xt = X + (size_t)(t * KT) * CF::RS + bg * TB * CP;
+#pragma unroll 1
+    for (int k0 = 0; k0 < KT; k0 += SUBIN) {
+      // register double buffering: fragments of step kk+1 load while step kk computes
+      T w0[TI], x0[TB * CP], w1[TI], x1[TB * CP];
+      load_frag(Ws, Xt, k0, w0, x0);
+#pragma unroll 2
+      for (int kk = k0; kk < k0 + SUBIN; kk += 2) {
+        load_frag(Ws, Xt, kk + 1, w1, x1);
+        fma_step(w0, x0);
+        if (kk + 2 < k0 + SUBIN) load_frag(Ws, Xt, kk + 2, w0, x0);
+        fma_step(w1, x1);
+      }
+      since += SUBIN;
+      if (since >= CF::SUB) {
+        flush();
+        since = 0;
+      }
     }
     __syncthreads();  // all reads of this W stage (and, on the last tile, of X) are done
     ring.release(tid);
   }
+  if (since > 0) flush();
 
-  // epilogue: activation rules, write next X in place
+  // epilogue: activation rules, write next X in place (one contiguous
+  // TB*CP vector per neuron: the thread's boxes are adjacent in the row)
 #pragma unroll
   for (int ti = 0; ti < TI; ++ti) {
-    const int i = i0 + ti;
+    const int i = CF::neuron(ng, ti);
     const bool valid = i < L.m_out;
     const T be = valid ? L.berr[i] : T(0);
+    T out[TB * CP];
+#pragma unroll
+    for (int c = 0; c < TB * CP; ++c) out[c] = T(0);
 #pragma unroll
     for (int tb = 0; tb < TB; ++tb) {
-      const int b = bg * TB + tb;
-      T out[CP];
-#pragma unroll
-      for (int c = 0; c < CP; ++c) out[c] = T(0);
       if (valid) {
         State<T, C, MODE> st;
         st.base = acc[ti][tb][0];
@@ -332,12 +366,13 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
         }
         st.e = (MODE == MODE_POINT) ? T(0) : Num<T>::add_ru(acc[ti][tb][C - 1], be);
         for (int a = 0; a < L.n_act; ++a) apply_act<T, C, MODE>(st, L.act[a]);
-        pack_next<T, C, MODE>(st, gamma_next, out);
+        pack_next<T, C, MODE>(st, gamma_next, out + tb * CP);
       }
-      T* dst = X + ((size_t)i * NB + b) * CP;
-#pragma unroll
-      for (int c = 0; c < CP; ++c) dst[c] = out[c];
     }
+    float4* dst = reinterpret_cast<float4*>(X + (size_t)i * CF::RS + bg * TB * CP);
+    const float4* srcv = reinterpret_cast<const float4*>(out);
+#pragma unroll
+    for (int q = 0; q < (int)(TB * CP * sizeof(T) / 16); ++q) dst[q] = srcv[q];
   }
   __syncthreads();
   (void)last;
@@ -361,7 +396,7 @@ SPK_DEV void narrow_layer(const LayerDev<T>& L, T* __restrict__ X, T* __restrict
     for (int c = 0; c < C; ++c) p[c] = T(0);
     for (int k = lane; k < L.m_in; k += 32) {
       const T wk = __ldg(wrow + k);
-      const T* xk = X + ((size_t)k * NB + b) * CP;
+      const T* xk = X + (size_t)k * CF::RS + b * CP;
       if (C == 1) {
         p[0] = Num<T>::fma_rn(wk, xk[0], p[0]);
       } else {
@@ -404,7 +439,7 @@ SPK_DEV void narrow_layer(const LayerDev<T>& L, T* __restrict__ X, T* __restrict
 #pragma unroll
       for (int c = 0; c < CP; ++c) out[c] = T(0);
       pack_next<T, C, MODE>(st, gamma_next, out);
-      T* dst = X + ((size_t)i * NB + b) * CP;
+      T* dst = X + (size_t)i * CF::RS + b * CP;
 #pragma unroll
       for (int c = 0; c < CP; ++c) dst[c] = out[c];
     }
@@ -412,8 +447,8 @@ SPK_DEV void narrow_layer(const LayerDev<T>& L, T* __restrict__ X, T* __restrict
   if (!last) {
     // zero the rows a following generic layer reads beyond m_out
     const int r_end = ((L.m_out + KT - 1) / KT) * KT;
-    const int n = (r_end - L.m_out) * NB * CP;
-    T* base = X + (size_t)L.m_out * NB * CP;
+    const int n = (r_end - L.m_out) * CF::RS;
+    T* base = X + (size_t)L.m_out * CF::RS;
     for (int q = tid; q < n; q += NT) base[q] = T(0);
   }
   __syncthreads();

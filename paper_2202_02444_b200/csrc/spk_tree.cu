@@ -14,6 +14,7 @@
 // (spatial.py:257-265) from one point-evaluation pass.
 #include <algorithm>
 #include <cmath>
+#include <mutex>
 #include <vector>
 
 #include "spk_kernels.cuh"
@@ -169,31 +170,68 @@ __global__ void face_sign_kernel(long long m, int d, const long long* __restrict
 struct spk_tree {
   int d = 0;
   int device = 0;
+  int start_depth = 0;
   std::vector<spk::TreeLevel> levels;
   long long bound_evals = 0;
+  cudaStream_t stream = nullptr;  // frees are ordered on the build stream
+  long long launches = 0;   // kernels launched by the build
+  double bound_ms = 0.0;    // CUDA-event time of the bound kernels
 };
 
 namespace spk {
 
-static void free_level(TreeLevel& L) {
-  cudaFree(L.lo); cudaFree(L.hi); cudaFree(L.blo); cudaFree(L.bhi);
-  cudaFree(L.label); cudaFree(L.face); cudaFree(L.parent);
+// All tree memory comes from the device's stream-ordered pool
+// (cudaMallocAsync): after the first build, a level costs no driver call.
+static void free_level(TreeLevel& L, cudaStream_t st) {
+  if (L.lo) cudaFreeAsync(L.lo, st);  // one block per level, see alloc_level
   L = TreeLevel();
 }
 
-static int alloc_level(TreeLevel& L, long long n, int d) {
+static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static int alloc_level(TreeLevel& L, long long n, int d, cudaStream_t st) {
   L.n = n;
   const size_t m = std::max<long long>(n, 1);
-  cudaError_t e = cudaSuccess;
-  if (e == cudaSuccess) e = cudaMalloc(&L.lo, m * d * sizeof(double));
-  if (e == cudaSuccess) e = cudaMalloc(&L.hi, m * d * sizeof(double));
-  if (e == cudaSuccess) e = cudaMalloc(&L.blo, m * sizeof(double));
-  if (e == cudaSuccess) e = cudaMalloc(&L.bhi, m * sizeof(double));
-  if (e == cudaSuccess) e = cudaMalloc(&L.label, m);
-  if (e == cudaSuccess) e = cudaMalloc(&L.face, m);
-  if (e == cudaSuccess) e = cudaMalloc(&L.parent, m * sizeof(long long));
+  const size_t b_lo = align_up(m * d * sizeof(double)), b_b = align_up(m * sizeof(double)),
+               b_i8 = align_up(m), b_par = align_up(m * sizeof(long long));
+  char* base = nullptr;
+  cudaError_t e = cudaMallocAsync(&base, 2 * b_lo + 2 * b_b + 2 * b_i8 + b_par, st);
   if (e != cudaSuccess) return cuda_fail(e, "tree level alloc");
+  L.lo = reinterpret_cast<double*>(base);
+  L.hi = reinterpret_cast<double*>(base + b_lo);
+  L.blo = reinterpret_cast<double*>(base + 2 * b_lo);
+  L.bhi = reinterpret_cast<double*>(base + 2 * b_lo + b_b);
+  L.label = reinterpret_cast<int8_t*>(base + 2 * b_lo + 2 * b_b);
+  L.face = reinterpret_cast<int8_t*>(base + 2 * b_lo + 2 * b_b + b_i8);
+  L.parent = reinterpret_cast<long long*>(base + 2 * b_lo + 2 * b_b + 2 * b_i8);
   return SPK_OK;
+}
+
+// per-thread pinned staging for the per-level block counts (grown, never freed)
+static bool pinned_scratch(size_t bytes, void** out) {
+  thread_local void* buf = nullptr;
+  thread_local size_t cap = 0;
+  if (bytes > cap) {
+    if (buf) cudaFreeHost(buf);
+    cap = std::max<size_t>(bytes, 1 << 16);
+    if (cudaMallocHost(&buf, cap) != cudaSuccess) { buf = nullptr; cap = 0; return false; }
+  }
+  *out = buf;
+  return true;
+}
+
+void keep_pool_memory(int device) {
+  static std::mutex mu;
+  static std::vector<int> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if ((int)done.size() <= device) done.resize(device + 1, 0);
+  if (done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[device] = 1;
 }
 
 }  // namespace spk
@@ -202,52 +240,68 @@ using namespace spk;
 
 extern "C" {
 
-int spk_tree_build(const spk_net* net, int policy, int n_keep, int precision, const double* root_lo,
-                   const double* root_hi, int max_depth, double delta, void* stream, spk_tree** out) {
+int spk_tree_build(const spk_net* net, int policy, int n_keep, int precision, int64_t n_roots,
+                   const double* root_lo, const double* root_hi, int start_depth, int max_depth, double delta,
+                   void* stream, spk_tree** out) {
   if (!net || !out) return fail(SPK_ERR_INVALID_PARAMETER, "null argument");
   *out = nullptr;
   const int d = net->input_dim;
   if (d > 3) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "tree build supports d <= 3");
   if (!(delta > 0.0)) return fail(SPK_ERR_INVALID_PARAMETER, "delta must be positive");
   if (max_depth > 60) return fail(SPK_ERR_DEPTH_OVERFLOW, "fixed depth exceeds 60");
-  for (int k = 0; k < d; ++k) {
-    if (!std::isfinite(root_lo[k]) || !std::isfinite(root_hi[k]) || !(root_hi[k] > root_lo[k]))
+  if (n_roots < 1 || start_depth < 0) return fail(SPK_ERR_INVALID_PARAMETER, "need >= 1 root, start_depth >= 0");
+  for (long long q = 0; q < n_roots * d; ++q) {
+    if (!std::isfinite(root_lo[q]) || !std::isfinite(root_hi[q]) || !(root_hi[q] > root_lo[q]))
       return fail(SPK_ERR_INVALID_PARAMETER, "bounds must be finite with positive extent");
   }
   DeviceGuard g(net->device);
+  keep_pool_memory(net->device);
   cudaStream_t st = (cudaStream_t)stream;
   auto tree = new spk_tree();
+  tree->stream = st;
   tree->d = d;
   tree->device = net->device;
+  tree->start_depth = start_depth;
   const double stop = delta / std::sqrt((double)d);
   int rc = SPK_OK;
   TreeLevel cur;
-  if ((rc = alloc_level(cur, 1, d)) != SPK_OK) { delete tree; return rc; }
-  cudaMemcpyAsync(cur.lo, root_lo, d * sizeof(double), cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(cur.hi, root_hi, d * sizeof(double), cudaMemcpyHostToDevice, st);
-  const long long minus1 = -1;
-  cudaMemcpyAsync(cur.parent, &minus1, sizeof(long long), cudaMemcpyHostToDevice, st);
-  cudaMemsetAsync(cur.face, 0, 1, st);
+  if ((rc = alloc_level(cur, n_roots, d, st)) != SPK_OK) { delete tree; return rc; }
+  cudaMemcpyAsync(cur.lo, root_lo, n_roots * d * sizeof(double), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(cur.hi, root_hi, n_roots * d * sizeof(double), cudaMemcpyHostToDevice, st);
+  cudaMemsetAsync(cur.parent, 0xff, n_roots * sizeof(long long), st);  // -1
+  cudaMemsetAsync(cur.face, 0, n_roots, st);
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEventCreate(&ev0);
+  cudaEventCreate(&ev1);
   int* counts = nullptr;
   uint8_t* flag = nullptr;
   long long* small_idx = nullptr;
   double* fpts = nullptr;
   double* fvals = nullptr;
   long long cap = 0, fcap = 0;
-  for (int depth = 0; rc == SPK_OK; ++depth) {
+  int* h_counts = nullptr;
+  for (int depth = start_depth; rc == SPK_OK; ++depth) {
     const long long n = cur.n;
+    cudaEventRecord(ev0, st);
     rc = spk_bound_aabb(net, policy, n_keep, precision, n, cur.lo, cur.hi, cur.blo, cur.bhi, cur.label, st);
+    cudaEventRecord(ev1, st);
     if (rc != SPK_OK) break;
+    tree->launches += 3;
     tree->bound_evals += n;
     cudaMemsetAsync(cur.face, 0, n, st);
     const int nb = (int)((n + TB_THREADS - 1) / TB_THREADS);
     if (n > cap) {
-      cudaFree(counts); cudaFree(flag); cudaFree(small_idx);
-      cap = std::max<long long>(n, 1024);
+      if (counts) { cudaFreeAsync(counts, st); cudaFreeAsync(flag, st); cudaFreeAsync(small_idx, st); }
+      cap = std::max<long long>(2 * n, 1024);
       const long long nbc = (cap + TB_THREADS - 1) / TB_THREADS;
-      if (cudaMalloc(&counts, 2 * nbc * sizeof(int)) != cudaSuccess ||
-          cudaMalloc(&flag, cap) != cudaSuccess || cudaMalloc(&small_idx, cap * sizeof(long long)) != cudaSuccess) {
+      if (cudaMallocAsync(&counts, 2 * nbc * sizeof(int), st) != cudaSuccess ||
+          cudaMallocAsync(&flag, cap, st) != cudaSuccess ||
+          cudaMallocAsync(&small_idx, cap * sizeof(long long), st) != cudaSuccess) {
         rc = fail(SPK_ERR_OUT_OF_MEMORY, "tree scratch");
+        break;
+      }
+      if (!pinned_scratch(2 * nbc * sizeof(int), (void**)&h_counts)) {
+        rc = fail(SPK_ERR_OUT_OF_MEMORY, "tree host scratch");
         break;
       }
     }
@@ -255,26 +309,29 @@ int spk_tree_build(const spk_net* net, int policy, int n_keep, int precision, co
     int* bsmall = counts + nb;
     tree_mark_kernel<<<nb, TB_THREADS, 0, st>>>(n, d, cur.lo, cur.hi, cur.label, depth, max_depth, stop, flag,
                                                 bsplit, bsmall);
-    // totals: sum of block counts (small launch, then one D2H)
+    // totals: block counts to pinned host memory, one sync per level
     long long totals[2] = {0, 0};
     {
-      std::vector<int> hc(2 * (size_t)nb);
-      cudaError_t e = cudaMemcpyAsync(hc.data(), counts, 2 * nb * sizeof(int), cudaMemcpyDeviceToHost, st);
+      const int* hc = h_counts;
+      cudaError_t e = cudaMemcpyAsync(h_counts, counts, 2 * nb * sizeof(int), cudaMemcpyDeviceToHost, st);
       if (e == cudaSuccess) e = cudaStreamSynchronize(st);
       if (e != cudaSuccess) { rc = cuda_fail(e, "tree level"); break; }
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev0, ev1);
+      tree->bound_ms += ms;
       for (int b = 0; b < nb; ++b) { totals[0] += hc[b]; totals[1] += hc[nb + b]; }
     }
     const long long k = totals[0], m = totals[1];
     TreeLevel next;
-    if (k > 0 && (rc = alloc_level(next, 2 * k, d)) != SPK_OK) break;
+    if (k > 0 && (rc = alloc_level(next, 2 * k, d, st)) != SPK_OK) break;
     tree_scatter_kernel<<<nb, TB_THREADS, 0, st>>>(n, d, cur.lo, cur.hi, flag, bsplit, bsmall, k, next.lo, next.hi,
                                                    next.parent, small_idx);
     if (m > 0) {
       if (m * 2 * d > fcap) {
-        cudaFree(fpts); cudaFree(fvals);
+        if (fpts) { cudaFreeAsync(fpts, st); cudaFreeAsync(fvals, st); }
         fcap = m * 2 * d;
-        if (cudaMalloc(&fpts, fcap * d * sizeof(double)) != cudaSuccess ||
-            cudaMalloc(&fvals, fcap * sizeof(double)) != cudaSuccess) {
+        if (cudaMallocAsync(&fpts, fcap * d * sizeof(double), st) != cudaSuccess ||
+            cudaMallocAsync(&fvals, fcap * sizeof(double), st) != cudaSuccess) {
           rc = fail(SPK_ERR_OUT_OF_MEMORY, "face points");
           break;
         }
@@ -284,6 +341,7 @@ int spk_tree_build(const spk_net* net, int policy, int n_keep, int precision, co
                                                                                              cur.hi, fpts);
       rc = spk_eval_batch(net, precision, np, fpts, fvals, st);
       if (rc != SPK_OK) break;
+      tree->launches += 3;
       face_sign_kernel<<<(int)((m + TB_THREADS - 1) / TB_THREADS), TB_THREADS, 0, st>>>(m, d, small_idx, fvals,
                                                                                           cur.face);
     }
@@ -294,14 +352,17 @@ int spk_tree_build(const spk_net* net, int policy, int n_keep, int precision, co
     if (k == 0) break;
     cur = next;
   }
-  if (cur.lo) free_level(cur);
-  cudaFree(counts); cudaFree(flag); cudaFree(small_idx); cudaFree(fpts); cudaFree(fvals);
+  if (cur.lo) free_level(cur, st);
+  if (counts) { cudaFreeAsync(counts, st); cudaFreeAsync(flag, st); cudaFreeAsync(small_idx, st); }
+  if (fpts) { cudaFreeAsync(fpts, st); cudaFreeAsync(fvals, st); }
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
   if (rc == SPK_OK) {
     cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) rc = cuda_fail(e, "tree sync");
   }
   if (rc != SPK_OK) {
-    for (auto& L : tree->levels) free_level(L);
+    for (auto& L : tree->levels) free_level(L, st);
     delete tree;
     return rc;
   }
@@ -312,7 +373,7 @@ int spk_tree_build(const spk_net* net, int policy, int n_keep, int precision, co
 int spk_tree_destroy(spk_tree* tree) {
   if (!tree) return SPK_OK;
   DeviceGuard g(tree->device);
-  for (auto& L : tree->levels) free_level(L);
+  for (auto& L : tree->levels) free_level(L, tree->stream);
   delete tree;
   return SPK_OK;
 }
@@ -324,6 +385,32 @@ int spk_tree_info(const spk_tree* tree, int* n_levels, int64_t* n_nodes, int64_t
   if (n_levels) *n_levels = (int)tree->levels.size();
   if (n_nodes) *n_nodes = total;
   if (bound_evals) *bound_evals = tree->bound_evals;
+  return SPK_OK;
+}
+
+int spk_tree_level_copy(const spk_tree* tree, int level, double* lo, double* hi, double* bound_lo,
+                        double* bound_hi, int8_t* label, int8_t* face, int64_t* parent) {
+  if (!tree || level < 0 || level >= (int)tree->levels.size())
+    return fail(SPK_ERR_INVALID_PARAMETER, "bad tree level");
+  DeviceGuard g(tree->device);
+  const TreeLevel& L = tree->levels[level];
+  const size_t n = (size_t)L.n, d = (size_t)tree->d;
+  struct { void* dst; const void* src; size_t bytes; } cp[] = {
+      {lo, L.lo, n * d * sizeof(double)}, {hi, L.hi, n * d * sizeof(double)},
+      {bound_lo, L.blo, n * sizeof(double)}, {bound_hi, L.bhi, n * sizeof(double)},
+      {label, L.label, n}, {face, L.face, n}, {parent, L.parent, n * sizeof(int64_t)}};
+  for (auto& c : cp) {
+    if (!c.dst || !c.bytes) continue;
+    cudaError_t e = cudaMemcpy(c.dst, c.src, c.bytes, cudaMemcpyDefault);
+    if (e != cudaSuccess) return cuda_fail(e, "tree level copy");
+  }
+  return SPK_OK;
+}
+
+int spk_tree_stats(const spk_tree* tree, int64_t* launches, double* bound_ms) {
+  if (!tree) return fail(SPK_ERR_INVALID_PARAMETER, "null tree");
+  if (launches) *launches = tree->launches;
+  if (bound_ms) *bound_ms = tree->bound_ms;
   return SPK_OK;
 }
 

@@ -1,0 +1,324 @@
+"""k-d bounding trees on the B200 (reference spatial.py:41-289).
+
+`build_spatial_tree` keeps the reference contract (returns a TreeNode tree
+whose nodes carry AABB, SignClass, depth, children and face_sign).  The
+whole breadth-first build runs in the C-ABI (`spk_tree_build`, K5): fused
+bound kernel per level, ballot/prefix-sum compaction of UNKNOWN nodes into
+the next frontier, FP64 midpoint splits identical to the reference's.
+
+`build_spatial_tree_arrays` returns the same tree as flat per-level arrays
+(no Python objects) -- the throughput API for 10^5..10^7-node trees.
+`build_spatial_tree_sharded` splits the frontier across ranks (one process
+per GPU) with no collective on the inner loop.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from . import device as dv
+from .errors import DepthOverflow, DimensionMismatch, InvalidBounds, InvalidParameter
+from .network import _precision_code, device_net
+from .range_core import AFFINE_FULL, SignClass, policy_code
+
+_MAX_DEPTH = 60
+_SIGN = {1: SignClass.POSITIVE, -1: SignClass.NEGATIVE, 0: SignClass.UNKNOWN}
+
+
+@dataclass(frozen=True)
+class AABB:
+    lo: np.ndarray
+    hi: np.ndarray
+
+    def __post_init__(self):
+        lo = np.asarray(self.lo, dtype=np.float64)
+        hi = np.asarray(self.hi, dtype=np.float64)
+        if lo.shape != hi.shape or lo.ndim != 1:
+            raise InvalidBounds("corners must be 1-d points of equal dimension")
+        if not (np.all(np.isfinite(lo)) and np.all(np.isfinite(hi))):
+            raise InvalidBounds("non-finite bounds")
+        if np.any(lo > hi):
+            raise InvalidBounds("lower corner exceeds upper corner")
+        object.__setattr__(self, "lo", lo)
+        object.__setattr__(self, "hi", hi)
+
+    @classmethod
+    def _trusted(cls, lo, hi):
+        box = object.__new__(cls)
+        object.__setattr__(box, "lo", lo)
+        object.__setattr__(box, "hi", hi)
+        return box
+
+    @property
+    def dim(self) -> int:
+        return self.lo.shape[0]
+
+    @property
+    def center(self):
+        return (self.lo + self.hi) / 2.0
+
+    @property
+    def extents(self):
+        return self.hi - self.lo
+
+    @property
+    def volume(self) -> float:
+        return float(np.prod(self.extents))
+
+    def split(self):
+        """Halve along the widest dimension (ties to the lowest index)."""
+        ax = int(np.argmax(self.extents))
+        mid = 0.5 * (self.lo[ax] + self.hi[ax])
+        hi_a = self.hi.copy()
+        hi_a[ax] = mid
+        lo_b = self.lo.copy()
+        lo_b[ax] = mid
+        return AABB(self.lo, hi_a), AABB(lo_b, self.hi)
+
+    def face_centers(self):
+        c = self.center
+        half = self.extents / 2.0
+        pts = np.repeat(c[None, :], 2 * self.dim, axis=0)
+        for i in range(self.dim):
+            pts[2 * i, i] = c[i] - half[i]
+            pts[2 * i + 1, i] = c[i] + half[i]
+        return pts
+
+
+@dataclass
+class TreeNode:
+    aabb: AABB
+    sign: SignClass
+    depth: int
+    children: tuple | None = None
+    face_sign: int | None = None
+
+    @property
+    def is_leaf(self) -> bool:
+        return self.children is None
+
+
+def iter_leaves(root: TreeNode):
+    stack = [root]
+    while stack:
+        node = stack.pop()
+        if node.is_leaf:
+            yield node
+        else:
+            stack.extend(node.children)
+
+
+@dataclass(frozen=True)
+class TriangleMesh:
+    vertices: np.ndarray
+    triangles: np.ndarray
+
+    def __post_init__(self):
+        v = np.asarray(self.vertices, dtype=np.float64).reshape(-1, 3)
+        t = np.asarray(self.triangles, dtype=np.int64).reshape(-1, 3)
+        if v.size and not np.all(np.isfinite(v)):
+            raise InvalidParameter("mesh vertices must be finite")
+        if t.size and (t.min() < 0 or t.max() >= len(v)):
+            raise InvalidParameter("triangle indices out of range")
+        object.__setattr__(self, "vertices", v)
+        object.__setattr__(self, "triangles", t)
+
+
+@dataclass
+class TreeLevel:
+    """One breadth-first level: AABB corners, bound, label (+1/-1/0),
+    face annotation (+1/-1, 0 none), parent index into the previous level."""
+
+    lo: object
+    hi: object
+    bound_lo: object
+    bound_hi: object
+    label: object
+    face: object
+    parent: object
+
+    def __len__(self):
+        return int(self.label.shape[0])
+
+
+@dataclass
+class TreeArrays:
+    levels: list
+    start_depth: int = 0
+    bound_evals: int = 0
+    launches: int = 0
+    bound_ms: float = 0.0
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def n_nodes(self) -> int:
+        return sum(len(l) for l in self.levels)
+
+    def keys(self):
+        """Path keys per level (root 1, low child 2k, high child 2k+1)."""
+        out = [np.arange(1, len(self.levels[0]) + 1, dtype=np.int64)]
+        for lv in self.levels[1:]:
+            par = _np(lv.parent)
+            k = len(par) // 2
+            bit = np.concatenate([np.zeros(k, np.int64), np.ones(k, np.int64)])
+            out.append(out[-1][par] * 2 + bit)
+        return out
+
+
+def _np(x):
+    return x.cpu().numpy() if dv.is_tensor(x) else x
+
+
+def _check_domain(net, bounds: AABB):
+    if bounds.dim != net.input_dim:
+        raise DimensionMismatch(f"bounds in R^{bounds.dim}, network expects R^{net.input_dim}")
+    if np.any(bounds.extents <= 0.0):
+        raise InvalidBounds("bounds must have positive extent")
+
+
+class _TreeHandle:
+    """Owns an spk_tree*; destroyed when the last zero-copy view dies."""
+
+    def __init__(self, ptr):
+        self.ptr = ptr
+
+    def __del__(self):
+        if self.ptr:
+            _lib.load().spk_tree_destroy(self.ptr)
+            self.ptr = None
+
+
+class _DeviceView:
+    """__cuda_array_interface__ view of library-owned device memory."""
+
+    def __init__(self, owner, ptr, shape, typestr):
+        self.owner = owner
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None, "stream": None}
+
+
+def _build(net, roots_lo, roots_hi, start_depth, delta, policy, max_depth, precision, to_host, device=None):
+    pcode, n_keep = policy_code(policy)
+    dn = device_net(net, device)
+    roots_lo = np.ascontiguousarray(roots_lo, dtype=np.float64)
+    roots_hi = np.ascontiguousarray(roots_hi, dtype=np.float64)
+    handle = C.c_void_p()
+    stream = dv.stream_ptr(dn.device)
+    _lib.call(
+        "spk_tree_build", dn.ptr, pcode, n_keep, _precision_code(precision), roots_lo.shape[0],
+        roots_lo.ctypes.data, roots_hi.ctypes.data, int(start_depth),
+        -1 if max_depth is None else int(max_depth), float(delta), stream, C.byref(handle),
+    )
+    owner = _TreeHandle(handle)
+    lib = _lib.load()
+    nl, nn, be = C.c_int(), C.c_int64(), C.c_int64()
+    _lib.check(lib.spk_tree_info(handle, C.byref(nl), C.byref(nn), C.byref(be)))
+    la, ms = C.c_int64(), C.c_double()
+    _lib.check(lib.spk_tree_stats(handle, C.byref(la), C.byref(ms)))
+    d = net.input_dim
+    levels = []
+    for i in range(nl.value):
+        levels.append(_level(owner, i, d, dn.device, to_host))
+    return TreeArrays(levels, int(start_depth), be.value, la.value, ms.value)
+
+
+_LEVEL_SPECS = (("lo", "<f8", 2), ("hi", "<f8", 2), ("bound_lo", "<f8", 1), ("bound_hi", "<f8", 1),
+                ("label", "|i1", 1), ("face", "|i1", 1), ("parent", "<i8", 1))
+
+
+def _level(owner, level, d, device, to_host):
+    """One level as NumPy copies (to_host) or zero-copy CUDA tensors that keep
+    the library's tree alive."""
+    n = C.c_int64()
+    ptrs = [C.c_void_p() for _ in range(7)]
+    _lib.check(_lib.load().spk_tree_level(owner.ptr, level, C.byref(n), *[C.byref(p) for p in ptrs]))
+    n = n.value
+    if to_host:
+        out = [np.empty((n, d) if nd == 2 else (n,), np.dtype(ts)) for _, ts, nd in _LEVEL_SPECS]
+        _lib.call("spk_tree_level_copy", owner.ptr, level, *[a.ctypes.data for a in out])
+        return TreeLevel(*out)
+    torch = dv._torch()
+    out = []
+    for (name, ts, nd), p in zip(_LEVEL_SPECS, ptrs):
+        shape = (n, d) if nd == 2 else (n,)
+        out.append(torch.as_tensor(_DeviceView(owner, p.value or 0, shape, ts), device=f"cuda:{device}"))
+    return TreeLevel(*out)
+
+
+def build_spatial_tree_arrays(net, bounds: AABB, delta: float = 0.001, policy=AFFINE_FULL,
+                              max_depth: int | None = None, precision: str = "fp32",
+                              to_host: bool = True) -> TreeArrays:
+    """build_spatial_tree as flat per-level arrays (see module docstring)."""
+    _check_domain(net, bounds)
+    if delta <= 0.0:
+        raise InvalidParameter("delta must be positive")
+    if max_depth is not None and max_depth > _MAX_DEPTH:
+        raise DepthOverflow(f"fixed depth {max_depth} exceeds {_MAX_DEPTH}")
+    return _build(net, bounds.lo[None, :], bounds.hi[None, :], 0, delta, policy, max_depth, precision, to_host)
+
+
+def build_spatial_tree(net, bounds: AABB, delta: float = 0.001, policy=AFFINE_FULL,
+                       max_depth: int | None = None, precision: str = "fp32") -> TreeNode:
+    """Breadth-first k-d bounding tree of the level set (spatial.py:214-289)."""
+    arrays = build_spatial_tree_arrays(net, bounds, delta, policy, max_depth, precision, to_host=True)
+    return materialize(arrays)
+
+
+def materialize(arrays: TreeArrays) -> TreeNode:
+    """TreeNode objects from level arrays (reference node layout)."""
+    prev = None
+    root = None
+    for depth, lv in enumerate(arrays.levels):
+        lo, hi = _np(lv.lo), _np(lv.hi)
+        lab, face, par = _np(lv.label), _np(lv.face), _np(lv.parent)
+        nodes = [
+            TreeNode(AABB._trusted(lo[i], hi[i]), _SIGN[int(lab[i])], arrays.start_depth + depth, None,
+                     None if face[i] == 0 else int(face[i]))
+            for i in range(len(lab))
+        ]
+        if prev is None:
+            root = nodes[0]
+        else:
+            k = len(nodes) // 2
+            for j in range(k):
+                prev[int(par[j])].children = (nodes[j], nodes[k + j])
+        prev = nodes
+    return root
+
+
+def build_spatial_tree_sharded(net, bounds: AABB, max_depth: int, policy, rank: int, world: int,
+                               precision: str = "fp32", min_roots_per_rank: int = 64,
+                               to_host: bool = False) -> TreeArrays:
+    """Fixed-depth build split across `world` ranks (one per GPU).
+
+    Every rank builds the top levels redundantly until the UNKNOWN frontier
+    holds >= min_roots_per_rank * world nodes (or max_depth is reached), then
+    refines its contiguous slice of that frontier to max_depth.  No
+    collective runs inside the build; the union of the ranks' levels below
+    the cut equals the unsharded tree (node AABBs are bit-identical because
+    splits are exact FP64 midpoints).
+    """
+    _check_domain(net, bounds)
+    cut = 0
+    top = None
+    while True:
+        top = build_spatial_tree_arrays(net, bounds, 1.0, policy, cut, precision, to_host=True)
+        last = top.levels[-1]
+        n_open = int((_np(last.label) == 0).sum())
+        if cut >= max_depth or n_open >= min_roots_per_rank * world or n_open == 0:
+            break
+        cut += max(1, int(np.ceil(np.log2(max(1, min_roots_per_rank * world) / max(1, n_open)))))
+        cut = min(cut, max_depth)
+    last = top.levels[-1]
+    open_idx = np.flatnonzero(_np(last.label) == 0)
+    part = np.array_split(open_idx, world)[rank]
+    if cut >= max_depth or part.size == 0:
+        top.meta.update(cut=cut, roots=int(part.size), top_nodes=top.n_nodes)
+        return top
+    sub = _build(net, _np(last.lo)[part], _np(last.hi)[part], cut, 1.0, policy, max_depth, precision, to_host)
+    sub.meta.update(cut=cut, roots=int(part.size), top_nodes=top.n_nodes, top_levels=top.levels)
+    return sub

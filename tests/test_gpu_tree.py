@@ -1,0 +1,126 @@
+"""K5 tree build on the GPU vs the reference's golden trees and the oracle.
+
+FP64 kernels: topology, AABBs (bit-exact), labels and face annotations equal
+the reference's.  FP32 kernels: on the common subtree (nodes present in both
+trees, matched by path key) AABBs are bit-identical and labels agree wherever
+both are definite; every node FP32 certifies is checked by dense sampling.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2202_02444_b200 as sp
+from oracle import spelunk_oracle as orc
+from paper_2202_02444_b200 import spatial
+from tests.test_oracle_golden import TREES, golden_tree
+
+pytestmark = pytest.mark.gpu
+BOUNDS = spatial.AABB(-np.ones(3), np.ones(3))
+GPU_TREES = {k: v for k, v in TREES.items() if v[1]["policy"] in ("affine-fixed", "interval")}
+
+
+def by_key(keys, *arrays):
+    order = np.argsort(keys)
+    return (keys[order],) + tuple(a[order] for a in arrays)
+
+
+@pytest.mark.parametrize("tag", sorted(GPU_TREES))
+def test_tree_fp64_equals_reference(golden, net_paths, tag):
+    netname, kw = GPU_TREES[tag]
+    net = sp.load_network(net_paths[netname])
+    arr = spatial.build_spatial_tree_arrays(net, BOUNDS, precision="fp64", **kw)
+    want = golden_tree(golden, tag)
+    keys = arr.keys()
+    assert len(arr.levels) == len(want)
+    for lv, k, w in zip(arr.levels, keys, want):
+        k1, lab, face, lo, hi = by_key(k, lv.label, lv.face, lv.lo, lv.hi)
+        k2, wl, wf, wlo, whi = by_key(w["keys"], w["sign"], w["face"], w["lo"], w["hi"])
+        np.testing.assert_array_equal(k1, k2)
+        np.testing.assert_array_equal(lab, wl)
+        np.testing.assert_array_equal(face, wf)
+        np.testing.assert_array_equal(lo, wlo)
+        np.testing.assert_array_equal(hi, whi)
+
+
+@pytest.mark.parametrize("tag", sorted(GPU_TREES))
+def test_tree_fp32_common_subtree(golden, net_paths, tag):
+    netname, kw = GPU_TREES[tag]
+    net = sp.load_network(net_paths[netname])
+    arr = spatial.build_spatial_tree_arrays(net, BOUNDS, precision="fp32", **kw)
+    want = golden_tree(golden, tag)
+    rng = np.random.default_rng(0)
+    onet = orc.as_oracle_net(net)
+    mism = 0
+    for lv, k, w in zip(arr.levels, arr.keys(), want):
+        common, ia, ib = np.intersect1d(k, w["keys"], return_indices=True)
+        np.testing.assert_array_equal(lv.lo[ia], w["lo"][ib])
+        np.testing.assert_array_equal(lv.hi[ia], w["hi"][ib])
+        a, b = lv.label[ia], w["sign"][ib]
+        both = (a != 0) & (b != 0)
+        np.testing.assert_array_equal(a[both], b[both])
+        mism += int(np.sum(a != b))
+        # soundness of FP32 certifications
+        cert = np.flatnonzero(lv.label != 0)[:200]
+        if cert.size:
+            pts = rng.uniform(lv.lo[cert][:, None, :], lv.hi[cert][:, None, :], (cert.size, 16, 3))
+            vals = orc.eval_points(onet, pts.reshape(-1, 3)).reshape(cert.size, -1)
+            sign = lv.label[cert][:, None]
+            assert np.all(np.where(sign > 0, vals > 0, vals < 0))
+    print(f"{tag}: FP32 label mismatches on common subtree {mism}")
+
+
+def test_tree_materialize_matches_reference_api(net_paths):
+    net = sp.load_network(net_paths["box"])
+    root = spatial.build_spatial_tree(net, BOUNDS, policy=sp.AFFINE_FIXED, max_depth=6)
+    depths = [l.depth for l in spatial.iter_leaves(root)]
+    assert max(depths) == 6
+    vol = sum(l.aabb.volume for l in spatial.iter_leaves(root))
+    assert abs(vol - 8.0) <= 1e-9
+    for leaf in spatial.iter_leaves(root):
+        if leaf.depth < 6:
+            assert leaf.sign is not sp.SignClass.UNKNOWN
+
+
+def test_tree_convergence_mode_interval(golden, net_paths):
+    """Convergence mode with face annotations vs the oracle (interval policy)."""
+    net = sp.load_network(net_paths["box"])
+    arr = spatial.build_spatial_tree_arrays(net, BOUNDS, delta=0.1, policy="interval", precision="fp64")
+    levels = orc.tree_levels(orc.as_oracle_net(net), -np.ones(3), np.ones(3), "interval", delta=0.1)
+    okeys = orc.node_keys(levels)
+    assert len(arr.levels) == len(levels)
+    for lv, k, ol, ok in zip(arr.levels, arr.keys(), levels, okeys):
+        k1, lab, face = by_key(k, lv.label, lv.face)
+        k2, wl, wf = by_key(ok, ol["label"], ol["face"])
+        np.testing.assert_array_equal(k1, k2)
+        np.testing.assert_array_equal(lab, wl)
+        np.testing.assert_array_equal(face, wf)
+
+
+def test_depth_overflow(net_paths):
+    net = sp.load_network(net_paths["box"])
+    with pytest.raises(sp.errors.DepthOverflow):
+        spatial.build_spatial_tree(net, BOUNDS, max_depth=61)
+
+
+def test_sharded_union_equals_full(net_paths):
+    """Frontier sharding: the union of 4 ranks' sub-trees = the full tree."""
+    net = sp.load_network(net_paths["relu4x32"])
+    full = spatial.build_spatial_tree_arrays(net, BOUNDS, policy="affine-fixed", max_depth=9)
+    fk = full.keys()
+    world = 4
+    parts = [spatial.build_spatial_tree_sharded(net, BOUNDS, 9, "affine-fixed", r, world, min_roots_per_rank=2, to_host=True)
+             for r in range(world)]
+    cut = parts[0].meta["cut"]
+    for depth in range(cut + 1, 10):
+        got = []
+        for p in parts:
+            if "top_levels" not in p.meta or depth - cut >= len(p.levels):
+                continue
+            # keys of a shard are relative to its roots; compare labels+AABBs as sets
+            lv = p.levels[depth - cut]
+            got.append(np.concatenate([lv.lo, lv.hi, lv.label[:, None].astype(float)], axis=1))
+        got = np.concatenate(got) if got else np.zeros((0, 7))
+        ref = full.levels[depth]
+        want = np.concatenate([ref.lo, ref.hi, ref.label[:, None].astype(float)], axis=1)
+        assert got.shape == want.shape
+        np.testing.assert_array_equal(np.unique(got, axis=0), np.unique(want, axis=0))

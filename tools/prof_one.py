@@ -1,0 +1,47 @@
+"""One warm launch of a fused bound kernel, for ncu captures.
+
+    python tools/prof_one.py c2level   # depth-18 level of C2 (262,144 AABBs, 8x256 ReLU, affine-fixed)
+    python tools/prof_one.py c5 [n]    # n on-device cubes through 8x256 (default 2^20)
+    python tools/prof_one.py c1        # 64^3 grid through 4x32
+"""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import paper_2202_02444_b200 as sp  # noqa: E402
+from paper_2202_02444_b200 import synth  # noqa: E402
+
+
+def main():
+    which = sys.argv[1] if len(sys.argv) > 1 else "c2level"
+    torch.cuda.set_device(0)
+    if which == "c2level":
+        net = synth.config_net("C2")
+        c, a = synth.grid_cubes(64)
+        lo_c = torch.from_numpy(c - 1 / 64).cuda()
+        hi_c = torch.from_numpy(c + 1 / 64).cuda()
+        run = lambda: sp.bound_aabb(net, lo_c, hi_c, sp.AFFINE_FIXED)
+    elif which == "c5":
+        n = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 20
+        net = synth.config_net("C5_256")
+        run = lambda: sp.bound_random_cubes(net, n, seed=1, half=1 / 64)
+    else:
+        net = synth.config_net("C1")
+        c, a = synth.grid_cubes(64)
+        ct, at = torch.from_numpy(c).cuda(), torch.from_numpy(a).cuda()
+        run = lambda: sp.range_bound_batch(net, ct, at, sp.AFFINE_FIXED)
+    for _ in range(3):
+        run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    run()
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"{which}: {e0.elapsed_time(e1):.3f} ms")
+
+
+if __name__ == "__main__":
+    main()
