@@ -158,6 +158,22 @@ int spk_tree_level(const spk_tree* tree, int level, int64_t* n, const double** l
                    const double** bound_lo, const double** bound_hi, const int8_t** label,
                    const int8_t** face, const int64_t** parent);
 
+/* K6: range-marching ray caster (_march_arrays, rays.py:88-138).
+ * Device pointers: origins (n x 3, or 3 values when origin_stride == 0),
+ * dirs (n x 3 unit vectors), optional t_init / sigma_init (n each, NULL =
+ * 0 / sigma0).  params6 (host): t_max, sigma0, eta_plus, eta_minus, delta,
+ * safety (RayCastParams, rays.py:48-71).  Outputs (device): hit (n bytes),
+ * t (n, +inf on miss), steps (n, probes per ray).  stats (host, optional,
+ * 3 x int64): lock-step rounds, ray-steps, certified steps. */
+int spk_march(const spk_net* net, int policy, int n_keep, int precision, int64_t n, const double* origins,
+              int64_t origin_stride, const double* dirs, const double* t_init, const double* sigma_init,
+              const double* params6, uint8_t* hit, double* t_out, double* steps, int64_t* stats,
+              void* stream);
+/* Camera.pixel_dirs (camera.py:82-92) on the device, bit-exact: frame9 =
+ * forward, right, true_up (host), dirs (device) = height x width x 3. */
+int spk_camera_dirs(const double* frame9, double half_w, double half_h, int width, int height,
+                    double* dirs, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

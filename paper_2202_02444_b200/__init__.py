@@ -41,4 +41,16 @@ from .range_core import (
     sign_classes,
 )
 
+from .camera import Camera
+from .rays import HitResult, Ray, RayCastParams, cast_camera, cast_ray, cast_rays, march_arrays
+from .spatial import (
+    AABB,
+    TreeNode,
+    TriangleMesh,
+    build_spatial_tree,
+    build_spatial_tree_arrays,
+    build_spatial_tree_sharded,
+    iter_leaves,
+)
+
 __version__ = "0.1.0"

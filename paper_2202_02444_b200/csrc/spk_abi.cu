@@ -100,7 +100,9 @@ int build_device_net(spk_net* net, DevNet<T>& dn) {
   std::vector<double> gam(net->layers.size());
   for (size_t l = 0; l < net->layers.size(); ++l) {
     const HostLayer& L = net->layers[l];
-    const bool narrow = L.m_out <= NARROW_MAX;
+    // only the final (width-1) layer takes the warp-reduction path; every
+    // hidden layer streams through the W tile ring
+    const bool narrow = (l + 1 == net->layers.size()) && L.m_out <= NARROW_MAX;
     int n_eff;
     if (narrow) {
       n_eff = (L.m_in + 31) / 32 + 6;
@@ -160,7 +162,7 @@ int build_device_net(spk_net* net, DevNet<T>& dn) {
     LayerDev<T>& D = nd.L[l];
     D.m_in = L.m_in;
     D.m_out = L.m_out;
-    D.narrow = L.m_out <= NARROW_MAX;
+    D.narrow = (l + 1 == net->layers.size()) && L.m_out <= NARROW_MAX;
     D.ntiles = D.narrow ? 0 : (L.m_in + KT - 1) / KT;
     D.n_act = (int)L.acts.size();
     for (int a = 0; a < D.n_act; ++a) D.act[a] = L.acts[a];

@@ -36,18 +36,86 @@ SPK_DEV double random_coord(unsigned long long seed, long long idx, int k, int d
   return (double)(z >> 11) * 0x1.0p-53 * 2.0 - 1.0;
 }
 
+// Inputs of one tile of NB boxes -> X rows [0, d) (packed columns), zeros
+// in rows [d, MMAX).  Shared by the fixed-shape and the symbol-carrying kernels.
+template <typename T, int C, int MMAX, int MODE>
+SPK_DEV void prep_inputs(const NetDev<T>& net, const BoxInput& in, long long n, long long g0, T* X, int tid,
+                         bool pack) {
+  using CF = Cfg<T, C, MMAX>;
+  constexpr int NB = CF::NB, CP = CF::CP;
+  const int d = net.d;
+  for (int q = tid; q < MMAX * NB; q += NT) {
+    const int k = q / NB, b = q % NB;
+    const long long gb = g0 + b;
+    T packed[CP];
+#pragma unroll
+    for (int c = 0; c < CP; ++c) packed[c] = T(0);
+    if (k < d && gb < n) {
+      State<T, C, MODE> st;
+      double centre;
+      double ax[3] = {0.0, 0.0, 0.0};
+      int n_ax = 0;
+      if (in.kind == IN_BOXES || in.kind == IN_POINTS) {
+        centre = in.a[gb * d + k];
+        if (in.kind == IN_BOXES) {
+          n_ax = in.s < 3 ? in.s : 3;
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            if (j < n_ax) ax[j] = in.b[(gb * in.s + j) * d + k];
+        }
+      } else if (in.kind == IN_AABB) {
+        const double l = in.a[gb * d + k], h = in.b[gb * d + k];
+        centre = (l + h) / 2.0;  // spatial.py:182-183, exact halving
+        n_ax = d < 3 ? d : 3;
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          if (j == k) ax[j] = (h - l) / 2.0;
+      } else {
+        centre = random_coord(in.seed, in.first + gb, k, d);
+        n_ax = d < 3 ? d : 3;
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          if (j == k) ax[j] = in.half;
+      }
+      input_state<T, C, MODE>(centre, ax, n_ax, 1, st);
+      if (pack) {
+        for (int a = 0; a < net.n_pre; ++a) apply_act<T, C, MODE>(st, net.pre_act[a]);
+        pack_next<T, C, MODE>(st, net.gamma_first, packed);
+      } else {
+        packed[0] = st.base;
+        if (MODE == MODE_AFFINE) {
+#pragma unroll
+          for (int j = 0; j < State<T, C, MODE>::S; ++j) packed[1 + j] = st.A[j];
+        }
+        packed[C - 1] = st.e;
+      }
+    }
+    T* dst = X + (size_t)k * CF::RS + b * CP;
+#pragma unroll
+    for (int c = 0; c < CP; ++c) dst[c] = packed[c];
+  }
+}
+
+template <typename T, int C, int MODE>
+SPK_DEV void emit_bounds(const BoundOutput& out, long long gb, const State<T, C, MODE>& st) {
+  double lo, hi;
+  final_bounds<T, C, MODE>(st, lo, hi);
+  out.lo[gb] = lo;
+  if (out.hi) out.hi[gb] = hi;
+  if (out.cls) out.cls[gb] = (int8_t)(lo > 0.0 ? 1 : (hi < 0.0 ? -1 : 0));
+}
+
 template <typename T, int C, int MMAX, int MODE>
 __global__ void __launch_bounds__(NT, 1)
     bound_kernel(const NetDev<T> net, const BoxInput in, const BoundOutput out, const long long n) {
   using CF = Cfg<T, C, MMAX>;
-  constexpr int NB = CF::NB, CP = CF::CP;
+  constexpr int NB = CF::NB;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* X = reinterpret_cast<T*>(smem_raw);
   T* Wst = X + CF::XS;
   T* NBUF = Wst + NSTAGE * CF::TILE;
   uint64_t* full = reinterpret_cast<uint64_t*>(NBUF + CF::NBUF);
   const int tid = threadIdx.x;
-  const int d = net.d;
 
   const long long nbt = (n + NB - 1) / NB;
   const long long mine = blockIdx.x < nbt ? (nbt - 1 - blockIdx.x) / gridDim.x + 1 : 0;
@@ -61,52 +129,10 @@ __global__ void __launch_bounds__(NT, 1)
 
   for (long long tile = blockIdx.x; tile < nbt; tile += gridDim.x) {
     const long long g0 = tile * NB;
-    // ---- inputs -> X rows [0, d); zeros elsewhere
-    for (int q = tid; q < MMAX * NB; q += NT) {
-      const int k = q / NB, b = q % NB;
-      const long long gb = g0 + b;
-      T packed[CP];
-#pragma unroll
-      for (int c = 0; c < CP; ++c) packed[c] = T(0);
-      if (k < d && gb < n) {
-        State<T, C, MODE> st;
-        double centre;
-        double ax[3] = {0.0, 0.0, 0.0};
-        int n_ax = 0;
-        if (in.kind == IN_BOXES || in.kind == IN_POINTS) {
-          centre = in.a[gb * d + k];
-          if (in.kind == IN_BOXES) {
-            n_ax = in.s < 3 ? in.s : 3;
-            for (int j = 0; j < n_ax; ++j) ax[j] = in.b[(gb * in.s + j) * d + k];
-          }
-        } else if (in.kind == IN_AABB) {
-          const double l = in.a[gb * d + k], h = in.b[gb * d + k];
-          centre = (l + h) / 2.0;  // spatial.py:182-183, exact halving
-          n_ax = d < 3 ? d : 3;
-          if (k < 3) ax[k] = (h - l) / 2.0;
-        } else {
-          centre = random_coord(in.seed, in.first + gb, k, d);
-          n_ax = d < 3 ? d : 3;
-          if (k < 3) ax[k] = in.half;
-        }
-        input_state<T, C, MODE>(centre, ax, n_ax, 1, st);
-        for (int a = 0; a < net.n_pre; ++a) apply_act<T, C, MODE>(st, net.pre_act[a]);
-        pack_next<T, C, MODE>(st, net.gamma_first, packed);
-      }
-      T* dst = X + (size_t)k * CF::RS + b * CP;
-#pragma unroll
-      for (int c = 0; c < CP; ++c) dst[c] = packed[c];
-    }
+    prep_inputs<T, C, MMAX, MODE>(net, in, n, g0, X, tid, true);
     __syncthreads();
-
     auto emit = [&](int b, const State<T, C, MODE>& st) {
-      const long long gb = g0 + b;
-      if (gb >= n) return;
-      double lo, hi;
-      final_bounds<T, C, MODE>(st, lo, hi);
-      out.lo[gb] = lo;
-      if (out.hi) out.hi[gb] = hi;
-      if (out.cls) out.cls[gb] = (int8_t)(lo > 0.0 ? 1 : (hi < 0.0 ? -1 : 0));
+      if (g0 + b < n) emit_bounds<T, C, MODE>(out, g0 + b, st);
     };
     run_layers<T, C, MMAX, MODE>(net, X, NBUF, ring, tid, emit);
   }

@@ -60,9 +60,12 @@ struct NetDev {
 
 template <typename T, int C, int MMAX>
 struct Cfg {
-  static constexpr int TI = sizeof(T) == 4 ? 8 : 4;
-  static constexpr int TB = C == 1 ? (sizeof(T) == 4 ? 8 : 4) : (C == 2 ? 4 : 2);
-  static constexpr int CP = C == 1 ? 1 : (C == 2 ? 2 : (C <= 4 ? 4 : ((C + 1) / 2) * 2));
+  static constexpr int VEC = 16 / (int)sizeof(T);  // elements per 16-byte vector
+  // register tile: TI neurons x TB boxes x C columns per thread
+  static constexpr int TI = C <= 6 ? (sizeof(T) == 4 ? 8 : 4)
+                                   : (C <= 20 ? VEC : (VEC / 2 > 0 ? VEC / 2 : 1));
+  static constexpr int TB = C == 1 ? (sizeof(T) == 4 ? 8 : 4) : (C == 2 ? 4 : (C <= 6 ? 2 : 1));
+  static constexpr int CP = C == 1 ? 1 : (C == 2 ? 2 : (C <= 4 ? 4 : (C <= 6 ? 6 : ((C + VEC - 1) / VEC) * VEC)));
   static constexpr int NG = MMAX / TI;
   static constexpr int NBG = NT / NG;
   static constexpr int NB = NBG * TB;
@@ -75,17 +78,23 @@ struct Cfg {
   static constexpr int RS0 = ((NB * CP * (int)sizeof(T) + 15) / 16) * 16 / (int)sizeof(T);
   static constexpr int RS = ((RS0 * (int)sizeof(T) / 16) % 2 == 1) ? RS0 : RS0 + 16 / (int)sizeof(T);
   static constexpr int XS = MMAX * RS;                   // elements of X
-  // a thread's TI neurons: TI/G groups of G consecutive neurons (G = one
-  // 16-byte vector); group q of neuron-group ng starts at q*NG*G + ng*G, so
-  // a warp's vector loads of a W row are contiguous (bank-conflict free)
-  static constexpr int G = 16 / (int)sizeof(T);
+  // a thread's TI neurons: TI/G groups of G consecutive neurons (G elements
+  // = one vector load); group q of neuron-group ng starts at q*NG*G + ng*G,
+  // so a warp's vector loads of a W row are contiguous (bank-conflict free)
+  static constexpr int G = TI < VEC ? TI : VEC;
   static constexpr int NBUF = NB * NARROW_MAX * CP;      // narrow-layer staging
   static constexpr size_t SMEM = sizeof(T) * (size_t)(XS + NSTAGE * TILE + NBUF) + 64;
   static_assert(NG >= 1 && NG <= NT && NT % NG == 0, "tile shape");
   static_assert((TB * CP * sizeof(T)) % 16 == 0, "vector loads of X");
-  static_assert((TI * sizeof(T)) % 16 == 0, "vector loads of W");
+  static_assert(TI % G == 0, "W vector groups");
   SPK_DEV static int neuron(int ng, int ti) { return (ti / G) * (NG * G) + ng * G + (ti % G); }
 };
+
+// copy N bytes (N in {4, 8, 16}) between 16/8/4-aligned addresses as one access
+template <int N> struct VecOf;
+template <> struct VecOf<16> { using type = float4; };
+template <> struct VecOf<8> { using type = float2; };
+template <> struct VecOf<4> { using type = float; };
 
 // ------------------------------------------------------------ mbarrier/TMA
 SPK_DEV uint32_t smem_u32(const void* p) {
@@ -246,14 +255,13 @@ SPK_DEV void final_bounds(const State<T, C, MODE>& st, double& lo, double& hi) {
 // round-to-nearest columns are summed in blocks of SUB k-steps (fresh
 // partials added to the running sums), so the rounding budget is
 // gamma_{SUB + ceil(m_in/SUB) + 1} instead of gamma_{m_in + 1}.
-template <typename T, int C, int MMAX, int MODE>
-SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, MMAX>& ring, int tid,
-                           bool last, T gamma_next) {
+template <typename T, int C, int MMAX>
+SPK_DEV void dense_kloop(const LayerDev<T>& L, const T* __restrict__ X, WRing<T, C, MMAX>& ring, int tid,
+                         T (&acc)[Cfg<T, C, MMAX>::TI][Cfg<T, C, MMAX>::TB][C]) {
   using CF = Cfg<T, C, MMAX>;
-  constexpr int TI = CF::TI, TB = CF::TB, CP = CF::CP, NB = CF::NB, KT = CF::KT;
+  constexpr int TI = CF::TI, TB = CF::TB, CP = CF::CP, KT = CF::KT;
   const int ng = tid % CF::NG, bg = tid / CF::NG;
 
-  T acc[TI][TB][C];
 #pragma unroll
   for (int ti = 0; ti < TI; ++ti) {
     const int i = CF::neuron(ng, ti);
@@ -293,10 +301,11 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
 
   // fragment loads for one k-step (W: TI values, X: TB*CP values)
   auto load_frag = [&](const T* __restrict__ Ws, const T* __restrict__ Xt, int kk, T* w, T* x) {
-    float4* wd = reinterpret_cast<float4*>(w);
+    using WV = typename VecOf<CF::G * (int)sizeof(T)>::type;
+    WV* wd = reinterpret_cast<WV*>(w);
 #pragma unroll
     for (int q = 0; q < TI / CF::G; ++q)
-      wd[q] = *reinterpret_cast<const float4*>(Ws + kk * MMAX + q * (CF::NG * CF::G) + ng * CF::G);
+      wd[q] = *reinterpret_cast<const WV*>(Ws + kk * MMAX + q * (CF::NG * CF::G) + ng * CF::G);
     const float4* xp = reinterpret_cast<const float4*>(Xt + (size_t)kk * CF::RS);
     float4* xd = reinterpret_cast<float4*>(x);
 #pragma unroll
@@ -344,6 +353,16 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
     ring.release(tid);
   }
   if (since > 0) flush();
+}
+
+template <typename T, int C, int MMAX, int MODE>
+SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, MMAX>& ring, int tid,
+                           bool last, T gamma_next) {
+  using CF = Cfg<T, C, MMAX>;
+  constexpr int TI = CF::TI, TB = CF::TB, CP = CF::CP;
+  const int ng = tid % CF::NG, bg = tid / CF::NG;
+  T acc[TI][TB][C];
+  dense_kloop<T, C, MMAX>(L, X, ring, tid, acc);
 
   // epilogue: activation rules, write next X in place (one contiguous
   // TB*CP vector per neuron: the thread's boxes are adjacent in the row)

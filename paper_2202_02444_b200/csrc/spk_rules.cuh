@@ -60,8 +60,10 @@ SPK_DEV double elu64(double x) { return x >= 0.0 ? x : expm1(x); }
 // range_core.py:238-264.  g = elu(x) - a x is convex, so its max is at an
 // endpoint and its global minimum is (a - 1) - a ln a (tangent point
 // x* = ln a); with a <= 0 (secant underflow) g = elu - a x is monotone.
+#define SPK_RULE __device__ __noinline__
+
 template <typename T>
-SPK_DEV int elu_affine(T lo_t, T hi_t, T& alpha, T& beta, T& gamma) {
+SPK_RULE int elu_affine(T lo_t, T hi_t, T& alpha, T& beta, T& gamma) {
   const double lo = (double)lo_t, hi = (double)hi_t;
   if (lo >= 0.0) { alpha = T(1); beta = T(0); gamma = T(0); return 0; }
   const double flo = elu64(lo), fhi = elu64(hi);
@@ -100,7 +102,7 @@ SPK_DEV void cos_range64(double lo, double hi, double& cmin, double& cmax) {
 // extremes among lo, hi and the first two 2pi-translates (at/after lo) of
 // +-arccos(alpha).
 template <typename T>
-SPK_DEV int sin_affine(T lo_t, T hi_t, T& alpha, T& beta, T& gamma) {
+SPK_RULE int sin_affine(T lo_t, T hi_t, T& alpha, T& beta, T& gamma) {
   const double lo = (double)lo_t, hi = (double)hi_t;
   double cmin, cmax;
   cos_range64(lo, hi, cmin, cmax);
@@ -132,7 +134,7 @@ SPK_DEV int sin_affine(T lo_t, T hi_t, T& alpha, T& beta, T& gamma) {
 // range_core.py:297-317: secant slope; remainder extremes at lo, hi and
 // +-artanh(sqrt(1 - alpha)) clamped into [lo, hi].
 template <typename T>
-SPK_DEV int tanh_affine(T lo_t, T hi_t, T& alpha, T& beta, T& gamma) {
+SPK_RULE int tanh_affine(T lo_t, T hi_t, T& alpha, T& beta, T& gamma) {
   const double lo = (double)lo_t, hi = (double)hi_t;
   const double flo = tanh(lo), fhi = tanh(hi);
   const double a = (hi == lo) ? 1.0 - flo * flo : (fhi - flo) / (hi - lo);
@@ -170,12 +172,21 @@ SPK_DEV int affine_rule(int act, T lo, T hi, T& alpha, T& beta, T& gamma) {
 // ------------------------------------------------------- interval images
 // range_core.py:326-349, rounded outward.
 template <typename T>
+SPK_RULE void interval_image_slow(int act, T lo, T hi, T& out_lo, T& out_hi);
+
+template <typename T>
 SPK_DEV void interval_image(int act, T lo, T hi, T& out_lo, T& out_hi) {
+  if (act == ACT_RELU) {
+    out_lo = fmax(lo, T(0));
+    out_hi = fmax(hi, T(0));
+    return;
+  }
+  interval_image_slow<T>(act, lo, hi, out_lo, out_hi);
+}
+
+template <typename T>
+SPK_RULE void interval_image_slow(int act, T lo, T hi, T& out_lo, T& out_hi) {
   switch (act) {
-    case ACT_RELU:
-      out_lo = fmax(lo, T(0));
-      out_hi = fmax(hi, T(0));
-      return;
     case ACT_ELU: {
       const double a = elu64((double)lo), b = elu64((double)hi);
       out_lo = lo >= T(0) ? lo : Num<T>::from_d_rd(a - pad64(fabs(a)));
@@ -208,8 +219,8 @@ SPK_DEV void interval_image(int act, T lo, T hi, T& out_lo, T& out_hi) {
 // Pointwise value (network.py:149-160), used by point evaluation.
 template <typename T> SPK_DEV T act_value(int act, T x);
 template <> SPK_DEV float act_value<float>(int act, float x) {
+  if (act == ACT_RELU) return fmaxf(x, 0.f);
   switch (act) {
-    case ACT_RELU: return fmaxf(x, 0.f);
     case ACT_ELU: return x >= 0.f ? x : expm1f(x);
     case ACT_SIN: return sinf(x);
     case ACT_TANH: return tanhf(x);
@@ -217,8 +228,8 @@ template <> SPK_DEV float act_value<float>(int act, float x) {
   }
 }
 template <> SPK_DEV double act_value<double>(int act, double x) {
+  if (act == ACT_RELU) return fmax(x, 0.0);
   switch (act) {
-    case ACT_RELU: return fmax(x, 0.0);
     case ACT_ELU: return x >= 0.0 ? x : expm1(x);
     case ACT_SIN: return sin(x);
     case ACT_TANH: return tanh(x);

@@ -1,0 +1,163 @@
+"""Range-marching ray casting on the B200 (reference rays.py:30-184).
+
+`cast_rays` / `cast_ray` keep the reference contract (lists of Ray in,
+HitResult out; default policy affine-fixed).  The whole march runs in the
+C-ABI (`spk_march`, K6): FP64 ray state, lock-step rounds over the compacted
+active set, one point-evaluation and one bound pass per round.
+`march_arrays` is the array API (NumPy or CUDA tensors) and `cast_camera`
+marches every pixel of a camera with directions generated on the device.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from . import device as dv
+from .camera import Camera
+from .errors import InvalidParameter, InvalidRay
+from .network import _precision_code, device_net
+from .range_core import AFFINE_FIXED, policy_code
+
+
+@dataclass(frozen=True)
+class Ray:
+    origin: np.ndarray
+    dir: np.ndarray
+
+    def __post_init__(self):
+        p = np.asarray(self.origin, dtype=np.float64)
+        r = np.asarray(self.dir, dtype=np.float64)
+        if p.shape != (3,) or r.shape != (3,):
+            raise InvalidRay("origin and dir must be 3-vectors")
+        if not (np.all(np.isfinite(p)) and np.all(np.isfinite(r))):
+            raise InvalidRay("non-finite ray")
+        if abs(np.linalg.norm(r) - 1.0) > 1e-9:
+            raise InvalidRay("direction must be a unit vector")
+        object.__setattr__(self, "origin", p)
+        object.__setattr__(self, "dir", r)
+
+
+@dataclass(frozen=True)
+class RayCastParams:
+    """rays.py:48-71."""
+
+    t_max: float = 10.0
+    sigma0: float | None = None
+    eta_plus: float = 1.5
+    eta_minus: float = 0.5
+    delta: float = 0.001
+    safety: float = 0.98
+
+    def __post_init__(self):
+        if self.t_max <= 0.0:
+            raise InvalidParameter("t_max must be positive")
+        if self.sigma0 is None:
+            object.__setattr__(self, "sigma0", self.t_max / 10.0)
+        if self.sigma0 <= 0.0:
+            raise InvalidParameter("sigma0 must be positive")
+        if self.eta_plus <= 1.0:
+            raise InvalidParameter("eta_plus must exceed 1")
+        if not 0.0 < self.eta_minus < 1.0:
+            raise InvalidParameter("eta_minus must lie in (0, 1)")
+        if self.delta <= 0.0:
+            raise InvalidParameter("delta must be positive")
+        if not 0.0 < self.safety <= 1.0:
+            raise InvalidParameter("safety must lie in (0, 1]")
+
+    def as_array(self):
+        return np.array([self.t_max, self.sigma0, self.eta_plus, self.eta_minus, self.delta, self.safety],
+                        dtype=np.float64)
+
+
+@dataclass(frozen=True)
+class HitResult:
+    hit: bool
+    t: float = float("inf")
+
+    @staticmethod
+    def hit_at(t: float) -> "HitResult":
+        return HitResult(True, t)
+
+    @staticmethod
+    def miss() -> "HitResult":
+        return HitResult(False)
+
+
+@dataclass
+class MarchStats:
+    rounds: int = 0
+    ray_steps: int = 0
+    certified_steps: int = 0
+    meta: dict = field(default_factory=dict)
+
+
+def march_arrays(net, origins, dirs, params: RayCastParams = RayCastParams(), policy=None,
+                 t_init=None, sigma_init=None, precision: str = "fp64", shared_origin: bool = False):
+    """Lock-step adaptive march of many rays (rays.py:88-138).
+
+    origins (n, 3) (or a single (3,) origin with shared_origin=True), dirs
+    (n, 3); NumPy arrays or CUDA tensors.  Returns (hit, t, steps, stats);
+    hit/t/steps come back as the same kind as `dirs`.
+    """
+    torch = dv._torch()
+    policy = AFFINE_FIXED if policy is None else policy
+    pcode, n_keep = policy_code(policy)
+    host = not dv.is_tensor(dirs)
+    dn = device_net(net, None if host else dirs.device.index)
+    dev = dn.device
+    d = dv.to_device(dirs, dev).reshape(-1, 3).contiguous()
+    n = d.shape[0]
+    o = dv.to_device(origins, dev).reshape(-1).contiguous() if shared_origin else \
+        dv.to_device(origins, dev).reshape(-1, 3).contiguous()
+    hit = torch.empty(n, dtype=torch.uint8, device=d.device)
+    t = torch.empty(n, dtype=torch.float64, device=d.device)
+    steps = torch.empty(n, dtype=torch.float64, device=d.device)
+    ti = dv.to_device(t_init, dev).contiguous() if t_init is not None else None
+    si = dv.to_device(sigma_init, dev).contiguous() if sigma_init is not None else None
+    p6 = params.as_array()
+    stats = np.zeros(3, np.int64)
+    if n:
+        _lib.call(
+            "spk_march", dn.ptr, pcode, n_keep, _precision_code(precision), n, o.data_ptr(),
+            0 if shared_origin else 3, d.data_ptr(), ti.data_ptr() if ti is not None else None,
+            si.data_ptr() if si is not None else None, p6.ctypes.data, hit.data_ptr(), t.data_ptr(),
+            steps.data_ptr(), stats.ctypes.data, dv.stream_ptr(dev),
+        )
+    st = MarchStats(int(stats[0]), int(stats[1]), int(stats[2]))
+    if host:
+        return hit.cpu().numpy().astype(bool), t.cpu().numpy(), steps.cpu().numpy(), st
+    return hit.bool(), t, steps, st
+
+
+def cast_rays(net, rays, params: RayCastParams = RayCastParams(), policy=None, threads: int = 1,
+              precision: str = "fp64") -> list:
+    """Cast many rays; elementwise identical to cast_ray on each (rays.py:151-184).
+    `threads` is accepted for API compatibility (the GPU march is batch-invariant)."""
+    rays = list(rays)
+    if not rays:
+        return []
+    origins = np.stack([r.origin for r in rays])
+    dirs = np.stack([r.dir for r in rays])
+    hit, t, _, _ = march_arrays(net, origins, dirs, params, policy, precision=precision)
+    return [HitResult(bool(h), float(tv)) for h, tv in zip(hit, t)]
+
+
+def cast_ray(net, ray: Ray, params: RayCastParams = RayCastParams(), policy=None,
+             precision: str = "fp64") -> HitResult:
+    return cast_rays(net, [ray], params, policy, precision=precision)[0]
+
+
+def cast_camera(net, camera: Camera, params: RayCastParams = RayCastParams(), policy=None,
+                precision: str = "fp64", device=None):
+    """March every pixel ray of a camera; directions are generated on the
+    device.  Returns (hit (H, W) bool, t (H, W), steps (H, W), stats) tensors."""
+    dirs = camera.pixel_dirs_device(device)
+    hit, t, steps, st = march_arrays(net, dv._torch().from_numpy(camera.position).to(dirs.device),
+                                     dirs.reshape(-1, 3), params, policy, precision=precision,
+                                     shared_origin=True)
+    h, w = camera.height, camera.width
+    return hit.reshape(h, w), t.reshape(h, w), steps.reshape(h, w), st
