@@ -76,6 +76,7 @@ enum { SPK_NEGATIVE = -1, SPK_UNKNOWN = 0, SPK_POSITIVE = 1 };
 
 typedef struct spk_net spk_net;
 typedef struct spk_tree spk_tree;
+typedef struct spk_mesh spk_mesh;
 
 const char* spk_last_error(void);
 int spk_version(void);
@@ -173,6 +174,24 @@ int spk_march(const spk_net* net, int policy, int n_keep, int precision, int64_t
  * forward, right, true_up (host), dirs (device) = height x width x 3. */
 int spk_camera_dirs(const double* frame9, double half_w, double half_h, int width, int height,
                     double* dirs, void* stream);
+
+/* K7: hierarchical marching cubes (extract_mesh, meshing.py:111-169) at
+ * resolution 2^m over the host box lo3..hi3; prune = 1 runs the index-range
+ * k-d prune over 3*(m - dense_levels) levels, prune = 0 extracts densely
+ * (extract_mesh_dense, meshing.py:100-108).  tri_table (256 x 15 int8, edge
+ * ids, 5 triangles max) and tri_count (256) are the reference's generated
+ * TRI_TABLE (mc_tables.py:95).  Vertices are deduplicated by global grid
+ * edge and numbered in first-visit order, like _MeshBuilder. */
+int spk_mesh_extract(const spk_net* net, int policy, int n_keep, int precision, const double* lo3,
+                     const double* hi3, int m, int dense_levels, int prune, const int8_t* tri_table,
+                     const uint8_t* tri_count, void* stream, spk_mesh** out);
+int spk_mesh_info(const spk_mesh* mesh, int64_t* n_vertices, int64_t* n_triangles, int64_t* n_blocks,
+                  int64_t* point_evals, int64_t* bound_evals);
+/* copy out (host or device pointers, any may be NULL): vertices n_v x 3,
+ * triangles n_t x 3 (vertex ids), vertex edge keys n_v
+ * ((i*(2^m+1) + j)*(2^m+1) + k) * 3 + axis of the edge's lower corner */
+int spk_mesh_copy(const spk_mesh* mesh, double* vertices, int64_t* triangles, uint64_t* vertex_keys);
+int spk_mesh_destroy(spk_mesh* mesh);
 
 #ifdef __cplusplus
 }

@@ -53,4 +53,6 @@ from .spatial import (
     iter_leaves,
 )
 
+from .meshing import extract_mesh, extract_mesh_arrays, extract_mesh_dense
+
 __version__ = "0.1.0"

@@ -1,0 +1,83 @@
+"""K7 hierarchical marching cubes on the GPU vs the reference's golden meshes.
+
+Connectivity: the triangle lists as edge-key triples must equal the
+reference's exactly (FP64 point evaluation; vertex ids are numbered in
+first-visit order like _MeshBuilder, so even the triangle arrays match).
+Vertex positions agree to 1e-12 (FP64 evaluation differs from the
+reference's einsum only in summation order).
+"""
+
+import numpy as np
+import pytest
+
+import paper_2202_02444_b200 as sp
+from oracle import spelunk_oracle as orc
+from paper_2202_02444_b200 import mc_tables, meshing
+from paper_2202_02444_b200.spatial import AABB
+
+pytestmark = pytest.mark.gpu
+BOUNDS = AABB(-np.ones(3), np.ones(3))
+MESHES = {
+    "offset_box_m5_fixed": ("offset_box", 5, "affine-fixed"),
+    "offset_box_m5_full": ("offset_box", 5, "affine-full"),
+    "relu_sdf_m5_fixed": ("relu_sdf", 5, "affine-fixed"),
+    "elu_sdf_m5_fixed": ("elu_sdf", 5, "affine-fixed"),
+}
+
+
+@pytest.mark.parametrize("tag", sorted(MESHES))
+def test_mesh_matches_reference(golden, net_paths, tag):
+    netname, m, pol = MESHES[tag]
+    net = sp.load_network(net_paths[netname])
+    res = meshing.extract_mesh_arrays(net, BOUNDS, m, 3, pol, precision="fp64")
+    wv, wt = golden[f"mesh/{tag}/vertices"], golden[f"mesh/{tag}/triangles"]
+    assert res.triangles.shape == wt.shape
+    np.testing.assert_array_equal(res.triangles, wt)          # first-visit numbering: identical arrays
+    assert np.max(np.abs(res.vertices - wv)) <= 1e-12
+    # oracle edge keys agree too
+    ov, ot, okeys = orc.mesh_extract(orc.as_oracle_net(net), -np.ones(3), np.ones(3), m, 3, pol)
+    np.testing.assert_array_equal(res.vertex_keys, okeys)
+
+
+def test_dense_matches_hierarchical(net_paths):
+    net = sp.load_network(net_paths["offset_box"])
+    h = meshing.extract_mesh_arrays(net, BOUNDS, 5, 3, "affine-fixed")
+    d = meshing.extract_mesh_arrays(net, BOUNDS, 5, 3, "affine-fixed", prune=False)
+    np.testing.assert_array_equal(meshing.triangle_key_set(h.triangles, h.vertex_keys),
+                                  meshing.triangle_key_set(d.triangles, d.vertex_keys))
+    assert h.point_evals < d.point_evals
+
+
+def test_mesh_fp32_connectivity(net_paths):
+    """FP32 evaluation: same triangles on every cell whose corner signs agree."""
+    net = sp.load_network(net_paths["relu_sdf"])
+    a = meshing.extract_mesh_arrays(net, BOUNDS, 6, 3, "affine-fixed", precision="fp64")
+    b = meshing.extract_mesh_arrays(net, BOUNDS, 6, 3, "affine-fixed", precision="fp32")
+    ka = {tuple(r) for r in meshing.triangle_key_set(a.triangles, a.vertex_keys)}
+    kb = {tuple(r) for r in meshing.triangle_key_set(b.triangles, b.vertex_keys)}
+    diff = len(ka ^ kb)
+    assert diff <= 0.001 * len(ka), diff
+    print(f"MESH fp32 vs fp64 differing triangles: {diff} of {len(ka)}")
+
+
+def test_mesh_edge_cases(net_paths):
+    const = sp.NetworkSpec(3, (sp.DenseLayer(np.zeros((1, 3)), np.array([1.0])),))
+    res = meshing.extract_mesh_arrays(const, BOUNDS, 4, 3, "affine-fixed")
+    assert len(res.vertices) == 0 and len(res.triangles) == 0
+    with pytest.raises(sp.errors.ResolutionTooSmall):
+        meshing.extract_mesh(const, BOUNDS, 3)
+
+
+def test_watertight_and_volume(net_paths):
+    from collections import Counter
+
+    net = sp.load_network(net_paths["offset_box"])
+    mesh = meshing.extract_mesh(net, BOUNDS, 5, policy="affine-fixed")
+    v, t = mesh.vertices, mesh.triangles
+    directed = Counter()
+    for a, b, c in t:
+        for e in ((a, b), (b, c), (c, a)):
+            directed[e] += 1
+    assert all(directed[(b, a)] == n for (a, b), n in directed.items())
+    v0, v1, v2 = v[t[:, 0]], v[t[:, 1]], v[t[:, 2]]
+    assert abs(np.einsum("ij,ij->", v0, np.cross(v1, v2)) / 6.0 - 1.0) <= 0.01

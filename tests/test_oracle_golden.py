@@ -125,3 +125,15 @@ def test_dense_mesh_matches_reference(golden, net_paths):
     v, t, _ = orc.mesh_extract_dense(orc.load_net(net_paths["relu_sdf"]), -np.ones(3), np.ones(3), 5)
     np.testing.assert_array_equal(v, golden["mesh/relu_sdf_m5_dense/vertices"])
     np.testing.assert_array_equal(t, golden["mesh/relu_sdf_m5_dense/triangles"])
+
+
+def test_package_mc_tables_match_reference(golden):
+    """The product's table generator (paper_2202_02444_b200/mc_tables.py)
+    reproduces the reference's generated TRI_TABLE / EDGE_TABLE."""
+    from paper_2202_02444_b200 import mc_tables
+
+    flat = [(c, *tri) for c in range(256) for tri in mc_tables.TRI_TABLE[c]]
+    np.testing.assert_array_equal(np.array(flat), golden["mc/tri_table"])
+    np.testing.assert_array_equal(np.array(mc_tables.EDGE_TABLE), golden["mc/edge_table"])
+    table, count = mc_tables.flat_tables()
+    assert table.shape == (256, 15) and int(count.sum()) == 820
