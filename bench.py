@@ -10,7 +10,8 @@ affine box bounds per second (tree nodes bounded / step time, whole job).
 At N > 1 the frontier below a redundant top cut is split across ranks (one
 process per GPU, no collective in the build): total work is fixed, so
 scaling is "strong".  `extra` carries the C5 throughput sweep point
-(16M on-device cubes, 8x256, one launch) and C1 (4x32, 64^3 grid).
+(16M on-device cubes, 8x256, one launch), C1 (4x32, 64^3 grid) and C3
+(SIREN 8x256 ray casting: rays/s, interval at 1024^2, truncate:16 at 256^2).
 
 Timing: W untimed warm-up steps, then K steps, each bracketed by a barrier
 and torch.cuda.synchronize(), timed with CUDA events on the launching
@@ -304,17 +305,9 @@ def run_ours(args, rank, world, local_rank):
             kernel_ms += arr.bound_ms
             kernel_boxes += arr.bound_evals
             units_local += useful_units(arr)
-    step_time = np.array(times)
-    if dist:
-        import torch.distributed as tdist
+    from paper_2202_02444_b200.shard import reduce_time_units
 
-        t = torch.tensor([step_time.sum(), float(units_local)], dtype=torch.float64, device=dev)
-        tmax = t.clone()
-        tdist.all_reduce(tmax[:1], op=tdist.ReduceOp.MAX)
-        tdist.all_reduce(t[1:], op=tdist.ReduceOp.SUM)
-        total_time, units = float(tmax[0]), float(t[1])
-    else:
-        total_time, units = float(step_time.sum()), float(units_local)
+    total_time, units = reduce_time_units(float(np.sum(times)), float(units_local), device=dev)
     value = units / total_time
 
     if rank != 0:
@@ -333,6 +326,9 @@ def run_ours(args, rank, world, local_rank):
     extra = {}
     extra["C5_8x256_16M"] = bench_c5(torch, sp, synth, "C5_256", 16 << 20, flush, peak_tf)
     extra["C1_4x32_64cubed"] = bench_c1(torch, sp, synth, flush, peak_tf)
+    if not args.no_rays:
+        extra["C3_siren_rays_interval_1024sq"] = bench_c3(torch, sp, synth, "interval", 1024)
+        extra["C3_siren_rays_truncate16_256sq"] = bench_c3(torch, sp, synth, "affine-truncate:16", 256)
 
     # ---- e2e through the public API (host arrays out)
     e2e = bench_e2e_tree(torch, sp, spatial, net, bounds, args)
@@ -407,6 +403,27 @@ def bench_c1(torch, sp, synth, flush, peak_tf):
             "frac_of_ffma_peak": n * flop / dt / 1e12 / peak_tf, "certified_fraction": cert}
 
 
+def bench_c3(torch, sp, synth, policy, res):
+    """C3: SIREN 3->8x256->1 (w0 = 30 folded, recentred), default camera
+    (reference bench.py:119-126), RayCastParams() defaults, FP32 kernels."""
+    from paper_2202_02444_b200.camera import default_camera
+
+    net = synth.config_net("C3")
+    cam = default_camera(res)
+    sp.cast_camera(net, default_camera(16), sp.RayCastParams(), policy, precision="fp32")  # warm
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    hit, t, steps, st = sp.cast_camera(net, cam, sp.RayCastParams(), policy, precision="fp32")
+    e1.record()
+    torch.cuda.synchronize()
+    dt = e0.elapsed_time(e1) / 1e3
+    n = res * res
+    return {"rays": n, "rays_per_s": n / dt, "ms": dt * 1e3, "ray_steps": st.ray_steps,
+            "steps_per_ray": st.ray_steps / n, "certified_steps": st.certified_steps,
+            "lockstep_rounds": st.rounds, "hit_fraction": float(hit.float().mean().item()), "policy": policy}
+
+
 def bench_e2e_tree(torch, sp, spatial, net, bounds, args):
     """Public API, host arrays out: build_spatial_tree_arrays(to_host=True)."""
     arr = spatial.build_spatial_tree_arrays(net, bounds, policy=sp.AFFINE_FIXED, max_depth=DEPTH, to_host=True)
@@ -451,6 +468,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-rays", action="store_true", help="skip the C3 ray-casting extra")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

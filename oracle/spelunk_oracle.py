@@ -437,7 +437,7 @@ def face_centres(los, his):
     return pts
 
 
-def tree_levels(net, lo, hi, policy="affine-fixed", delta=0.001, max_depth=None):
+def tree_levels(net, lo, hi, policy="affine-fixed", delta=0.001, max_depth=None, start_depth=0):
     """Breadth-first k-d tree (spatial.py:214-289) as flat per-level arrays.
 
     Level k+1 holds the low children of level k's split nodes (in order) then
@@ -447,16 +447,16 @@ def tree_levels(net, lo, hi, policy="affine-fixed", delta=0.001, max_depth=None)
     parent int64 (index into the previous level, -1 for the root).
     """
     net = as_oracle_net(net)
-    lo = np.asarray(lo, dtype=np.float64)
-    hi = np.asarray(hi, dtype=np.float64)
+    lo = np.atleast_2d(np.asarray(lo, dtype=np.float64))   # one root, or a frontier slice
+    hi = np.atleast_2d(np.asarray(hi, dtype=np.float64))
     if max_depth is not None and max_depth > 60:
         raise ValueError("DepthOverflow")
-    d = lo.shape[0]
+    d = lo.shape[1]
     stop = delta / np.sqrt(d)
-    los, his = lo[None, :].copy(), hi[None, :].copy()
-    parent = np.array([-1], dtype=np.int64)
+    los, his = lo.copy(), hi.copy()
+    parent = np.full(len(los), -1, dtype=np.int64)
     levels = []
-    depth = 0
+    depth = start_depth
     while True:
         blo, bhi = bound_aabbs(net, los, his, policy)
         label = sign_labels(blo, bhi)

@@ -302,20 +302,19 @@ def build_spatial_tree_sharded(net, bounds: AABB, max_depth: int, policy, rank: 
     the cut equals the unsharded tree (node AABBs are bit-identical because
     splits are exact FP64 midpoints).
     """
+    from .shard import first_cut, split_frontier
+
     _check_domain(net, bounds)
-    cut = 0
-    top = None
+    cut = first_cut(world, min_roots_per_rank, max_depth)
     while True:
         top = build_spatial_tree_arrays(net, bounds, 1.0, policy, cut, precision, to_host=True)
-        last = top.levels[-1]
-        n_open = int((_np(last.label) == 0).sum())
+        n_open = int((_np(top.levels[-1].label) == 0).sum())
         if cut >= max_depth or n_open >= min_roots_per_rank * world or n_open == 0:
             break
-        cut += max(1, int(np.ceil(np.log2(max(1, min_roots_per_rank * world) / max(1, n_open)))))
-        cut = min(cut, max_depth)
+        cut = min(max_depth, cut + 1)
     last = top.levels[-1]
     open_idx = np.flatnonzero(_np(last.label) == 0)
-    part = np.array_split(open_idx, world)[rank]
+    part = split_frontier(open_idx, rank, world)
     if cut >= max_depth or part.size == 0:
         top.meta.update(cut=cut, roots=int(part.size), top_nodes=top.n_nodes)
         return top
