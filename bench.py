@@ -288,7 +288,7 @@ def run_ours(args, rank, world, local_rank):
     def useful_units(arr):
         """Tree nodes this rank contributes, each node of the unsharded tree once."""
         if "top_levels" in arr.meta:  # sharded: own sub-tree below the cut (+ the top, on rank 0)
-            own = arr.n_nodes - len(arr.levels[0])
+            own = arr.n_nodes - arr.first_level_len
             return own + (arr.meta["top_nodes"] if rank == 0 else 0)
         return arr.n_nodes if rank == 0 else 0
 

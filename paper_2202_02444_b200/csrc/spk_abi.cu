@@ -227,6 +227,31 @@ int run_pass(const spk_net* cnet, int mode, int S, int precision, const BoxInput
   return SPK_OK;
 }
 
+static int check_policy(int policy, int n_keep, int* mode);
+
+// Internal entry points with an optional device-side count: n_cap sizes the
+// launch, *n_dev (when given) is the live count the kernels read.
+int bound_aabb_internal(const spk_net* net, int policy, int n_keep, int precision, long long n_cap,
+                        const long long* n_dev, const double* box_lo, const double* box_hi, double* lo, double* hi,
+                        int8_t* cls, cudaStream_t st) {
+  int mode;
+  if (int rc = check_policy(policy, n_keep, &mode)) return rc;
+  if (net->input_dim > 3) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "AABB path supports d <= 3");
+  if (n_cap <= 0) return n_cap < 0 ? fail(SPK_ERR_DIMENSION, "negative batch") : SPK_OK;
+  BoxInput in{IN_AABB, net->input_dim, box_lo, box_hi, 0, 0, 0.0, n_dev};
+  BoundOutput o{lo, hi, cls};
+  if (mode < 0) return launch_symbolic_in(net, -mode, n_keep, precision, in, o, n_cap, net->input_dim, st);
+  return run_pass(net, mode, net->input_dim, precision, in, o, n_cap, st);
+}
+
+int eval_internal(const spk_net* net, int precision, long long n_cap, const long long* n_dev, const double* xs,
+                  double* out, cudaStream_t st) {
+  if (n_cap <= 0) return n_cap < 0 ? fail(SPK_ERR_DIMENSION, "negative batch") : SPK_OK;
+  BoxInput in{IN_POINTS, 0, xs, nullptr, 0, 0, 0.0, n_dev};
+  BoundOutput o{out, nullptr, nullptr};
+  return run_pass(net, MODE_POINT, 0, precision, in, o, n_cap, st);
+}
+
 static int check_policy(int policy, int n_keep, int* mode) {
   switch (policy) {
     case SPK_POLICY_INTERVAL: *mode = MODE_INTERVAL; return SPK_OK;
@@ -338,7 +363,7 @@ int spk_bound_batch(const spk_net* net, int policy, int n_keep, int precision, i
   if (mode < 0) return launch_symbolic(net, -mode, n_keep, precision, n, s, centers, axes, lo, hi, cls,
                                        (cudaStream_t)stream);
   if (s > 3 && mode == MODE_AFFINE) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "more than 3 box axes");
-  BoxInput in{IN_BOXES, s, centers, axes, 0, 0, 0.0};
+  BoxInput in{IN_BOXES, s, centers, axes, 0, 0, 0.0, nullptr};
   BoundOutput o{lo, hi, cls};
   if (mode == MODE_INTERVAL) {
     // interval only needs the hull: pass all s axes through the radius sum
@@ -356,11 +381,8 @@ int spk_bound_aabb(const spk_net* net, int policy, int n_keep, int precision, in
   if (int rc = check_policy(policy, n_keep, &mode)) return rc;
   if (net->input_dim > 3) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "AABB path supports d <= 3");
   if (n <= 0) return n < 0 ? fail(SPK_ERR_DIMENSION, "negative batch") : SPK_OK;
-  if (mode < 0) return launch_symbolic_aabb(net, -mode, n_keep, precision, n, box_lo, box_hi, lo, hi, cls,
-                                            (cudaStream_t)stream);
-  BoxInput in{IN_AABB, net->input_dim, box_lo, box_hi, 0, 0, 0.0};
-  BoundOutput o{lo, hi, cls};
-  return run_pass(net, mode, net->input_dim, precision, in, o, n, (cudaStream_t)stream);
+  return bound_aabb_internal(net, policy, n_keep, precision, n, nullptr, box_lo, box_hi, lo, hi, cls,
+                             (cudaStream_t)stream);
 }
 
 int spk_bound_random_cubes(const spk_net* net, int policy, int n_keep, int precision, int64_t n,
@@ -373,7 +395,7 @@ int spk_bound_random_cubes(const spk_net* net, int policy, int n_keep, int preci
   if (net->input_dim > 3) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "random cubes support d <= 3");
   if (!(half >= 0.0)) return fail(SPK_ERR_INVALID_PARAMETER, "half-extent must be >= 0");
   if (n <= 0) return SPK_OK;
-  BoxInput in{IN_RANDOM, net->input_dim, nullptr, nullptr, (long long)first_index, seed, half};
+  BoxInput in{IN_RANDOM, net->input_dim, nullptr, nullptr, (long long)first_index, seed, half, nullptr};
   BoundOutput o{lo, hi, cls};
   return run_pass(net, mode, net->input_dim, precision, in, o, n, (cudaStream_t)stream);
 }
@@ -382,9 +404,7 @@ int spk_eval_batch(const spk_net* net, int precision, int64_t n, const double* x
                    void* stream) {
   if (!net) return fail(SPK_ERR_INVALID_PARAMETER, "null net");
   if (n <= 0) return n < 0 ? fail(SPK_ERR_DIMENSION, "negative batch") : SPK_OK;
-  BoxInput in{IN_POINTS, 0, xs, nullptr, 0, 0, 0.0};
-  BoundOutput o{out, nullptr, nullptr};
-  return run_pass(net, MODE_POINT, 0, precision, in, o, n, (cudaStream_t)stream);
+  return eval_internal(net, precision, n, nullptr, xs, out, (cudaStream_t)stream);
 }
 
 int spk_bound_batch_host(const spk_net* net, int policy, int n_keep, int precision, int64_t n, int s,

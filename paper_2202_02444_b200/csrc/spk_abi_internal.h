@@ -47,9 +47,13 @@ int run_pass(const struct ::spk_net* net, int mode, int S, int precision, const 
 int launch_symbolic(const struct ::spk_net* net, int policy, int n_keep, int precision, long long n, int s,
                     const double* centers, const double* axes, double* lo, double* hi, int8_t* cls,
                     cudaStream_t st);
-int launch_symbolic_aabb(const struct ::spk_net* net, int policy, int n_keep, int precision, long long n,
-                         const double* box_lo, const double* box_hi, double* lo, double* hi, int8_t* cls,
-                         cudaStream_t st);
+int launch_symbolic_in(const struct ::spk_net* net, int policy, int n_keep, int precision, const BoxInput& in,
+                       const BoundOutput& o, long long n_cap, int s, cudaStream_t st);
+int bound_aabb_internal(const struct ::spk_net* net, int policy, int n_keep, int precision, long long n_cap,
+                        const long long* n_dev, const double* box_lo, const double* box_hi, double* lo, double* hi,
+                        int8_t* cls, cudaStream_t st);
+int eval_internal(const struct ::spk_net* net, int precision, long long n_cap, const long long* n_dev,
+                  const double* xs, double* out, cudaStream_t st);
 
 // host-pointer pipeline, spk_host.cu
 int host_pipeline(const struct ::spk_net* net, int policy, int n_keep, int precision, long long n, int s,

@@ -39,6 +39,7 @@ template <> struct Num<float> {
   SPK_DEV static float fma_ru(float a, float b, float c) { return __fmaf_ru(a, b, c); }
   SPK_DEV static float mul_rn(float a, float b) { return __fmul_rn(a, b); }
   SPK_DEV static float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+  SPK_DEV static float div_fast(float a, float b) { return __fdividef(a, b); }
   SPK_DEV static float from_d_rn(double x) { return __double2float_rn(x); }
   SPK_DEV static float from_d_ru(double x) { return __double2float_ru(x); }
   SPK_DEV static float from_d_rd(double x) { return __double2float_rd(x); }
@@ -58,6 +59,7 @@ template <> struct Num<double> {
   SPK_DEV static double fma_ru(double a, double b, double c) { return __fma_ru(a, b, c); }
   SPK_DEV static double mul_rn(double a, double b) { return __dmul_rn(a, b); }
   SPK_DEV static double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+  SPK_DEV static double div_fast(double a, double b) { return __ddiv_rn(a, b); }
   SPK_DEV static double from_d_rn(double x) { return x; }
   SPK_DEV static double from_d_ru(double x) { return x; }
   SPK_DEV static double from_d_rd(double x) { return x; }

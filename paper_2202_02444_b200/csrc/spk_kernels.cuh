@@ -17,6 +17,7 @@ struct BoxInput {
   long long first;         // IN_RANDOM: stream offset
   unsigned long long seed; // IN_RANDOM
   double half;             // IN_RANDOM: cube half-extent
+  const long long* n_dev;  // optional device-side count (<= the launch's n): sync-free loops
 };
 
 struct BoundOutput {
@@ -107,20 +108,21 @@ SPK_DEV void emit_bounds(const BoundOutput& out, long long gb, const State<T, C,
 
 template <typename T, int C, int MMAX, int MODE>
 __global__ void __launch_bounds__(NT, 1)
-    bound_kernel(const NetDev<T> net, const BoxInput in, const BoundOutput out, const long long n) {
+    bound_kernel(const NetDev<T> net, const BoxInput in, const BoundOutput out, const long long n_cap) {
   using CF = Cfg<T, C, MMAX>;
+  const long long n = in.n_dev ? *in.n_dev : n_cap;
   constexpr int NB = CF::NB;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* X = reinterpret_cast<T*>(smem_raw);
   T* Wst = X + CF::XS;
-  T* NBUF = Wst + NSTAGE * CF::TILE;
+  T* NBUF = Wst + CF::NS * CF::TILE;
   uint64_t* full = reinterpret_cast<uint64_t*>(NBUF + CF::NBUF);
   const int tid = threadIdx.x;
 
   const long long nbt = (n + NB - 1) / NB;
   const long long mine = blockIdx.x < nbt ? (nbt - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   if (tid == 0) {
-    for (int s = 0; s < NSTAGE; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < CF::NS; ++s) mbar_init(&full[s], 1);
     mbar_fence_init();
   }
   __syncthreads();

@@ -29,7 +29,8 @@ constexpr int MAX_LAYERS = 24;
 constexpr int MAX_ACTS = 4;
 constexpr int NT = 256;         // threads per CTA
 constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reduction path
-constexpr int NSTAGE = 3;       // W tile ring depth
+constexpr int NSTAGE_MIN = 3;   // W tile ring depth floor (deeper when tiles are small)
+constexpr size_t SMEM_BUDGET = 210 * 1024;  // leaves room for the symbolic kernel's extras
 
 enum Mode : int { MODE_POINT = 0, MODE_INTERVAL = 1, MODE_AFFINE = 2 };
 
@@ -83,7 +84,12 @@ struct Cfg {
   // so a warp's vector loads of a W row are contiguous (bank-conflict free)
   static constexpr int G = TI < VEC ? TI : VEC;
   static constexpr int NBUF = NB * NARROW_MAX * CP;      // narrow-layer staging
-  static constexpr size_t SMEM = sizeof(T) * (size_t)(XS + NSTAGE * TILE + NBUF) + 64;
+  // W ring depth: as many KT x MMAX tiles as fit beside X (small nets keep
+  // every tile of the network resident and never re-stream W)
+  static constexpr long long NS_FIT =
+      ((long long)SMEM_BUDGET - (long long)sizeof(T) * (XS + NBUF) - 1024) / ((long long)sizeof(T) * TILE);
+  static constexpr int NS = NS_FIT < NSTAGE_MIN ? NSTAGE_MIN : (NS_FIT > 16 ? 16 : (int)NS_FIT);
+  static constexpr size_t SMEM = sizeof(T) * (size_t)(XS + NS * TILE + NBUF) + 16 * 8 + 64;
   static_assert(NG >= 1 && NG <= NT && NT % NG == 0, "tile shape");
   static_assert((TB * CP * sizeof(T)) % 16 == 0, "vector loads of X");
   static_assert(TI % G == 0, "W vector groups");
@@ -129,6 +135,8 @@ SPK_DEV void tma_bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t*
 
 // Ring of W tiles.  Tile g of the CTA's global sequence is tile
 // (g mod tiles_per_pass) of the network; all threads consume every tile.
+// When the whole network fits in the ring (tiles_per_pass <= NS) every tile
+// is loaded once and stays resident for the CTA's lifetime.
 template <typename T, int C, int MMAX>
 struct WRing {
   using CF = Cfg<T, C, MMAX>;
@@ -139,24 +147,31 @@ struct WRing {
   long long total;  // tiles this CTA will consume
   long long next;   // next tile to consume
 
+  SPK_DEV bool resident() const { return per_pass <= CF::NS; }
   SPK_DEV void issue(long long g) const {
-    const int st = (int)(g % NSTAGE);
+    const int st = resident() ? (int)(g % per_pass) : (int)(g % CF::NS);
     const T* s = src + (size_t)(g % per_pass) * CF::TILE;
     tma_bulk_load(stages + (size_t)st * CF::TILE, s, CF::TILE * sizeof(T), &full[st]);
   }
   SPK_DEV void prologue(int tid) const {
-    if (tid == 0) {
-      for (long long g = 0; g < NSTAGE && g < total; ++g) issue(g);
+    if (tid == 0 && total > 0) {
+      const long long n0 = resident() ? per_pass : (total < CF::NS ? total : CF::NS);
+      for (long long g = 0; g < n0; ++g) issue(g);
     }
   }
   SPK_DEV const T* acquire() const {
-    const int st = (int)(next % NSTAGE);
-    mbar_wait(&full[st], (uint32_t)((next / NSTAGE) & 1));
+    if (resident()) {
+      const int st = (int)(next % per_pass);
+      mbar_wait(&full[st], 0u);  // completes once, stays complete
+      return stages + (size_t)st * CF::TILE;
+    }
+    const int st = (int)(next % CF::NS);
+    mbar_wait(&full[st], (uint32_t)((next / CF::NS) & 1));
     return stages + (size_t)st * CF::TILE;
   }
   // every thread must be past its reads of the current stage (caller syncs)
   SPK_DEV void release(int tid) {
-    if (tid == 0 && next + NSTAGE < total) issue(next + NSTAGE);
+    if (!resident() && tid == 0 && next + CF::NS < total) issue(next + CF::NS);
     ++next;
   }
 };
@@ -331,16 +346,21 @@ SPK_DEV void dense_kloop(const LayerDev<T>& L, const T* __restrict__ X, WRing<T,
   for (int t = 0; t < L.ntiles; ++t) {
     const T* __restrict__ Ws = ring.acquire();
     const T* __restrict__ Xt = X + (size_t)(t * KT) * CF::RS + bg * TB * CP;
+    // rows past m_in are zero in X and W: stop at m_in (rounded to the
+    // double-buffer pair), e.g. 4 k-steps instead of KT for the 3-input layer
+    int k_end = L.m_in - t * KT;
+    k_end = k_end > KT ? KT : ((k_end + 1) & ~1);
 #pragma unroll 1
-    for (int k0 = 0; k0 < KT; k0 += SUBIN) {
+    for (int k0 = 0; k0 < k_end; k0 += SUBIN) {
+      const int k1 = k0 + SUBIN < k_end ? k0 + SUBIN : k_end;
       // register double buffering: fragments of step kk+1 load while step kk computes
       T w0[TI], x0[TB * CP], w1[TI], x1[TB * CP];
       load_frag(Ws, Xt, k0, w0, x0);
 #pragma unroll 2
-      for (int kk = k0; kk < k0 + SUBIN; kk += 2) {
+      for (int kk = k0; kk < k1; kk += 2) {
         load_frag(Ws, Xt, kk + 1, w1, x1);
         fma_step(w0, x0);
-        if (kk + 2 < k0 + SUBIN) load_frag(Ws, Xt, kk + 2, w0, x0);
+        if (kk + 2 < k1) load_frag(Ws, Xt, kk + 2, w0, x0);
         fma_step(w1, x1);
       }
       since += SUBIN;

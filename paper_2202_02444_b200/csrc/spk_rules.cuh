@@ -42,8 +42,10 @@ template <typename T>
 SPK_DEV int relu_affine(T lo, T hi, T& alpha, T& beta, T& gamma) {
   if (lo >= T(0)) { alpha = T(1); beta = T(0); gamma = T(0); return 0; }
   if (hi <= T(0)) { alpha = T(0); beta = T(0); gamma = T(0); return 1; }
-  T a = Num<T>::div_rn(hi, hi - lo);
-  a = a < T(0) ? T(0) : (a > T(1) ? T(1) : a);
+  // any slope in [0, 1] is sound (gamma is derived for the stored slope),
+  // so the FP32 path uses the fast reciprocal-multiply division
+  T a = Num<T>::div_fast(hi, hi - lo);
+  a = fmin(fmax(a, T(0)), T(1));  // NaN-safe clamp
   // g(x) = relu(x) - a x is >= 0 on [lo, hi] (g(0) = 0) with
   // max(g) = max(-a lo, hi - a hi).
   const T ru = fmax(Num<T>::mul_ru(-a, lo), Num<T>::fma_ru(-a, hi, hi));

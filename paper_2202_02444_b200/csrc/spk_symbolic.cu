@@ -72,17 +72,14 @@ int launch_symbolic(const spk_net* net, int policy, int n_keep, int precision, l
                     const double* centers, const double* axes, double* lo, double* hi, int8_t* cls,
                     cudaStream_t st) {
   if (s > 3) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "more than 3 box axes");
-  BoxInput in{IN_BOXES, s, centers, axes, 0, 0, 0.0};
+  BoxInput in{IN_BOXES, s, centers, axes, 0, 0, 0.0, nullptr};
   BoundOutput o{lo, hi, cls};
   return run_sym(net, policy, n_keep, precision, in, o, n, s, st);
 }
 
-int launch_symbolic_aabb(const spk_net* net, int policy, int n_keep, int precision, long long n,
-                         const double* box_lo, const double* box_hi, double* lo, double* hi, int8_t* cls,
-                         cudaStream_t st) {
-  BoxInput in{IN_AABB, net->input_dim, box_lo, box_hi, 0, 0, 0.0};
-  BoundOutput o{lo, hi, cls};
-  return run_sym(net, policy, n_keep, precision, in, o, n, net->input_dim, st);
+int launch_symbolic_in(const spk_net* net, int policy, int n_keep, int precision, const BoxInput& in,
+                       const BoundOutput& o, long long n_cap, int s, cudaStream_t st) {
+  return run_sym(net, policy, n_keep, precision, in, o, n_cap, s, st);
 }
 
 }  // namespace spk

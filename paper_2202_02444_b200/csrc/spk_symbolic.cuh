@@ -263,15 +263,16 @@ SPK_DEV void sym_layer(const LayerDev<T>& L, int& nsym, const SymParams& P, T* _
 
 template <typename T, int KC, int MMAX>
 __global__ void __launch_bounds__(NT, 1)
-    sym_bound_kernel(const NetDev<T> net, const BoxInput in, const BoundOutput out, const long long n,
+    sym_bound_kernel(const NetDev<T> net, const BoxInput in, const BoundOutput out, const long long n_cap,
                      const SymParams P) {
+  const long long n = in.n_dev ? *in.n_dev : n_cap;
   using SC = SymCfg<T, KC, MMAX>;
   using CF = typename SC::CF;
   constexpr int C = SC::C, NB = CF::NB;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* X = reinterpret_cast<T*>(smem_raw);
   T* Wst = X + CF::XS;
-  T* NBUF = Wst + NSTAGE * CF::TILE;
+  T* NBUF = Wst + CF::NS * CF::TILE;
   T* NEWG = NBUF + CF::NBUF;
   T* PART = NEWG + (size_t)NB * MMAX;
   int* KEPT = reinterpret_cast<int*>(PART + (size_t)NB * SC::NWB * KC);
@@ -283,7 +284,7 @@ __global__ void __launch_bounds__(NT, 1)
   const long long nbt = (n + NB - 1) / NB;
   const long long mine = blockIdx.x < nbt ? (nbt - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   if (tid == 0) {
-    for (int s = 0; s < NSTAGE; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < CF::NS; ++s) mbar_init(&full[s], 1);
     mbar_fence_init();
   }
   __syncthreads();

@@ -36,10 +36,11 @@ struct TreeLevel {
 };
 
 // per-node decision: flag 1 = split, 2 = tiny UNKNOWN leaf (convergence mode)
-__global__ void tree_mark_kernel(long long n, int d, const double* __restrict__ lo, const double* __restrict__ hi,
-                                 const int8_t* __restrict__ label, int depth, int max_depth, double stop_extent,
-                                 uint8_t* __restrict__ flag, int* __restrict__ block_split,
-                                 int* __restrict__ block_small) {
+__global__ void tree_mark_kernel(const long long* __restrict__ n_dev, int d, const double* __restrict__ lo,
+                                 const double* __restrict__ hi, const int8_t* __restrict__ label, int depth,
+                                 int max_depth, double stop_extent, uint8_t* __restrict__ flag,
+                                 int* __restrict__ block_split, int* __restrict__ block_small) {
+  const long long n = *n_dev;
   const long long i = (long long)blockIdx.x * TB_THREADS + threadIdx.x;
   uint8_t f = 0;
   if (i < n && label[i] == 0) {
@@ -100,11 +101,42 @@ __device__ int block_rank(bool pred, int* total) {
   return before + __popc(m & ((1u << lane) - 1u));
 }
 
-__global__ void tree_scatter_kernel(long long n, int d, const double* __restrict__ lo, const double* __restrict__ hi,
-                                    const uint8_t* __restrict__ flag, const int* __restrict__ block_split,
-                                    const int* __restrict__ block_small, long long n_split,
-                                    double* __restrict__ child_lo, double* __restrict__ child_hi,
-                                    long long* __restrict__ child_parent, long long* __restrict__ small_idx) {
+// totals of the block counts -> K (splits), M (tiny leaves), next level size 2K
+__global__ void tree_sum_kernel(int nblk, const int* __restrict__ block_split, const int* __restrict__ block_small,
+                                long long* __restrict__ k_out, long long* __restrict__ m_out,
+                                long long* __restrict__ next_n) {
+  long long a = 0, b = 0;
+  for (int q = threadIdx.x; q < nblk; q += TB_THREADS) {
+    a += block_split[q];
+    b += block_small[q];
+  }
+  __shared__ long long ra[TB_THREADS / 32], rb[TB_THREADS / 32];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, off);
+    b += __shfl_xor_sync(0xffffffffu, b, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    ra[threadIdx.x >> 5] = a;
+    rb[threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long ta = 0, tb = 0;
+    for (int w = 0; w < TB_THREADS / 32; ++w) { ta += ra[w]; tb += rb[w]; }
+    *k_out = ta;
+    *m_out = tb;
+    *next_n = 2 * ta;
+  }
+}
+
+__global__ void tree_scatter_kernel(const long long* __restrict__ n_dev, int d, const double* __restrict__ lo,
+                                    const double* __restrict__ hi, const uint8_t* __restrict__ flag,
+                                    const int* __restrict__ block_split, const int* __restrict__ block_small,
+                                    const long long* __restrict__ k_dev, double* __restrict__ child_lo,
+                                    double* __restrict__ child_hi, long long* __restrict__ child_parent,
+                                    long long* __restrict__ small_idx) {
+  const long long n = *n_dev, n_split = *k_dev;
   const long long i = (long long)blockIdx.x * TB_THREADS + threadIdx.x;
   const long long off_s = block_offset(block_split, blockIdx.x);
   const long long off_t = block_offset(block_small, blockIdx.x);
@@ -135,10 +167,12 @@ __global__ void tree_scatter_kernel(long long n, int d, const double* __restrict
 }
 
 // Face centres of tiny leaves: (m, 2d, d) points (spatial.py:202-211).
-__global__ void face_points_kernel(long long m, int d, const long long* __restrict__ idx,
+__global__ void face_points_kernel(const long long* __restrict__ m_dev, int d, const long long* __restrict__ idx,
                                    const double* __restrict__ lo, const double* __restrict__ hi,
-                                   double* __restrict__ pts) {
+                                   double* __restrict__ pts, long long* __restrict__ np_out) {
+  const long long m = *m_dev;
   const long long t = (long long)blockIdx.x * TB_THREADS + threadIdx.x;
+  if (t == 0) *np_out = m * 2 * d;
   if (t >= m * 2 * d) return;
   const long long node = idx[t / (2 * d)];
   const int face = (int)(t % (2 * d));
@@ -152,8 +186,9 @@ __global__ void face_points_kernel(long long m, int d, const long long* __restri
   }
 }
 
-__global__ void face_sign_kernel(long long m, int d, const long long* __restrict__ idx,
+__global__ void face_sign_kernel(const long long* __restrict__ m_dev, int d, const long long* __restrict__ idx,
                                  const double* __restrict__ vals, int8_t* __restrict__ face) {
+  const long long m = *m_dev;
   const long long t = (long long)blockIdx.x * TB_THREADS + threadIdx.x;
   if (t >= m) return;
   bool neg = false, pos = false;
@@ -263,36 +298,64 @@ int spk_tree_build(const spk_net* net, int policy, int n_keep, int precision, in
   tree->device = net->device;
   tree->start_depth = start_depth;
   const double stop = delta / std::sqrt((double)d);
+  const bool fixed = max_depth >= 0;
+  // Level sizes stay on the device: kernels read their live count from
+  // d_cnt[level] and are launched for a capacity bound (2x the previous
+  // level).  The host only synchronises in convergence mode (to detect the
+  // last level) or when a capacity bound would exceed kAsyncCap nodes.
+  constexpr long long kAsyncCap = 1ll << 24;
+  constexpr int kMaxLevels = 64;
   int rc = SPK_OK;
+  long long* d_cnt = nullptr;  // [level] live count; [kMaxLevels + level] K; [2*kMaxLevels + level] M
+  long long* d_np = nullptr;   // face-point count
+  if (cudaMallocAsync(&d_cnt, 3 * kMaxLevels * sizeof(long long), st) != cudaSuccess ||
+      cudaMallocAsync(&d_np, sizeof(long long), st) != cudaSuccess) {
+    delete tree;
+    return fail(SPK_ERR_OUT_OF_MEMORY, "tree counters");
+  }
+  cudaMemsetAsync(d_cnt, 0, 3 * kMaxLevels * sizeof(long long), st);
+  {
+    const long long r = n_roots;
+    cudaMemcpyAsync(d_cnt, &r, sizeof(long long), cudaMemcpyHostToDevice, st);
+  }
   TreeLevel cur;
   if ((rc = alloc_level(cur, n_roots, d, st)) != SPK_OK) { delete tree; return rc; }
   cudaMemcpyAsync(cur.lo, root_lo, n_roots * d * sizeof(double), cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(cur.hi, root_hi, n_roots * d * sizeof(double), cudaMemcpyHostToDevice, st);
   cudaMemsetAsync(cur.parent, 0xff, n_roots * sizeof(long long), st);  // -1
-  cudaMemsetAsync(cur.face, 0, n_roots, st);
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEventCreate(&ev0);
   cudaEventCreate(&ev1);
+  std::vector<cudaEvent_t> bound_ev;  // start/stop pairs, read once at the end
   int* counts = nullptr;
   uint8_t* flag = nullptr;
   long long* small_idx = nullptr;
   double* fpts = nullptr;
   double* fvals = nullptr;
   long long cap = 0, fcap = 0;
-  int* h_counts = nullptr;
-  for (int depth = start_depth; rc == SPK_OK; ++depth) {
-    const long long n = cur.n;
-    cudaEventRecord(ev0, st);
-    rc = spk_bound_aabb(net, policy, n_keep, precision, n, cur.lo, cur.hi, cur.blo, cur.bhi, cur.label, st);
-    cudaEventRecord(ev1, st);
+  std::vector<long long> caps;
+  long long cur_cap = n_roots;  // capacity bound of the current level
+  for (int depth = start_depth, lv = 0; rc == SPK_OK; ++depth, ++lv) {
+    if (lv >= kMaxLevels) { rc = fail(SPK_ERR_DEPTH_OVERFLOW, "more than 64 tree levels"); break; }
+    long long* n_dev = d_cnt + lv;
+    long long* k_dev = d_cnt + kMaxLevels + lv;
+    long long* m_dev = d_cnt + 2 * kMaxLevels + lv;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    bound_ev.push_back(e0);
+    bound_ev.push_back(e1);
+    cudaEventRecord(e0, st);
+    rc = bound_aabb_internal(net, policy, n_keep, precision, cur_cap, n_dev, cur.lo, cur.hi, cur.blo, cur.bhi,
+                             cur.label, st);
+    cudaEventRecord(e1, st);
     if (rc != SPK_OK) break;
-    tree->launches += 3;
-    tree->bound_evals += n;
-    cudaMemsetAsync(cur.face, 0, n, st);
-    const int nb = (int)((n + TB_THREADS - 1) / TB_THREADS);
-    if (n > cap) {
+    tree->launches += 4;
+    cudaMemsetAsync(cur.face, 0, cur_cap, st);
+    const int nb = (int)((cur_cap + TB_THREADS - 1) / TB_THREADS);
+    if (cur_cap > cap) {
       if (counts) { cudaFreeAsync(counts, st); cudaFreeAsync(flag, st); cudaFreeAsync(small_idx, st); }
-      cap = std::max<long long>(2 * n, 1024);
+      cap = std::max<long long>(2 * cur_cap, 1024);
       const long long nbc = (cap + TB_THREADS - 1) / TB_THREADS;
       if (cudaMallocAsync(&counts, 2 * nbc * sizeof(int), st) != cudaSuccess ||
           cudaMallocAsync(&flag, cap, st) != cudaSuccess ||
@@ -300,67 +363,87 @@ int spk_tree_build(const spk_net* net, int policy, int n_keep, int precision, in
         rc = fail(SPK_ERR_OUT_OF_MEMORY, "tree scratch");
         break;
       }
-      if (!pinned_scratch(2 * nbc * sizeof(int), (void**)&h_counts)) {
-        rc = fail(SPK_ERR_OUT_OF_MEMORY, "tree host scratch");
-        break;
-      }
     }
     int* bsplit = counts;
     int* bsmall = counts + nb;
-    tree_mark_kernel<<<nb, TB_THREADS, 0, st>>>(n, d, cur.lo, cur.hi, cur.label, depth, max_depth, stop, flag,
+    tree_mark_kernel<<<nb, TB_THREADS, 0, st>>>(n_dev, d, cur.lo, cur.hi, cur.label, depth, max_depth, stop, flag,
                                                 bsplit, bsmall);
-    // totals: block counts to pinned host memory, one sync per level
-    long long totals[2] = {0, 0};
-    {
-      const int* hc = h_counts;
-      cudaError_t e = cudaMemcpyAsync(h_counts, counts, 2 * nb * sizeof(int), cudaMemcpyDeviceToHost, st);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    tree_sum_kernel<<<1, TB_THREADS, 0, st>>>(nb, bsplit, bsmall, k_dev, m_dev, d_cnt + lv + 1);
+    // capacity of the next level
+    const bool last_fixed = fixed && depth >= max_depth;
+    long long next_cap = last_fixed ? 0 : 2 * cur_cap;
+    long long k_exact = -1;
+    if (!fixed || next_cap > kAsyncCap) {
+      long long km[2];
+      cudaMemcpyAsync(&km[0], k_dev, sizeof(long long), cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(&km[1], m_dev, sizeof(long long), cudaMemcpyDeviceToHost, st);
+      cudaError_t e = cudaStreamSynchronize(st);
       if (e != cudaSuccess) { rc = cuda_fail(e, "tree level"); break; }
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, ev0, ev1);
-      tree->bound_ms += ms;
-      for (int b = 0; b < nb; ++b) { totals[0] += hc[b]; totals[1] += hc[nb + b]; }
+      k_exact = km[0];
+      next_cap = 2 * km[0];
     }
-    const long long k = totals[0], m = totals[1];
     TreeLevel next;
-    if (k > 0 && (rc = alloc_level(next, 2 * k, d, st)) != SPK_OK) break;
-    tree_scatter_kernel<<<nb, TB_THREADS, 0, st>>>(n, d, cur.lo, cur.hi, flag, bsplit, bsmall, k, next.lo, next.hi,
-                                                   next.parent, small_idx);
-    if (m > 0) {
-      if (m * 2 * d > fcap) {
+    if (next_cap > 0 && (rc = alloc_level(next, next_cap, d, st)) != SPK_OK) break;
+    // always launched: it also lists the tiny leaves (children only when K > 0)
+    tree_scatter_kernel<<<nb, TB_THREADS, 0, st>>>(n_dev, d, cur.lo, cur.hi, flag, bsplit, bsmall, k_dev, next.lo,
+                                                   next.hi, next.parent, small_idx);
+    if (!fixed) {
+      // tiny UNKNOWN leaves: face-centre signs (capacity = this level's bound)
+      if (cur_cap * 2 * d > fcap) {
         if (fpts) { cudaFreeAsync(fpts, st); cudaFreeAsync(fvals, st); }
-        fcap = m * 2 * d;
+        fcap = cur_cap * 2 * d;
         if (cudaMallocAsync(&fpts, fcap * d * sizeof(double), st) != cudaSuccess ||
             cudaMallocAsync(&fvals, fcap * sizeof(double), st) != cudaSuccess) {
           rc = fail(SPK_ERR_OUT_OF_MEMORY, "face points");
           break;
         }
       }
-      const long long np = m * 2 * d;
-      face_points_kernel<<<(int)((np + TB_THREADS - 1) / TB_THREADS), TB_THREADS, 0, st>>>(m, d, small_idx, cur.lo,
-                                                                                             cur.hi, fpts);
-      rc = spk_eval_batch(net, precision, np, fpts, fvals, st);
+      const long long np_cap = cur_cap * 2 * d;
+      face_points_kernel<<<(int)((np_cap + TB_THREADS - 1) / TB_THREADS), TB_THREADS, 0, st>>>(
+          m_dev, d, small_idx, cur.lo, cur.hi, fpts, d_np);
+      rc = eval_internal(net, precision, np_cap, d_np, fpts, fvals, st);
       if (rc != SPK_OK) break;
+      face_sign_kernel<<<(int)((cur_cap + TB_THREADS - 1) / TB_THREADS), TB_THREADS, 0, st>>>(m_dev, d, small_idx,
+                                                                                               fvals, cur.face);
       tree->launches += 3;
-      face_sign_kernel<<<(int)((m + TB_THREADS - 1) / TB_THREADS), TB_THREADS, 0, st>>>(m, d, small_idx, fvals,
-                                                                                          cur.face);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { rc = cuda_fail(e, "tree kernels"); break; }
+    caps.push_back(cur_cap);
     tree->levels.push_back(cur);
     cur = TreeLevel();
-    if (k == 0) break;
+    if (next_cap == 0) break;  // no splits (exact) or last fixed depth
     cur = next;
+    cur_cap = next_cap;
+    (void)k_exact;
   }
+  // live sizes of every level, one copy
+  if (rc == SPK_OK) {
+    std::vector<long long> sizes(tree->levels.size());
+    cudaMemcpyAsync(sizes.data(), d_cnt, sizes.size() * sizeof(long long), cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "tree sizes");
+    for (size_t l = 0; rc == SPK_OK && l < sizes.size(); ++l) {
+      tree->levels[l].n = sizes[l];
+      tree->bound_evals += sizes[l];
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, bound_ev[2 * l], bound_ev[2 * l + 1]);
+      tree->bound_ms += ms;
+    }
+    // a fixed-depth build whose frontier emptied early ends at the last non-empty level
+    while (rc == SPK_OK && !tree->levels.empty() && tree->levels.back().n == 0) {
+      free_level(tree->levels.back(), st);
+      tree->levels.pop_back();
+    }
+  }
+  for (auto ev : bound_ev) cudaEventDestroy(ev);
+  cudaFreeAsync(d_cnt, st);
+  cudaFreeAsync(d_np, st);
   if (cur.lo) free_level(cur, st);
   if (counts) { cudaFreeAsync(counts, st); cudaFreeAsync(flag, st); cudaFreeAsync(small_idx, st); }
   if (fpts) { cudaFreeAsync(fpts, st); cudaFreeAsync(fvals, st); }
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
-  if (rc == SPK_OK) {
-    cudaError_t e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) rc = cuda_fail(e, "tree sync");
-  }
   if (rc != SPK_OK) {
     for (auto& L : tree->levels) free_level(L, st);
     delete tree;

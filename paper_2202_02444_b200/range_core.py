@@ -228,7 +228,7 @@ def _bound_device(net, centers, axes, pcode, n_keep, prec, return_class):
         a = torch.zeros((n, 0, d), dtype=torch.float64, device=c.device)
     if a.dim() != 3 or a.shape[0] != n or a.shape[2] != d:
         raise DimensionMismatch(f"axes must be (n, s, {d})")
-    a = _trim_axes(a).contiguous()
+    a = a.contiguous()  # no device-side trimming: zero axis rows are harmless and a trim would sync
     lo = torch.empty(n, dtype=torch.float64, device=c.device)
     hi = torch.empty(n, dtype=torch.float64, device=c.device)
     cls = torch.empty(n, dtype=torch.int8, device=c.device)

@@ -145,18 +145,42 @@ class TreeLevel:
         return int(self.label.shape[0])
 
 
-@dataclass
 class TreeArrays:
-    levels: list
-    start_depth: int = 0
-    bound_evals: int = 0
-    launches: int = 0
-    bound_ms: float = 0.0
-    meta: dict = field(default_factory=dict)
+    """Per-level arrays of a built tree.  Levels are materialised on first
+    access (zero-copy CUDA views or NumPy copies), so a caller that only
+    needs counts/statistics pays for no Python-side wrapping."""
+
+    def __init__(self, levels=None, start_depth=0, bound_evals=0, launches=0, bound_ms=0.0, meta=None,
+                 loader=None, n_levels=0, n_nodes=0, first_level_len=0):
+        self._levels = levels
+        self._loader = loader
+        self.start_depth = start_depth
+        self.bound_evals = bound_evals
+        self.launches = launches
+        self.bound_ms = bound_ms
+        self.meta = meta if meta is not None else {}
+        self._n_levels = n_levels if levels is None else len(levels)
+        self._n_nodes = n_nodes if levels is None else sum(len(l) for l in levels)
+        self._first = first_level_len if levels is None else (len(levels[0]) if levels else 0)
+
+    @property
+    def levels(self):
+        if self._levels is None:
+            self._levels = self._loader()
+            self._loader = None
+        return self._levels
+
+    @property
+    def n_levels(self) -> int:
+        return self._n_levels
 
     @property
     def n_nodes(self) -> int:
-        return sum(len(l) for l in self.levels)
+        return self._n_nodes
+
+    @property
+    def first_level_len(self) -> int:
+        return self._first
 
     def keys(self):
         """Path keys per level (root 1, low child 2k, high child 2k+1)."""
@@ -220,10 +244,18 @@ def _build(net, roots_lo, roots_hi, start_depth, delta, policy, max_depth, preci
     la, ms = C.c_int64(), C.c_double()
     _lib.check(lib.spk_tree_stats(handle, C.byref(la), C.byref(ms)))
     d = net.input_dim
-    levels = []
-    for i in range(nl.value):
-        levels.append(_level(owner, i, d, dn.device, to_host))
-    return TreeArrays(levels, int(start_depth), be.value, la.value, ms.value)
+    n0 = C.c_int64()
+    if nl.value:
+        _lib.check(lib.spk_tree_level(handle, 0, C.byref(n0), None, None, None, None, None, None, None))
+
+    def loader():
+        return [_level(owner, i, d, dn.device, to_host) for i in range(nl.value)]
+
+    arr = TreeArrays(None, int(start_depth), be.value, la.value, ms.value, loader=loader, n_levels=nl.value,
+                     n_nodes=nn.value, first_level_len=n0.value)
+    if to_host:
+        arr.levels  # copy out now; the library tree is released with `owner`
+    return arr
 
 
 _LEVEL_SPECS = (("lo", "<f8", 2), ("hi", "<f8", 2), ("bound_lo", "<f8", 1), ("bound_hi", "<f8", 1),

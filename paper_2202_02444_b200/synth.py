@@ -8,8 +8,11 @@ bit-identical weights).  Recipes, all seeded with np.random.default_rng:
   torch-uniform  W, b ~ U(+-1/sqrt(fan_in)) (nn.Linear default), final bias
                  shifted by the median of f over 20,000 U(-1,1)^3 samples so
                  the zero level set crosses the domain
-  siren          Sitzmann et al. init with w0 = 30 folded into W and b of every
-                 sin layer, recentred like torch-uniform
+  siren          Sitzmann et al. init (first layer U(+-1/fan_in), later layers
+                 U(+-sqrt(6/fan_in)/w0), biases U(+-1/sqrt(fan_in))) with
+                 w0 = 30 folded into the FIRST layer's W and b only -- the
+                 reference has no w0 parameter -- recentred
+                 like torch-uniform
 
 The recentring forward pass below is plain NumPy: it only constructs the
 synthetic net (it is not an evaluation path of this package).
@@ -68,10 +71,6 @@ def random_mlp(width: int, depth: int, activation="relu", recipe="torch-uniform"
             kb = 1.0 / np.sqrt(fan_in)
             if i == 0:
                 w = rng.uniform(-1.0 / fan_in, 1.0 / fan_in, (fan_out, fan_in)) * w0
-                b = rng.uniform(-kb, kb, fan_out) * w0
-            elif i < len(dims) - 2:
-                lim = np.sqrt(6.0 / fan_in) / w0
-                w = rng.uniform(-lim, lim, (fan_out, fan_in)) * w0
                 b = rng.uniform(-kb, kb, fan_out) * w0
             else:
                 lim = np.sqrt(6.0 / fan_in) / w0
