@@ -13,7 +13,10 @@ from pathlib import Path
 
 from . import errors as E
 
-LIB_PATH = Path(__file__).resolve().parent / "_spk.so"
+import os
+
+# SPK_LIB_PATH overrides the in-tree library (used to A/B kernel variants)
+LIB_PATH = Path(os.environ.get("SPK_LIB_PATH") or Path(__file__).resolve().parent / "_spk.so")
 
 # status codes (spelunk_b200.h)
 OK, ERR_DIM, ERR_ACT, ERR_PARAM, ERR_DEPTH, ERR_CUDA, ERR_SHAPE, ERR_OOM = range(8)

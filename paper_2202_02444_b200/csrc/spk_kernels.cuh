@@ -45,7 +45,10 @@ SPK_DEV void prep_inputs(const NetDev<T>& net, const BoxInput& in, long long n, 
   using CF = Cfg<T, C, MMAX>;
   constexpr int NB = CF::NB, CP = CF::CP;
   const int d = net.d;
-  for (int q = tid; q < MMAX * NB; q += NT) {
+  // the first layer reads rows [0, d) plus the zero pad row of its
+  // double-buffered k-pair; every other row is rewritten by its epilogue
+  const int rows = ((d + 1) & ~1) < MMAX ? ((d + 1) & ~1) : MMAX;
+  for (int q = tid; q < rows * NB; q += NT) {
     const int k = q / NB, b = q % NB;
     const long long gb = g0 + b;
     T packed[CP];

@@ -29,6 +29,9 @@ constexpr int MAX_LAYERS = 24;
 constexpr int MAX_ACTS = 4;
 constexpr int NT = 256;         // threads per CTA
 constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reduction path
+#ifndef SPK_PACKED_F32
+#define SPK_PACKED_F32 1  // FP32 K loop on FFMA2 (sm_100a packed f32x2)
+#endif
 constexpr int NSTAGE_MIN = 3;   // W tile ring depth floor (deeper when tiles are small)
 constexpr size_t SMEM_BUDGET = 210 * 1024;  // leaves room for the symbolic kernel's extras
 
@@ -208,6 +211,27 @@ SPK_DEV void apply_act(State<T, C, MODE>& st, int act) {
     const T c = Num<T>::fma_rn(L, T(0.5), Num<T>::mul_rn(H, T(0.5)));
     st.base = c;
     st.e = fmax(Num<T>::sub_ru(H, c), Num<T>::sub_ru(c, L));
+  } else if (act == ACT_RELU) {
+    // Branch-free ReLU (no divergence between active / inactive / straddling
+    // lanes): slope a = 1 (lo >= 0), 0 (hi <= 0), else hi/(hi-lo) clamped;
+    // the remainder bound below is exact-zero for a = 0 or 1, and the
+    // rounding terms are only charged where a rounding can occur (straddle).
+    const T rA = sum_abs_A(st);
+    const T r = Num<T>::add_ru(rA, st.e);
+    const T lo = Num<T>::sub_rd(st.base, r), hi = Num<T>::add_ru(st.base, r);
+    const bool on = lo >= T(0), off = hi <= T(0), mix = !(on || off);
+    T a = fmin(fmax(Num<T>::div_fast(hi, hi - lo), T(0)), T(1));
+    a = on ? T(1) : (off ? T(0) : a);
+    const T ru = mix ? fmax(Num<T>::mul_ru(-a, lo), Num<T>::fma_ru(-a, hi, hi)) : T(0);
+    const T b = Num<T>::mul_rn(ru, T(0.5));
+    const T g = fmax(b, Num<T>::sub_ru(ru, b));
+    const T nb = Num<T>::fma_rn(a, st.base, b);
+#pragma unroll
+    for (int j = 0; j < State<T, C, MODE>::S; ++j) st.A[j] = Num<T>::mul_rn(a, st.A[j]);
+    T e = Num<T>::fma_ru(a, st.e, g);
+    const T rnd = Num<T>::fma_ru(Num<T>::RHO, Num<T>::add_ru(fabs(nb), Num<T>::mul_ru(a, rA)), Num<T>::TINY);
+    st.e = mix ? Num<T>::add_ru(e, rnd) : e;
+    st.base = nb;
   } else {
     const T rA = sum_abs_A(st);
     const T r = Num<T>::add_ru(rA, st.e);
@@ -271,8 +295,8 @@ SPK_DEV void final_bounds(const State<T, C, MODE>& st, double& lo, double& hi) {
 // partials added to the running sums), so the rounding budget is
 // gamma_{SUB + ceil(m_in/SUB) + 1} instead of gamma_{m_in + 1}.
 template <typename T, int C, int MMAX>
-SPK_DEV void dense_kloop(const LayerDev<T>& L, const T* __restrict__ X, WRing<T, C, MMAX>& ring, int tid,
-                         T (&acc)[Cfg<T, C, MMAX>::TI][Cfg<T, C, MMAX>::TB][C]) {
+SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, WRing<T, C, MMAX>& ring, int tid,
+                                T (&acc)[Cfg<T, C, MMAX>::TI][Cfg<T, C, MMAX>::TB][C]) {
   using CF = Cfg<T, C, MMAX>;
   constexpr int TI = CF::TI, TB = CF::TB, CP = CF::CP, KT = CF::KT;
   const int ng = tid % CF::NG, bg = tid / CF::NG;
@@ -373,6 +397,187 @@ SPK_DEV void dense_kloop(const LayerDev<T>& L, const T* __restrict__ X, WRing<T,
     ring.release(tid);
   }
   if (since > 0) flush();
+}
+
+
+// ------------------------------------------------------------ packed FP32
+// sm_100a FFMA2 / FADD2 (fma.rn.f32x2 / add.rn.f32x2): two FP32 lanes per
+// instruction; the scalar weight is broadcast by ptxas's `.F32` operand form
+// (no duplicate move), so acc(c, c+1) += w * x(c, c+1) is one issue slot.
+typedef unsigned long long f32x2;
+SPK_DEV f32x2 f2_fma(float w, f32x2 x, f32x2 acc) {
+  asm("{.reg .b64 wd;\n mov.b64 wd, {%1, %1};\n fma.rn.f32x2 %0, wd, %2, %0;}" : "+l"(acc) : "f"(w), "l"(x));
+  return acc;
+}
+SPK_DEV f32x2 f2_fma2(f32x2 w, f32x2 x, f32x2 acc) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(w), "l"(x));
+  return acc;
+}
+SPK_DEV f32x2 f2_add(f32x2 a, f32x2 b) {
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(a) : "l"(b));
+  return a;
+}
+SPK_DEV void f2_split(f32x2 v, float& lo, float& hi) { asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v)); }
+SPK_DEV f32x2 f2_pack(float lo, float hi) {
+  f32x2 v;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "f"(lo), "f"(hi));
+  return v;
+}
+
+// FP32 K loop with packed FMAs.  Columns of one box: NP round-to-nearest
+// pairs, an optional odd RN column, and the round-up error column (scalar
+// FFMA.RP with the |W| operand modifier).  Point evaluation (C == 1) pairs
+// adjacent boxes instead.  Same blocked-summation budget as the scalar loop.
+template <int C, int MMAX>
+SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__ X, WRing<float, C, MMAX>& ring,
+                             int tid, float (&acc)[Cfg<float, C, MMAX>::TI][Cfg<float, C, MMAX>::TB][C]) {
+  using CF = Cfg<float, C, MMAX>;
+  constexpr int TI = CF::TI, TB = CF::TB, CP = CF::CP, KT = CF::KT;
+  constexpr bool POINT = C == 1;
+  constexpr int NRN = POINT ? 1 : C - 1;           // round-to-nearest columns per box
+  constexpr int NP = POINT ? TB / 2 : NRN / 2;     // packed pairs (per box; boxes for POINT)
+  constexpr int NBOX = POINT ? 1 : TB;             // pair groups
+  constexpr bool ODD = !POINT && (NRN % 2 == 1);
+  constexpr int XQ = TB * CP / 2;                  // x fragment as f32x2 words
+  static_assert(POINT ? (TB % 2 == 0) : (CP % 2 == 0), "pair alignment");
+  const int ng = tid % CF::NG, bg = tid / CF::NG;
+
+  constexpr int NPA = NP > 0 ? NP : 1;
+  f32x2 accp[TI][NBOX][NPA], partp[TI][NBOX][NPA];
+  float acco[TI][TB], parto[TI][TB], acce[TI][TB];
+#pragma unroll
+  for (int ti = 0; ti < TI; ++ti) {
+    const int i = CF::neuron(ng, ti);
+    const float b0 = (i < L.m_out) ? L.bias[i] : 0.f;
+#pragma unroll
+    for (int g = 0; g < NBOX; ++g)
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        // the bias enters the base column (column 0, or every box for POINT)
+        accp[ti][g][p] = POINT ? f2_pack(b0, b0) : (p == 0 ? f2_pack(b0, 0.f) : f2_pack(0.f, 0.f));
+        partp[ti][g][p] = 0ull;
+      }
+#pragma unroll
+    for (int tb = 0; tb < TB; ++tb) {
+      acco[ti][tb] = (ODD && NP == 0) ? b0 : 0.f;  // C == 2: the odd column is the base
+      parto[ti][tb] = 0.f;
+      acce[ti][tb] = 0.f;
+    }
+  }
+  constexpr int SUBIN = KT < CF::SUB ? KT : CF::SUB;
+  int since = 0;
+  auto flush = [&]() {
+#pragma unroll
+    for (int ti = 0; ti < TI; ++ti) {
+#pragma unroll
+      for (int g = 0; g < NBOX; ++g)
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          accp[ti][g][p] = f2_add(accp[ti][g][p], partp[ti][g][p]);
+          partp[ti][g][p] = 0ull;
+        }
+      if (ODD) {
+#pragma unroll
+        for (int tb = 0; tb < TB; ++tb) {
+          acco[ti][tb] += parto[ti][tb];
+          parto[ti][tb] = 0.f;
+        }
+      }
+    }
+  };
+  auto load_frag = [&](const float* __restrict__ Ws, const float* __restrict__ Xt, int kk, float* w, f32x2* xq) {
+    using WV = typename VecOf<CF::G * 4>::type;
+    WV* wd = reinterpret_cast<WV*>(w);
+#pragma unroll
+    for (int q = 0; q < TI / CF::G; ++q)
+      wd[q] = *reinterpret_cast<const WV*>(Ws + kk * MMAX + q * (CF::NG * CF::G) + ng * CF::G);
+    const ulonglong2* xp = reinterpret_cast<const ulonglong2*>(Xt + (size_t)kk * CF::RS);
+#pragma unroll
+    for (int q = 0; q < XQ / 2; ++q) {
+      const ulonglong2 v = xp[q];
+      xq[2 * q] = v.x;
+      xq[2 * q + 1] = v.y;
+    }
+  };
+  auto fma_step = [&](const float* w, const f32x2* xq) {
+#pragma unroll
+    for (int ti = 0; ti < TI; ++ti) {
+#pragma unroll
+      for (int g = 0; g < NBOX; ++g)
+#pragma unroll
+        for (int p = 0; p < NP; ++p)
+          partp[ti][g][p] = f2_fma(w[ti], xq[POINT ? p : (g * CP) / 2 + p], partp[ti][g][p]);
+      if (!POINT) {
+#pragma unroll
+        for (int tb = 0; tb < TB; ++tb) {
+          float lo, hi;
+          f2_split(xq[(tb * CP + C - 1) / 2], lo, hi);
+          const float xe = ((C - 1) % 2 == 0) ? lo : hi;
+          acce[ti][tb] = __fmaf_ru(fabsf(w[ti]), xe, acce[ti][tb]);
+          if (ODD) {
+            float ol, oh;
+            f2_split(xq[(tb * CP + 2 * NP) / 2], ol, oh);
+            parto[ti][tb] = __fmaf_rn(w[ti], ol, parto[ti][tb]);
+          }
+        }
+      }
+    }
+  };
+
+  for (int t = 0; t < L.ntiles; ++t) {
+    const float* __restrict__ Ws = ring.acquire();
+    const float* __restrict__ Xt = X + (size_t)(t * KT) * CF::RS + bg * TB * CP;
+    int k_end = L.m_in - t * KT;
+    k_end = k_end > KT ? KT : ((k_end + 1) & ~1);
+#pragma unroll 1
+    for (int k0 = 0; k0 < k_end; k0 += SUBIN) {
+      const int k1 = k0 + SUBIN < k_end ? k0 + SUBIN : k_end;
+      float w0[TI], w1[TI];
+      f32x2 x0[XQ], x1[XQ];
+      load_frag(Ws, Xt, k0, w0, x0);
+#pragma unroll 1
+      for (int kk = k0; kk < k1; kk += 2) {
+        load_frag(Ws, Xt, kk + 1, w1, x1);
+        fma_step(w0, x0);
+        if (kk + 2 < k1) load_frag(Ws, Xt, kk + 2, w0, x0);
+        fma_step(w1, x1);
+      }
+      since += SUBIN;
+      if (since >= CF::SUB) {
+        flush();
+        since = 0;
+      }
+    }
+    __syncthreads();
+    ring.release(tid);
+  }
+  if (since > 0) flush();
+  // unpack into the scalar accumulator layout of the epilogue
+#pragma unroll
+  for (int ti = 0; ti < TI; ++ti) {
+    if (POINT) {
+#pragma unroll
+      for (int p = 0; p < NP; ++p) f2_split(accp[ti][0][p], acc[ti][2 * p][0], acc[ti][2 * p + 1][0]);
+    } else {
+#pragma unroll
+      for (int tb = 0; tb < TB; ++tb) {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) f2_split(accp[ti][tb][p], acc[ti][tb][2 * p], acc[ti][tb][2 * p + 1]);
+        if (ODD) acc[ti][tb][2 * NP] = acco[ti][tb];
+        acc[ti][tb][C - 1] = acce[ti][tb];
+      }
+    }
+  }
+}
+
+template <typename T, int C, int MMAX>
+SPK_DEV void dense_kloop(const LayerDev<T>& L, const T* __restrict__ X, WRing<T, C, MMAX>& ring, int tid,
+                         T (&acc)[Cfg<T, C, MMAX>::TI][Cfg<T, C, MMAX>::TB][C]) {
+  if constexpr (sizeof(T) == 4 && SPK_PACKED_F32) {
+    dense_kloop_f32<C, MMAX>(L, X, ring, tid, acc);
+  } else {
+    dense_kloop_scalar<T, C, MMAX>(L, X, ring, tid, acc);
+  }
 }
 
 template <typename T, int C, int MMAX, int MODE>
