@@ -124,18 +124,22 @@ __global__ void __launch_bounds__(NT, 1)
 
   const long long nbt = (n + NB - 1) / NB;
   const long long mine = blockIdx.x < nbt ? (nbt - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  unsigned* released = reinterpret_cast<unsigned*>(full + 16);
   if (tid == 0) {
-    for (int s = 0; s < CF::NS; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < CF::NS; ++s) {
+      mbar_init(&full[s], 1);
+      released[s] = 0u;
+    }
     mbar_fence_init();
   }
   __syncthreads();
-  WRing<T, C, MMAX> ring{Wst, full, net.wtiles, net.tiles_per_pass, mine * net.tiles_per_pass, 0};
-  if (net.tiles_per_pass > 0) ring.prologue(tid);
+  WRing<T, C, MMAX> ring{Wst, full, released, net.wtiles, net.tiles_per_pass, mine * net.tiles_per_pass, 0};
+  ring.prologue(tid);
 
   for (long long tile = blockIdx.x; tile < nbt; tile += gridDim.x) {
     const long long g0 = tile * NB;
     prep_inputs<T, C, MMAX, MODE>(net, in, n, g0, X, tid, true);
-    __syncthreads();
+    csync();
     auto emit = [&](int b, const State<T, C, MODE>& st) {
       if (g0 + b < n) emit_bounds<T, C, MODE>(out, g0 + b, st);
     };

@@ -27,7 +27,7 @@ namespace spk {
 
 constexpr int MAX_LAYERS = 24;
 constexpr int MAX_ACTS = 4;
-constexpr int NT = 256;         // threads per CTA
+constexpr int NT = 256;         // threads per CTA (8 warps)
 constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reduction path
 #ifndef SPK_PACKED_F32
 #define SPK_PACKED_F32 1  // FP32 K loop on FFMA2 (sm_100a packed f32x2)
@@ -92,7 +92,7 @@ struct Cfg {
   static constexpr long long NS_FIT =
       ((long long)SMEM_BUDGET - (long long)sizeof(T) * (XS + NBUF) - 1024) / ((long long)sizeof(T) * TILE);
   static constexpr int NS = NS_FIT < NSTAGE_MIN ? NSTAGE_MIN : (NS_FIT > 16 ? 16 : (int)NS_FIT);
-  static constexpr size_t SMEM = sizeof(T) * (size_t)(XS + NS * TILE + NBUF) + 16 * 8 + 64;
+  static constexpr size_t SMEM = sizeof(T) * (size_t)(XS + NS * TILE + NBUF) + 2 * 16 * 8 + 64;
   static_assert(NG >= 1 && NG <= NT && NT % NG == 0, "tile shape");
   static_assert((TB * CP * sizeof(T)) % 16 == 0, "vector loads of X");
   static_assert(TI % G == 0, "W vector groups");
@@ -126,6 +126,12 @@ SPK_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+SPK_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// barrier among the NT compute threads only (the producer warp never joins)
+SPK_DEV void csync() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
+
 SPK_DEV void tma_bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
@@ -137,14 +143,19 @@ SPK_DEV void tma_bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t*
 }
 
 // Ring of W tiles.  Tile g of the CTA's global sequence is tile
-// (g mod tiles_per_pass) of the network; all threads consume every tile.
-// When the whole network fits in the ring (tiles_per_pass <= NS) every tile
-// is loaded once and stays resident for the CTA's lifetime.
+// (g mod tiles_per_pass) of the network; all warps consume every tile in
+// order.  Each warp releases a stage with one shared-memory atomic; the last
+// of the 8 warps to release it issues the refill (cp.async.bulk into the same
+// stage), so warps never synchronise with each other per tile and no extra
+// producer warp (which would cost ~25% of the register file) is needed.  When
+// the whole network fits in the ring (tiles_per_pass <= NS) every tile is
+// loaded once and stays resident for the CTA's lifetime.
 template <typename T, int C, int MMAX>
 struct WRing {
   using CF = Cfg<T, C, MMAX>;
   T* stages;
   uint64_t* full;
+  unsigned* released;  // per-stage count of warps done with the current round
   const T* src;
   int per_pass;
   long long total;  // tiles this CTA will consume
@@ -172,9 +183,21 @@ struct WRing {
     mbar_wait(&full[st], (uint32_t)((next / CF::NS) & 1));
     return stages + (size_t)st * CF::TILE;
   }
-  // every thread must be past its reads of the current stage (caller syncs)
+  // the calling warp is done reading the current stage
   SPK_DEV void release(int tid) {
-    if (!resident() && tid == 0 && next + CF::NS < total) issue(next + CF::NS);
+    if (!resident()) {
+      __syncwarp();
+      if ((tid & 31) == 0) {
+        const int st = (int)(next % CF::NS);
+        if (atomicAdd(&released[st], 1u) == NT / 32 - 1) {
+          released[st] = 0u;
+          if (next + CF::NS < total) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(next + CF::NS);
+          }
+        }
+      }
+    }
     ++next;
   }
 };
@@ -393,10 +416,10 @@ SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, W
         since = 0;
       }
     }
-    __syncthreads();  // all reads of this W stage (and, on the last tile, of X) are done
-    ring.release(tid);
+    ring.release(tid);  // this warp is done with the stage
   }
   if (since > 0) flush();
+  csync();  // every warp finished reading X before any epilogue rewrites it
 }
 
 
@@ -548,10 +571,10 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
         since = 0;
       }
     }
-    __syncthreads();
     ring.release(tid);
   }
   if (since > 0) flush();
+  csync();
   // unpack into the scalar accumulator layout of the epilogue
 #pragma unroll
   for (int ti = 0; ti < TI; ++ti) {
@@ -618,7 +641,7 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
 #pragma unroll
     for (int q = 0; q < (int)(TB * CP * sizeof(T) / 16); ++q) dst[q] = srcv[q];
   }
-  __syncthreads();
+  csync();
   (void)last;
 }
 
@@ -663,7 +686,7 @@ SPK_DEV void narrow_layer(const LayerDev<T>& L, T* __restrict__ X, T* __restrict
       for (int c = 0; c < C; ++c) dst[c] = p[c];
     }
   }
-  __syncthreads();
+  csync();
   // epilogue
   for (int it = tid; it < items; it += NT) {
     const int b = it / L.m_out, i = it % L.m_out;
@@ -695,7 +718,7 @@ SPK_DEV void narrow_layer(const LayerDev<T>& L, T* __restrict__ X, T* __restrict
     T* base = X + (size_t)L.m_out * CF::RS;
     for (int q = tid; q < n; q += NT) base[q] = T(0);
   }
-  __syncthreads();
+  csync();
 }
 
 // ---------------------------------------------------------------- the pass

@@ -114,7 +114,7 @@ SPK_DEV void sym_activation(int act, int m_out, int& nsym, const SymParams& P, T
 #pragma unroll
     for (int j = 0; j < KC; ++j) PART[(bg * SC::NWB + ng / 32) * KC + j] = pn[j];
   }
-  __syncthreads();
+  csync();
 
   // ---- C: selection, one warp per box
   const int total = n_old + m_out;
@@ -185,7 +185,7 @@ SPK_DEV void sym_activation(int act, int m_out, int& nsym, const SymParams& P, T
       kept[lane] = -1;
     }
   }
-  __syncthreads();
+  csync();
 
   // ---- D: rebuild rows in kept order, fold dropped columns into e
 #pragma unroll
@@ -216,7 +216,7 @@ SPK_DEV void sym_activation(int act, int m_out, int& nsym, const SymParams& P, T
     row[C - 1] = e;
   }
   nsym = n_new;
-  __syncthreads();
+  csync();
 }
 
 // Hidden dense layer + its activations + packing for the next layer.
@@ -243,7 +243,7 @@ SPK_DEV void sym_layer(const LayerDev<T>& L, int& nsym, const SymParams& P, T* _
       row[c] = v;
     }
   }
-  __syncthreads();
+  csync();
   for (int a = 0; a < L.n_act; ++a)
     sym_activation<T, KC, MMAX>(L.act[a], L.m_out, nsym, P, X, NEWG, PART, KEPT, SLOTOLD, tid);
   // pack: v = e + gamma' (|base| + sum|A| + e) for the next dense layer
@@ -258,7 +258,7 @@ SPK_DEV void sym_layer(const LayerDev<T>& L, int& nsym, const SymParams& P, T* _
     const T e = row[C - 1];
     row[C - 1] = Num<T>::fma_ru(L.gamma_next, Num<T>::add_ru(Num<T>::add_ru(fabs(row[0]), rA), e), e);
   }
-  __syncthreads();
+  csync();
 }
 
 template <typename T, int KC, int MMAX>
@@ -278,23 +278,27 @@ __global__ void __launch_bounds__(NT, 1)
   int* KEPT = reinterpret_cast<int*>(PART + (size_t)NB * SC::NWB * KC);
   int* SLOTOLD = KEPT + NB * KC;
   uint64_t* full = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(SLOTOLD + NB * KC) + 15) & ~(uintptr_t)15);
+      (reinterpret_cast<uintptr_t>(SLOTOLD + NB * KC) + 15) & ~(uintptr_t)15);  // full[16], empty[16]
   const int tid = threadIdx.x;
 
   const long long nbt = (n + NB - 1) / NB;
   const long long mine = blockIdx.x < nbt ? (nbt - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  unsigned* released = reinterpret_cast<unsigned*>(full + 16);
   if (tid == 0) {
-    for (int s = 0; s < CF::NS; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < CF::NS; ++s) {
+      mbar_init(&full[s], 1);
+      released[s] = 0u;
+    }
     mbar_fence_init();
   }
   __syncthreads();
-  WRing<T, C, MMAX> ring{Wst, full, net.wtiles, net.tiles_per_pass, mine * net.tiles_per_pass, 0};
-  if (net.tiles_per_pass > 0) ring.prologue(tid);
+  WRing<T, C, MMAX> ring{Wst, full, released, net.wtiles, net.tiles_per_pass, mine * net.tiles_per_pass, 0};
+  ring.prologue(tid);
 
   for (long long tile = blockIdx.x; tile < nbt; tile += gridDim.x) {
     const long long g0 = tile * NB;
     prep_inputs<T, C, MMAX, MODE_AFFINE>(net, in, n, g0, X, tid, true);
-    __syncthreads();
+    csync();
     int nsym = P.s0;
     for (int l = 0; l < net.n_layers; ++l) {
       const LayerDev<T>& L = net.L[l];
