@@ -256,7 +256,7 @@ def run_ours(args, rank, world, local_rank):
     import paper_2202_02444_b200 as sp
     from paper_2202_02444_b200 import _lib, spatial, synth
 
-    torch.cuda.set_device(local_rank)
+    torch.cuda.set_device(local_rank % max(1, torch.cuda.device_count()))
     dev = torch.cuda.current_device()
     dist = world > 1
     if dist:
@@ -307,7 +307,8 @@ def run_ours(args, rank, world, local_rank):
             units_local += useful_units(arr)
     from paper_2202_02444_b200.shard import reduce_time_units
 
-    total_time, units = reduce_time_units(float(np.sum(times)), float(units_local), device=dev)
+    total_time, units = reduce_time_units(float(np.sum(times)), float(units_local),
+                                          device=dev if args.dist_backend == "nccl" else "cpu")
     value = units / total_time
 
     if rank != 0:
@@ -469,6 +470,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rays", action="store_true", help="skip the C3 ray-casting extra")
+    ap.add_argument("--dist-backend", default="nccl", help="nccl (default) or gloo (functional checks of the "
+                    "sharded path with several ranks on one GPU)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -482,8 +485,12 @@ def main():
         import torch
         import torch.distributed as tdist
 
-        torch.cuda.set_device(local_rank)
-        tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        dev = local_rank % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(dev)
+        if args.dist_backend == "nccl":
+            tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+        else:
+            tdist.init_process_group(args.dist_backend)
     line = run_ours(args, rank, world, local_rank)
     if line is not None:
         print(json.dumps(line), flush=True)
