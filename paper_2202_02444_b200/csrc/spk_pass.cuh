@@ -220,6 +220,35 @@ SPK_DEV T sum_abs_A(const State<T, C, MODE>& st) {
   return r;
 }
 
+// Non-ReLU affine activations (ELU / sin / tanh).  Inline (a by-reference
+// call would force the state into local memory on every path); the rule
+// itself -- the FP64 transcendental part -- is out of line (spk_rules.cuh).
+template <typename T, int C, int MODE>
+SPK_DEV void apply_affine_general(State<T, C, MODE>& st, int act) {
+  const T rA = sum_abs_A(st);
+  const T r = Num<T>::add_ru(rA, st.e);
+  const T lo = Num<T>::sub_rd(st.base, r), hi = Num<T>::add_ru(st.base, r);
+  T a, b, g;
+  const int kind = affine_rule<T>(act, lo, hi, a, b, g);
+  if (kind == 0) return;
+  if (kind == 1) {
+    st.base = T(0);
+#pragma unroll
+    for (int j = 0; j < State<T, C, MODE>::S; ++j) st.A[j] = T(0);
+    st.e = T(0);
+    return;
+  }
+  const T nb = Num<T>::fma_rn(a, st.base, b);
+#pragma unroll
+  for (int j = 0; j < State<T, C, MODE>::S; ++j) st.A[j] = Num<T>::mul_rn(a, st.A[j]);
+  const T aa = fabs(a);
+  T e = Num<T>::fma_ru(aa, st.e, g);
+  // rounding of a*base+b and of the a*A_j products
+  e = Num<T>::fma_ru(Num<T>::RHO, Num<T>::add_ru(fabs(nb), Num<T>::mul_ru(aa, rA)), e);
+  st.e = Num<T>::add_ru(e, Num<T>::TINY);
+  st.base = nb;
+}
+
 // Apply one activation to the state (sound rules; range_core.py:583-603 for
 // affine-fixed, :639-641 for interval, network.py:149-160 for points).
 template <typename T, int C, int MODE>
@@ -256,31 +285,9 @@ SPK_DEV void apply_act(State<T, C, MODE>& st, int act) {
     st.e = mix ? Num<T>::add_ru(e, rnd) : e;
     st.base = nb;
   } else {
-    const T rA = sum_abs_A(st);
-    const T r = Num<T>::add_ru(rA, st.e);
-    const T lo = Num<T>::sub_rd(st.base, r), hi = Num<T>::add_ru(st.base, r);
-    T a, b, g;
-    const int kind = affine_rule<T>(act, lo, hi, a, b, g);
-    if (kind == 0) return;
-    if (kind == 1) {
-      st.base = T(0);
-#pragma unroll
-      for (int j = 0; j < State<T, C, MODE>::S; ++j) st.A[j] = T(0);
-      st.e = T(0);
-      return;
-    }
-    const T nb = Num<T>::fma_rn(a, st.base, b);
-#pragma unroll
-    for (int j = 0; j < State<T, C, MODE>::S; ++j) st.A[j] = Num<T>::mul_rn(a, st.A[j]);
-    const T aa = fabs(a);
-    T e = Num<T>::fma_ru(aa, st.e, g);
-    // rounding of a*base+b and of the a*A_j products
-    e = Num<T>::fma_ru(Num<T>::RHO, Num<T>::add_ru(fabs(nb), Num<T>::mul_ru(aa, rA)), e);
-    st.e = Num<T>::add_ru(e, Num<T>::TINY);
-    st.base = nb;
+    apply_affine_general<T, C, MODE>(st, act);
   }
 }
-
 // Column values handed to the next dense layer.
 template <typename T, int C, int MODE>
 SPK_DEV void pack_next(const State<T, C, MODE>& st, T gamma_next, T* out) {
@@ -614,6 +621,37 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
 
   // epilogue: activation rules, write next X in place (one contiguous
   // TB*CP vector per neuron: the thread's boxes are adjacent in the row)
+  if (MODE == MODE_POINT) {
+    // point values: ReLU unrolled; any other activation through ONE rolled
+    // loop per neuron so its (large) code exists once (instruction cache)
+#pragma unroll
+    for (int ti = 0; ti < TI; ++ti) {
+      const int i = CF::neuron(ng, ti);
+      T out[TB * CP];
+#pragma unroll
+      for (int tb = 0; tb < TB; ++tb) out[tb * CP] = i < L.m_out ? acc[ti][tb][0] : T(0);
+      for (int a = 0; a < L.n_act; ++a) {
+        const int act = L.act[a];
+        if (act == ACT_RELU) {
+#pragma unroll
+          for (int tb = 0; tb < TB; ++tb) out[tb * CP] = fmax(out[tb * CP], T(0));
+        } else if (act != ACT_IDENTITY) {
+#pragma unroll 1
+          for (int tb = 0; tb < TB; ++tb) out[tb * CP] = act_value_slow<T>(act, out[tb * CP]);
+        }
+      }
+      if (i >= L.m_out) {
+#pragma unroll
+        for (int tb = 0; tb < TB; ++tb) out[tb * CP] = T(0);
+      }
+      float4* dst = reinterpret_cast<float4*>(X + (size_t)i * CF::RS + bg * TB * CP);
+      const float4* srcv = reinterpret_cast<const float4*>(out);
+#pragma unroll
+      for (int q = 0; q < (int)(TB * CP * sizeof(T) / 16); ++q) dst[q] = srcv[q];
+    }
+    csync();
+    return;
+  }
 #pragma unroll
   for (int ti = 0; ti < TI; ++ti) {
     const int i = CF::neuron(ng, ti);

@@ -218,25 +218,22 @@ SPK_RULE void interval_image_slow(int act, T lo, T hi, T& out_lo, T& out_hi) {
   }
 }
 
-// Pointwise value (network.py:149-160), used by point evaluation.
-template <typename T> SPK_DEV T act_value(int act, T x);
-template <> SPK_DEV float act_value<float>(int act, float x) {
-  if (act == ACT_RELU) return fmaxf(x, 0.f);
+// Pointwise value (network.py:149-160), used by point evaluation.  ReLU is
+// inline; the other activations live out of line so the unrolled epilogue
+// stays small (instruction-cache pressure).
+template <typename T>
+SPK_RULE T act_value_slow(int act, T x) {  // float / double overloads of the CUDA math library
   switch (act) {
-    case ACT_ELU: return x >= 0.f ? x : expm1f(x);
-    case ACT_SIN: return sinf(x);
-    case ACT_TANH: return tanhf(x);
-    default: return x;
-  }
-}
-template <> SPK_DEV double act_value<double>(int act, double x) {
-  if (act == ACT_RELU) return fmax(x, 0.0);
-  switch (act) {
-    case ACT_ELU: return x >= 0.0 ? x : expm1(x);
+    case ACT_ELU: return x >= T(0) ? x : expm1(x);
     case ACT_SIN: return sin(x);
     case ACT_TANH: return tanh(x);
     default: return x;
   }
+}
+template <typename T>
+SPK_DEV T act_value(int act, T x) {
+  if (act == ACT_RELU) return fmax(x, T(0));
+  return act_value_slow<T>(act, x);
 }
 
 }  // namespace spk

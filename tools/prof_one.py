@@ -27,6 +27,22 @@ def main():
         n = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 20
         net = synth.config_net("C5_256")
         run = lambda: sp.bound_random_cubes(net, n, seed=1, half=1 / 64)
+    elif which in ("eval256", "eval512"):
+        net = synth.config_net("C2" if which == "eval256" else "C4")
+        n = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 22
+        x = torch.rand((n, 3), dtype=torch.float64, device="cuda") * 2 - 1
+        run = lambda: sp.eval_batch(net, x, precision="fp32")
+    elif which == "c5interval":
+        n = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 22
+        net = synth.config_net("C5_256")
+        run = lambda: sp.bound_random_cubes(net, n, seed=1, half=1 / 64, policy=sp.INTERVAL_ONLY)
+    elif which == "c5trunc":
+        n = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 18
+        net = synth.config_net("C5_256")
+        c = torch.rand((n, 3), dtype=torch.float64, device="cuda") * 2 - 1
+        a = torch.zeros((n, 1, 3), dtype=torch.float64, device="cuda")
+        a[:, 0, 0] = 1 / 64
+        run = lambda: sp.range_bound_batch(net, c, a, sp.affine_truncate(16))
     else:
         net = synth.config_net("C1")
         c, a = synth.grid_cubes(64)
@@ -40,7 +56,8 @@ def main():
     run()
     e1.record()
     torch.cuda.synchronize()
-    print(f"{which}: {e0.elapsed_time(e1):.3f} ms")
+    ms = e0.elapsed_time(e1)
+    print(f"{which}: {ms:.3f} ms")
 
 
 if __name__ == "__main__":
