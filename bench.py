@@ -327,6 +327,8 @@ def run_ours(args, rank, world, local_rank):
     extra = {}
     extra["C5_8x256_16M"] = bench_c5(torch, sp, synth, "C5_256", 16 << 20, flush, peak_tf)
     extra["C1_4x32_64cubed"] = bench_c1(torch, sp, synth, flush, peak_tf)
+    if not args.no_mesh:
+        extra["C4_elu8x512_mesh_256cubed"] = bench_c4(torch, sp, synth, 8)
     if not args.no_rays:
         extra["C3_siren_rays_interval_1024sq"] = bench_c3(torch, sp, synth, "interval", 1024)
         extra["C3_siren_rays_truncate16_256sq"] = bench_c3(torch, sp, synth, "affine-truncate:16", 256)
@@ -425,6 +427,28 @@ def bench_c3(torch, sp, synth, policy, res):
             "lockstep_rounds": st.rounds, "hit_fraction": float(hit.float().mean().item()), "policy": policy}
 
 
+def bench_c4(torch, sp, synth, m):
+    """C4 (reduced resolution): hierarchical marching cubes of the ELU
+    3->8x512->1 net (torch-uniform, recentred) at 2^m cells per axis,
+    affine-fixed prune, FP32 corner evaluation.  (1024^3 = m 10 is the
+    config; it is 64x the corner evaluations of m = 8.)"""
+    from paper_2202_02444_b200 import meshing
+    from paper_2202_02444_b200.spatial import AABB
+
+    net = synth.config_net("C4")
+    bounds = AABB(-np.ones(3), np.ones(3))
+    meshing.extract_mesh_arrays(net, bounds, 5, 3, sp.AFFINE_FIXED, precision="fp32")  # warm
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = meshing.extract_mesh_arrays(net, bounds, m, 3, sp.AFFINE_FIXED, precision="fp32")
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    return {"m": m, "seconds": dt, "triangles": int(len(res.triangles)), "vertices": int(len(res.vertices)),
+            "surviving_blocks": res.n_blocks, "point_evals": res.point_evals, "bound_evals": res.bound_evals,
+            "point_evals_per_s": res.point_evals / dt,
+            "note": "wall clock through the public API incl. mesh copy to host"}
+
+
 def bench_e2e_tree(torch, sp, spatial, net, bounds, args):
     """Public API, host arrays out: build_spatial_tree_arrays(to_host=True)."""
     arr = spatial.build_spatial_tree_arrays(net, bounds, policy=sp.AFFINE_FIXED, max_depth=DEPTH, to_host=True)
@@ -470,6 +494,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rays", action="store_true", help="skip the C3 ray-casting extra")
+    ap.add_argument("--no-mesh", action="store_true", help="skip the C4 mesh extra")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (default) or gloo (functional checks of the "
                     "sharded path with several ranks on one GPU)")
     args = ap.parse_args()
