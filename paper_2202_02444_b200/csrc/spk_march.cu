@@ -13,7 +13,10 @@
 //      with t < t_max are re-compacted (warp ballot + block prefix) for the
 //      next round.
 // With the certification decisions equal, t is bit-identical to the
-// reference's (same FP64 operations in the same order).
+// reference's (same FP64 operations in the same order).  For interval and
+// affine-fixed the probe evaluation and the segment bound run as ONE fused
+// network pass per round (spk_march_pass.cuh); truncate / full use the
+// point kernel + symbolic bound kernel.
 // Camera rays (Camera.pixel_dirs, camera.py:74-92) are generated on the
 // device with round-to-nearest FP64 ops in numpy's evaluation order, so they
 // match the reference bit for bit.
@@ -21,16 +24,12 @@
 #include <cmath>
 #include <vector>
 
-#include "spk_kernels.cuh"
+#include "spk_march_pass.cuh"
 #include "spk_abi_internal.h"
 
 namespace spk {
 
 constexpr int MT = 256;
-
-struct MarchParamsDev {
-  double t_max, sigma0, eta_plus, eta_minus, delta, safety;
-};
 
 __global__ void camera_dirs_kernel(int W, int H, double fx, double fy, double fz, double rx, double ry, double rz,
                                    double ux, double uy, double uz, double half_w, double half_h,
@@ -238,14 +237,31 @@ int spk_march(const spk_net* net, int policy, int n_keep, int precision, int64_t
     for (int b = 0; b < nblk; ++b) na += hcnt[b];
     if (rc == SPK_OK) compact_kernel<<<nblk, MT, 0, st>>>(n, live, nullptr, bcnt, cur);
   }
+  const bool fused = policy == SPK_POLICY_INTERVAL || policy == SPK_POLICY_AFFINE_FIXED;
+  const int sm = sm_count_for(net->device);
   while (rc == SPK_OK && na > 0) {
     const int ab = (int)((na + MT - 1) / MT);
-    march_gen_kernel<<<ab, MT, 0, st>>>(na, cur, origins, origin_stride, dirs, t, sig, P, probe, cen, ax);
-    rc = spk_eval_batch(net, precision, na, probe, fp, st);
-    if (rc != SPK_OK) break;
-    rc = spk_bound_batch(net, policy, n_keep, precision, na, 1, cen, ax, blo, bhi, nullptr, st);
-    if (rc != SPK_OK) break;
-    march_update_kernel<<<ab, MT, 0, st>>>(na, cur, fp, blo, bhi, P, t, sig, steps, hit, t_out, neg0, live, cert);
+    if (fused) {
+      MarchState M{cur, origins, origin_stride, dirs, t, sig, steps, hit, t_out, neg0, live, cert};
+      cudaError_t ke;
+      if (precision == SPK_FP64) {
+        const NetDev<double>* nd;
+        if ((rc = get_dev<double>(const_cast<spk_net*>(net), &nd)) != SPK_OK) break;
+        ke = dispatch_march_round<double>(net->mmax, policy == SPK_POLICY_AFFINE_FIXED, *nd, M, P, na, sm, st);
+      } else {
+        const NetDev<float>* nd;
+        if ((rc = get_dev<float>(const_cast<spk_net*>(net), &nd)) != SPK_OK) break;
+        ke = dispatch_march_round<float>(net->mmax, policy == SPK_POLICY_AFFINE_FIXED, *nd, M, P, na, sm, st);
+      }
+      if (ke != cudaSuccess) { rc = cuda_fail(ke, "march round"); break; }
+    } else {
+      march_gen_kernel<<<ab, MT, 0, st>>>(na, cur, origins, origin_stride, dirs, t, sig, P, probe, cen, ax);
+      rc = spk_eval_batch(net, precision, na, probe, fp, st);
+      if (rc != SPK_OK) break;
+      rc = spk_bound_batch(net, policy, n_keep, precision, na, 1, cen, ax, blo, bhi, nullptr, st);
+      if (rc != SPK_OK) break;
+      march_update_kernel<<<ab, MT, 0, st>>>(na, cur, fp, blo, bhi, P, t, sig, steps, hit, t_out, neg0, live, cert);
+    }
     evals += na;
     ++rounds;
     count_kernel<<<ab, MT, 0, st>>>(na, live, cur, bcnt);

@@ -35,7 +35,16 @@ constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reducti
 constexpr int NSTAGE_MIN = 3;   // W tile ring depth floor (deeper when tiles are small)
 constexpr size_t SMEM_BUDGET = 210 * 1024;  // leaves room for the symbolic kernel's extras
 
-enum Mode : int { MODE_POINT = 0, MODE_INTERVAL = 1, MODE_AFFINE = 2 };
+enum Mode : int {
+  MODE_POINT = 0,
+  MODE_INTERVAL = 1,
+  MODE_AFFINE = 2,
+  MODE_MI = 3,  // ray march round: point value + interval bound   (columns: x, c, v)
+  MODE_MA = 4   // ray march round: point value + affine-fixed S=1 (columns: x, base, A, v)
+};
+// bound part of a mode, and the column offset of the bound state
+constexpr int bound_mode(int m) { return m == MODE_MI ? MODE_INTERVAL : (m == MODE_MA ? MODE_AFFINE : m); }
+constexpr int pv_off(int m) { return m >= MODE_MI ? 1 : 0; }
 
 template <typename T>
 struct LayerDev {
@@ -206,10 +215,13 @@ struct WRing {
 // Per-(neuron, box) state between layers.
 template <typename T, int C, int MODE>
 struct State {
-  static constexpr int S = MODE == MODE_AFFINE ? C - 2 : 0;
+  static constexpr int BM = bound_mode(MODE);
+  static constexpr int OFF = pv_off(MODE);
+  static constexpr int S = BM == MODE_AFFINE ? C - 2 - OFF : 0;
   T base;       // value / centre / affine base
   T A[S > 0 ? S : 1];
   T e;          // interval radius / affine error (not yet pre-inflated)
+  T pv;         // march modes: point value at the probe
 };
 
 template <typename T, int C, int MODE>
@@ -254,9 +266,11 @@ SPK_DEV void apply_affine_general(State<T, C, MODE>& st, int act) {
 template <typename T, int C, int MODE>
 SPK_DEV void apply_act(State<T, C, MODE>& st, int act) {
   if (act == ACT_IDENTITY) return;  // skipped, range_core.py:586-587
-  if (MODE == MODE_POINT) {
+  constexpr int BM = bound_mode(MODE);
+  if (MODE >= MODE_MI) st.pv = act_value<T>(act, st.pv);
+  if (BM == MODE_POINT) {
     st.base = act_value<T>(act, st.base);
-  } else if (MODE == MODE_INTERVAL) {
+  } else if (BM == MODE_INTERVAL) {
     const T lo = Num<T>::sub_rd(st.base, st.e), hi = Num<T>::add_ru(st.base, st.e);
     T L, H;
     interval_image<T>(act, lo, hi, L, H);
@@ -291,15 +305,17 @@ SPK_DEV void apply_act(State<T, C, MODE>& st, int act) {
 // Column values handed to the next dense layer.
 template <typename T, int C, int MODE>
 SPK_DEV void pack_next(const State<T, C, MODE>& st, T gamma_next, T* out) {
-  out[0] = st.base;
+  constexpr int BM = bound_mode(MODE), OFF = pv_off(MODE);
+  if (MODE >= MODE_MI) out[0] = st.pv;
+  out[OFF] = st.base;
   // v = e + gamma' (|base| + sum|A| + e): gamma' covers the next layer's
   // FMA rounding and (FP32) the rounding of the FP64 weights to T.
-  if (MODE == MODE_INTERVAL) {
-    out[1] = Num<T>::fma_ru(gamma_next, Num<T>::add_ru(fabs(st.base), st.e), st.e);
-  } else if (MODE == MODE_AFFINE) {
+  if (BM == MODE_INTERVAL) {
+    out[OFF + 1] = Num<T>::fma_ru(gamma_next, Num<T>::add_ru(fabs(st.base), st.e), st.e);
+  } else if (BM == MODE_AFFINE) {
     const T rA = sum_abs_A(st);
 #pragma unroll
-    for (int j = 0; j < State<T, C, MODE>::S; ++j) out[1 + j] = st.A[j];
+    for (int j = 0; j < State<T, C, MODE>::S; ++j) out[OFF + 1 + j] = st.A[j];
     out[C - 1] = Num<T>::fma_ru(gamma_next, Num<T>::add_ru(Num<T>::add_ru(fabs(st.base), rA), st.e), st.e);
   }
 }
@@ -307,9 +323,10 @@ SPK_DEV void pack_next(const State<T, C, MODE>& st, T gamma_next, T* out) {
 // Final bound of a width-1 output: lo/hi rounded outward.
 template <typename T, int C, int MODE>
 SPK_DEV void final_bounds(const State<T, C, MODE>& st, double& lo, double& hi) {
-  if (MODE == MODE_POINT) {
+  constexpr int BM = bound_mode(MODE);
+  if (BM == MODE_POINT) {
     lo = hi = (double)st.base;
-  } else if (MODE == MODE_INTERVAL) {
+  } else if (BM == MODE_INTERVAL) {
     lo = (double)Num<T>::sub_rd(st.base, st.e);
     hi = (double)Num<T>::add_ru(st.base, st.e);
   } else {
@@ -319,12 +336,29 @@ SPK_DEV void final_bounds(const State<T, C, MODE>& st, double& lo, double& hi) {
   }
 }
 
+// State of one (neuron, box) from its accumulated columns (+ the bias term's
+// rounding budget be on the error column; march modes carry the point value
+// in column 0).
+template <typename T, int C, int MODE>
+SPK_DEV State<T, C, MODE> state_from(const T* col, T be) {
+  constexpr int BM = bound_mode(MODE), OFF = pv_off(MODE);
+  State<T, C, MODE> st;
+  st.pv = OFF ? col[0] : T(0);
+  st.base = col[OFF];
+  if (BM == MODE_AFFINE) {
+#pragma unroll
+    for (int j = 0; j < State<T, C, MODE>::S; ++j) st.A[j] = col[OFF + 1 + j];
+  }
+  st.e = (BM == MODE_POINT) ? T(0) : Num<T>::add_ru(col[C - 1], be);
+  return st;
+}
+
 // ------------------------------------------------------------ dense layers
 // Generic layer: register-tiled contraction over the W ring.  The
 // round-to-nearest columns are summed in blocks of SUB k-steps (fresh
 // partials added to the running sums), so the rounding budget is
 // gamma_{SUB + ceil(m_in/SUB) + 1} instead of gamma_{m_in + 1}.
-template <typename T, int C, int MMAX>
+template <typename T, int C, int MMAX, int BIAS2 = -1>
 SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, WRing<T, C, MMAX>& ring, int tid,
                                 T (&acc)[Cfg<T, C, MMAX>::TI][Cfg<T, C, MMAX>::TB][C]) {
   using CF = Cfg<T, C, MMAX>;
@@ -339,7 +373,7 @@ SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, W
     for (int tb = 0; tb < TB; ++tb) {
       acc[ti][tb][0] = b0;
 #pragma unroll
-      for (int c = 1; c < C; ++c) acc[ti][tb][c] = T(0);
+      for (int c = 1; c < C; ++c) acc[ti][tb][c] = (c == BIAS2) ? b0 : T(0);
     }
   }
 
@@ -458,7 +492,7 @@ SPK_DEV f32x2 f2_pack(float lo, float hi) {
 // pairs, an optional odd RN column, and the round-up error column (scalar
 // FFMA.RP with the |W| operand modifier).  Point evaluation (C == 1) pairs
 // adjacent boxes instead.  Same blocked-summation budget as the scalar loop.
-template <int C, int MMAX>
+template <int C, int MMAX, int BIAS2 = -1>
 SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__ X, WRing<float, C, MMAX>& ring,
                              int tid, float (&acc)[Cfg<float, C, MMAX>::TI][Cfg<float, C, MMAX>::TB][C]) {
   using CF = Cfg<float, C, MMAX>;
@@ -484,7 +518,8 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
         // the bias enters the base column (column 0, or every box for POINT)
-        accp[ti][g][p] = POINT ? f2_pack(b0, b0) : (p == 0 ? f2_pack(b0, 0.f) : f2_pack(0.f, 0.f));
+        accp[ti][g][p] = POINT ? f2_pack(b0, b0)
+                               : (p == 0 ? f2_pack(b0, BIAS2 == 1 ? b0 : 0.f) : f2_pack(0.f, 0.f));
         partp[ti][g][p] = 0ull;
       }
 #pragma unroll
@@ -600,13 +635,15 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
   }
 }
 
-template <typename T, int C, int MMAX>
+// BIAS2 >= 0: a second column that also starts from the bias (march modes:
+// the point value in column 0 and the bound's base in column 1)
+template <typename T, int C, int MMAX, int BIAS2 = -1>
 SPK_DEV void dense_kloop(const LayerDev<T>& L, const T* __restrict__ X, WRing<T, C, MMAX>& ring, int tid,
                          T (&acc)[Cfg<T, C, MMAX>::TI][Cfg<T, C, MMAX>::TB][C]) {
   if constexpr (sizeof(T) == 4 && SPK_PACKED_F32) {
-    dense_kloop_f32<C, MMAX>(L, X, ring, tid, acc);
+    dense_kloop_f32<C, MMAX, BIAS2>(L, X, ring, tid, acc);
   } else {
-    dense_kloop_scalar<T, C, MMAX>(L, X, ring, tid, acc);
+    dense_kloop_scalar<T, C, MMAX, BIAS2>(L, X, ring, tid, acc);
   }
 }
 
@@ -617,7 +654,7 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
   constexpr int TI = CF::TI, TB = CF::TB, CP = CF::CP;
   const int ng = tid % CF::NG, bg = tid / CF::NG;
   T acc[TI][TB][C];
-  dense_kloop<T, C, MMAX>(L, X, ring, tid, acc);
+  dense_kloop<T, C, MMAX, (MODE >= MODE_MI ? 1 : -1)>(L, X, ring, tid, acc);
 
   // epilogue: activation rules, write next X in place (one contiguous
   // TB*CP vector per neuron: the thread's boxes are adjacent in the row)
@@ -663,13 +700,7 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
 #pragma unroll
     for (int tb = 0; tb < TB; ++tb) {
       if (valid) {
-        State<T, C, MODE> st;
-        st.base = acc[ti][tb][0];
-        if (MODE == MODE_AFFINE) {
-#pragma unroll
-          for (int j = 0; j < State<T, C, MODE>::S; ++j) st.A[j] = acc[ti][tb][1 + j];
-        }
-        st.e = (MODE == MODE_POINT) ? T(0) : Num<T>::add_ru(acc[ti][tb][C - 1], be);
+        State<T, C, MODE> st = state_from<T, C, MODE>(acc[ti][tb], be);
         for (int a = 0; a < L.n_act; ++a) apply_act<T, C, MODE>(st, L.act[a]);
         pack_next<T, C, MODE>(st, gamma_next, out + tb * CP);
       }
@@ -729,13 +760,12 @@ SPK_DEV void narrow_layer(const LayerDev<T>& L, T* __restrict__ X, T* __restrict
   for (int it = tid; it < items; it += NT) {
     const int b = it / L.m_out, i = it % L.m_out;
     const T* src = NBUF + ((size_t)b * NARROW_MAX + i) * CP;
-    State<T, C, MODE> st;
-    st.base = src[0] + L.bias[i];
-    if (MODE == MODE_AFFINE) {
+    T col[C];
 #pragma unroll
-      for (int j = 0; j < State<T, C, MODE>::S; ++j) st.A[j] = src[1 + j];
-    }
-    st.e = (MODE == MODE_POINT) ? T(0) : Num<T>::add_ru(src[C - 1], L.berr[i]);
+    for (int c = 0; c < C; ++c) col[c] = src[c];
+    col[0] += L.bias[i];
+    if (pv_off(MODE)) col[1] += L.bias[i];  // march modes: the bound's base column too
+    State<T, C, MODE> st = state_from<T, C, MODE>(col, L.berr[i]);
     for (int a = 0; a < L.n_act; ++a) apply_act<T, C, MODE>(st, L.act[a]);
     if (last) {
       emit(b, st);

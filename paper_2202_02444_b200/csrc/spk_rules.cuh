@@ -176,12 +176,34 @@ SPK_DEV int affine_rule(int act, T lo, T hi, T& alpha, T& beta, T& gamma) {
 template <typename T>
 SPK_RULE void interval_image_slow(int act, T lo, T hi, T& out_lo, T& out_hi);
 
+// FP32 sin image for |lo|, |hi| <= 2048 (range_core.py:338-345).  sinf is
+// within 2 ulp (<= 2^-23 absolute on [-1, 1]).  The FP32 modular test can
+// only misplace an extremum by the rounding of (x - pi/2)/2pi, k*2pi and the
+// adds: <= 6e-4 for |x| <= 2048.  A peak wrongly detected yields +-1 (safe);
+// a peak wrongly missed lies within 6e-4 of an endpoint, where sin is within
+// (6e-4)^2/2 < 2e-7 of +-1, so the 2^-18 pad keeps the image sound.  Larger
+// arguments take the FP64 path.
+SPK_DEV bool sin_image_f32(float lo, float hi, float& out_lo, float& out_hi) {
+  if (!(fabsf(lo) <= 2048.f && fabsf(hi) <= 2048.f)) return false;
+  constexpr float kTwoPiF = 6.2831855f, kHalfPiF = 1.5707964f, pad = 3.814697265625e-06f;  // 2^-18
+  const float sl = sinf(lo), sh = sinf(hi);
+  float mn = __fsub_rd(fminf(sl, sh), pad), mx = __fadd_ru(fmaxf(sl, sh), pad);
+  if (floorf((hi - kHalfPiF) / kTwoPiF) * kTwoPiF + kHalfPiF >= lo) mx = 1.f;
+  if (floorf((hi + kHalfPiF) / kTwoPiF) * kTwoPiF - kHalfPiF >= lo) mn = -1.f;
+  out_lo = fmaxf(mn, -1.f);
+  out_hi = fminf(mx, 1.f);
+  return true;
+}
+
 template <typename T>
 SPK_DEV void interval_image(int act, T lo, T hi, T& out_lo, T& out_hi) {
   if (act == ACT_RELU) {
     out_lo = fmax(lo, T(0));
     out_hi = fmax(hi, T(0));
     return;
+  }
+  if constexpr (sizeof(T) == 4) {
+    if (act == ACT_SIN && sin_image_f32(lo, hi, out_lo, out_hi)) return;
   }
   interval_image_slow<T>(act, lo, hi, out_lo, out_hi);
 }
