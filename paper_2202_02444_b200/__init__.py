@@ -42,7 +42,16 @@ from .range_core import (
 )
 
 from .camera import Camera
-from .rays import HitResult, Ray, RayCastParams, cast_camera, cast_ray, cast_rays, march_arrays
+from .rays import (
+    HitResult,
+    Ray,
+    RayCastParams,
+    cast_camera,
+    cast_camera_sharded,
+    cast_ray,
+    cast_rays,
+    march_arrays,
+)
 from .spatial import (
     AABB,
     TreeNode,

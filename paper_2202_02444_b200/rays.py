@@ -161,3 +161,26 @@ def cast_camera(net, camera: Camera, params: RayCastParams = RayCastParams(), po
                                      shared_origin=True)
     h, w = camera.height, camera.width
     return hit.reshape(h, w), t.reshape(h, w), steps.reshape(h, w), st
+
+
+def cast_camera_sharded(net, camera: Camera, rank: int, world: int, params: RayCastParams = RayCastParams(),
+                        policy=None, precision: str = "fp64", tile: int = 16, device=None):
+    """This rank's share of a camera image: interleaved tile x tile pixel
+    tiles (tile i -> rank i mod world, shard.pixel_tiles) for static load
+    balance; no collective inside the march.  Returns (pixel_index tensor,
+    hit, t, steps, stats) for the rank's pixels (row-major image indices)."""
+    from .shard import pixel_tiles
+
+    torch = dv._torch()
+    dirs = camera.pixel_dirs_device(device).reshape(-1, 3)
+    w, h = camera.width, camera.height
+    idx = []
+    for ty, tx in pixel_tiles(w, h, tile, rank, world):
+        ys = torch.arange(ty, min(ty + tile, h), device=dirs.device)
+        xs = torch.arange(tx, min(tx + tile, w), device=dirs.device)
+        idx.append((ys[:, None] * w + xs[None, :]).reshape(-1))
+    pix = torch.cat(idx) if idx else torch.zeros(0, dtype=torch.int64, device=dirs.device)
+    sel = dirs.index_select(0, pix).contiguous()
+    origin = torch.from_numpy(camera.position).to(dirs.device)
+    hit, t, steps, st = march_arrays(net, origin, sel, params, policy, precision=precision, shared_origin=True)
+    return pix, hit, t, steps, st

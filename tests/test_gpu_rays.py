@@ -92,3 +92,21 @@ def test_cast_rays_api_and_edge_cases(nets):
     want = orc.march(orc.as_oracle_net(box), o, d, orc.MarchParams(t_max=4.0), "affine-fixed",
                      t_init=[1.0], sigma_init=[0.01])
     assert bool(h1[0]) == bool(want[0][0]) and t1[0] == want[1][0] and s1[0] == want[2][0]
+
+
+def test_camera_sharded_union_equals_full(nets):
+    """Pixel-tile sharding: the union of 3 ranks' pixels reproduces the full image."""
+    import torch
+
+    cam = sp.Camera(np.array([1.6, 1.2, 2.0]), np.zeros(3), np.array([0.0, 1.0, 0.0]), 40.0, (40, 24))
+    net = nets["relu_sdf"]
+    hit, t, steps, _ = sp.cast_camera(net, cam, sp.RayCastParams(), "affine-fixed", precision="fp64")
+    full_t = t.reshape(-1).cpu().numpy()
+    got = np.full(full_t.shape, np.nan)
+    for r in range(3):
+        pix, h, tr, s, _ = sp.cast_camera_sharded(net, cam, r, 3, sp.RayCastParams(), "affine-fixed",
+                                                  precision="fp64", tile=16)
+        p = pix.cpu().numpy()
+        assert np.all(np.isnan(got[p]))
+        got[p] = tr.cpu().numpy()
+    np.testing.assert_array_equal(got, full_t)

@@ -1,0 +1,30 @@
+"""Small run of every kernel family, for compute-sanitizer (one tool per run):
+fused bound (interval / fixed / truncate / full, FP32 + FP64), point eval, tree
+build (fixed + convergence), fused and unfused march, marching cubes."""
+import sys
+
+import numpy as np
+
+sys.path.insert(0, ".")
+import paper_2202_02444_b200 as sp  # noqa: E402
+from paper_2202_02444_b200 import meshing, spatial, synth  # noqa: E402
+
+net = synth.random_mlp(64, 3, "relu", "torch-uniform", seed=1)
+small = sp.load_network("tests/golden/nets/relu12.json")
+rng = np.random.default_rng(0)
+c = rng.uniform(-1, 1, (700, 3))
+a = np.zeros((700, 3, 3))
+a[:, np.arange(3), np.arange(3)] = 0.05
+for pol in ("interval", "affine-fixed", "affine-truncate:8"):
+    for prec in ("fp32", "fp64"):
+        sp.range_bound_batch(net, c, a, pol, precision=prec)
+sp.range_bound_batch(small, c, a, "affine-full")
+sp.eval_batch(net, c, precision="fp32")
+b = spatial.AABB(-np.ones(3), np.ones(3))
+spatial.build_spatial_tree_arrays(net, b, policy="affine-fixed", max_depth=6)
+spatial.build_spatial_tree_arrays(small, b, delta=0.3, policy="interval")
+cam = sp.Camera(np.array([1.6, 1.2, 2.0]), np.zeros(3), np.array([0.0, 1.0, 0.0]), 40.0, (16, 8))
+sp.cast_camera(net, cam, sp.RayCastParams(t_max=3.0), "affine-fixed", precision="fp32")
+sp.cast_camera(net, cam, sp.RayCastParams(t_max=3.0), "affine-truncate:8", precision="fp32")
+meshing.extract_mesh_arrays(net, b, 4, 3, "affine-fixed")
+print("sanitize smoke done")
