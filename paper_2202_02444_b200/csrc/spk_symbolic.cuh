@@ -11,14 +11,17 @@
 //   B. per box: L1 norm of every live old symbol over all neurons (warp
 //      shuffles + fixed-order cross-warp sum, deterministic);
 //   C. per box, one warp: keep the n_keep largest candidates by (norm desc,
-//      index asc) -- the reference's stable argsort -- with
-//      n_keep rounds of a warp arg-max; kept symbols stay in index order;
+//      index asc) -- the reference's stable argsort: a 32-step
+//      binary search for the n_keep-th largest norm bit pattern with warp
+//      REDUX counts, then ballot prefixes keep ties in index order; kept
+//      symbols stay in index order;
 //   D. every (neuron, box): rebuild the row in the kept order and fold the
 //      dropped |coefficients| into the error channel with round-up adds.
 // affine-full is the same path with nothing ever dropped (capacity KC must
 // hold s + sum of activation widths).  The symbol count is uniform across
 // boxes (it depends only on layer widths), so every box has the same layout.
 #pragma once
+#include <type_traits>
 #include "spk_kernels.cuh"
 
 namespace spk {
@@ -140,50 +143,60 @@ SPK_DEV void sym_activation(int act, int m_out, int& nsym, const SymParams& P, T
       }
       return fabs(NEWG[b * MMAX + (c - n_old)]);
     };
+    // Top-n_keep by (norm desc, index asc) -- the reference's stable argsort
+    // (SPEC.md:215).  Norms are >= 0, so their IEEE bit patterns order like
+    // the values: binary-search the n_keep-th largest key K with warp-wide
+    // counts (REDUX), keep every key > K and the lowest-index keys == K.
+    using KeyT = typename std::conditional<sizeof(T) == 4, unsigned, unsigned long long>::type;
     constexpr int PER = (SC::CAND + 31) / 32;
-    T val[PER];
+    constexpr int KBITS = 8 * (int)sizeof(KeyT);
+    KeyT key[PER];
+    bool valid[PER];
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
       const int c = lane + 32 * q;
-      val[q] = c < total ? norm_of(c) : T(-1);
+      valid[q] = c < total;
+      const T v = valid[q] ? norm_of(c) : T(0);
+      if constexpr (sizeof(T) == 4) key[q] = __float_as_uint((float)v);
+      else key[q] = (KeyT)__double_as_longlong((double)v);
     }
-    int mine = -1;  // this lane's pick for output rank == lane
-    for (int round = 0; round < P.n_keep; ++round) {
-      // local best: largest value, lowest candidate index on ties
-      T bv = T(-2);
-      int bc = 1 << 30;
+    KeyT klo = 0, khi = ~(KeyT)0;
+    for (int it = 0; it < KBITS && klo < khi; ++it) {
+      const KeyT mid = klo + (khi - klo) / 2 + 1;
+      unsigned cnt = 0;
 #pragma unroll
-      for (int q = 0; q < PER; ++q) {
-        const int c = lane + 32 * q;
-        if (val[q] > bv || (val[q] == bv && c < bc)) { bv = val[q]; bc = c; }
-      }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const T ov = __shfl_xor_sync(0xffffffffu, bv, off);
-        const int oc = __shfl_xor_sync(0xffffffffu, bc, off);
-        if (ov > bv || (ov == bv && oc < bc)) { bv = ov; bc = oc; }
-      }
-      if ((bc & 31) == lane) {
-#pragma unroll
-        for (int q = 0; q < PER; ++q)
-          if (lane + 32 * q == bc) val[q] = T(-3);
-      }
-      if (lane == round) mine = bc;
+      for (int q = 0; q < PER; ++q) cnt += (valid[q] && key[q] >= mid) ? 1u : 0u;
+      cnt = __reduce_add_sync(0xffffffffu, cnt);
+      if (cnt >= (unsigned)P.n_keep) klo = mid;
+      else khi = mid - 1;
     }
-    // kept symbols in index order: rank of each pick among all picks
-    int rank = 0;
-    for (int q = 0; q < P.n_keep; ++q) {
-      const int other = __shfl_sync(0xffffffffu, mine, q);
-      rank += (lane < P.n_keep && other < mine) ? 1 : 0;
-    }
+    const KeyT kth = klo;
+    unsigned greater = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) greater += (valid[q] && key[q] > kth) ? 1u : 0u;
+    greater = __reduce_add_sync(0xffffffffu, greater);
+    const int need_eq = P.n_keep - (int)greater;
+    // kept flags in index order (candidate c = lane + 32 q: q-major, lane-minor)
+    const unsigned lt = (1u << lane) - 1u;
+    int eq_seen = 0, kept_seen = 0;
     for (int p = lane; p < KC; p += 32) slot_old[p] = -1;
     __syncwarp();
-    if (lane < P.n_keep) {
-      kept[rank] = mine;
-      if (mine < n_old) slot_old[mine] = rank;
-    } else if (lane < KC) {
-      kept[lane] = -1;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const bool eq = valid[q] && key[q] == kth;
+      const unsigned meq = __ballot_sync(0xffffffffu, eq);
+      const bool keep = (valid[q] && key[q] > kth) || (eq && eq_seen + __popc(meq & lt) < need_eq);
+      eq_seen += __popc(meq);
+      const unsigned mk = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const int slot = kept_seen + __popc(mk & lt);
+        const int c = lane + 32 * q;
+        kept[slot] = c;
+        if (c < n_old) slot_old[c] = slot;
+      }
+      kept_seen += __popc(mk);
     }
+    for (int p = P.n_keep + lane; p < KC; p += 32) kept[p] = -1;
   }
   csync();
 
