@@ -17,6 +17,7 @@
  *                                        (NumPy) arrays, copies included
  *   spk_tree_build                    <- build_spatial_tree (spatial.py:214-289)
  *   spk_march                         <- _march_arrays (rays.py:88-138)
+ *   spk_frustum_cast                  <- cast_frustum_image (rays.py:232-341)
  *   spk_mesh_blocks / spk_mesh_cells  <- extract_mesh (meshing.py:111-169)
  *
  * Conventions: plain pointers and sizes, no torch types.  "Device" pointers
@@ -174,6 +175,24 @@ int spk_march(const spk_net* net, int policy, int n_keep, int precision, int64_t
  * forward, right, true_up (host), dirs (device) = height x width x 3. */
 int spk_camera_dirs(const double* frame9, double half_w, double half_h, int width, int height,
                     double* dirs, void* stream);
+
+/* §8(f1): frustum range-marching of a whole camera image
+ * (cast_frustum_image, rays.py:232-341).  position3, frame9 (forward, right,
+ * true_up), params6 (RayCastParams: t_max, sigma0, eta+, eta-, delta,
+ * safety) are host arrays; half_w / half_h are Camera.half_extents.  The
+ * width x height image is split into an initial_grid x initial_grid block
+ * grid (min'd with the resolution; it must divide it, else
+ * SPK_ERR_INVALID_PARAMETER).  Frusta march by slab-box bounds
+ * (frustum_slab_box, camera.py:99-135) through spk_bound_batch and split
+ * while their front face is wider than 2 sigma; single pixels finish via
+ * spk_march.  hit (u8), t, steps (amortised per-pixel steps) are row-major
+ * height x width DEVICE images.  stats (host, 4, optional): frustum rounds,
+ * frustum steps, single-pixel hand-offs, their ray steps.  Returns after
+ * the stream has drained. */
+int spk_frustum_cast(const spk_net* net, int policy, int n_keep, int precision, const double* position3,
+                     const double* frame9, double half_w, double half_h, int width, int height,
+                     int initial_grid, const double* params6, uint8_t* hit, double* t, double* steps,
+                     int64_t* stats, void* stream);
 
 /* K7: hierarchical marching cubes (extract_mesh, meshing.py:111-169) at
  * resolution 2^m over the host box lo3..hi3; prune = 1 runs the index-range

@@ -582,6 +582,129 @@ def pixel_dirs(position, look_at, up, vertical_fov, width, height):
     return d / np.linalg.norm(d, axis=2, keepdims=True)
 
 
+class _PinholeRays:
+    """Single-pixel directions and slab boxes (camera.py:85-135)."""
+
+    def __init__(self, position, look_at, up, vertical_fov, width, height):
+        self.pos = np.asarray(position, dtype=np.float64)
+        self.fwd, self.right, self.tup = camera_frame(position, look_at, up)
+        self.hh = math.tan(math.radians(vertical_fov) / 2.0)
+        self.hw = self.hh * width / height
+        self.w, self.h = width, height
+
+    def u(self, i):
+        return ((float(i) + 0.5) / self.w * 2.0 - 1.0) * self.hw
+
+    def v(self, j):
+        return (1.0 - (float(j) + 0.5) / self.h * 2.0) * self.hh
+
+    def dir(self, i, j):
+        d = self.fwd + self.u(i) * self.right + self.v(j) * self.tup
+        return d / np.linalg.norm(d)
+
+    def corners(self, px0, px1, py0, py1):
+        return (self.dir(px0, py1 - 1), self.dir(px1 - 1, py1 - 1), self.dir(px0, py0), self.dir(px1 - 1, py0))
+
+    def slab(self, px0, px1, py0, py1, t0, t1):
+        """Hull of the 9 candidate unit directions (pixel-centre corners and
+        zero-clamped midlines) scaled by t0 and t1, per frame axis."""
+        u0, u1 = self.u(px0), self.u(px1 - 1)
+        v0, v1 = self.v(py1 - 1), self.v(py0)
+        uc = min(max(0.0, u0), u1)
+        vc = min(max(0.0, v0), v1)
+        ws = []
+        for vv in (v0, v1, vc):
+            for uu in (u0, u1, uc):
+                ell = np.sqrt(1.0 + uu * uu + vv * vv)
+                ws.append((1.0 / ell, uu / ell, vv / ell))
+        ws = np.array(ws)
+        wmin, wmax = ws.min(axis=0), ws.max(axis=0)
+        lo = np.minimum(t0 * wmin, t1 * wmin)
+        hi = np.maximum(t0 * wmax, t1 * wmax)
+        mid, half = (lo + hi) / 2.0, (hi - lo) / 2.0
+        centre = self.pos + mid[0] * self.fwd + mid[1] * self.right + mid[2] * self.tup
+        axes = [half[k] * vec for k, vec in enumerate((self.fwd, self.right, self.tup)) if half[k] > 0.0]
+        return centre, np.array(axes).reshape(-1, 3)
+
+
+def frustum_cast(net, position, look_at, up, vertical_fov, width, height, params=MarchParams(),
+                 policy="affine-fixed", initial_grid=16):
+    """Frustum range-march over the pixel grid (rays.py:232-341).
+
+    Rectangles of pixels march together while their front face is narrower
+    than 2 sigma; wider ones split across the longer pixel side.  Single
+    pixels finish with the per-ray march from their frustum's (t, sigma).
+    Returns (hit (H, W) bool, t (H, W), steps (H, W))."""
+    net = as_oracle_net(net)
+    cam = _PinholeRays(position, look_at, up, vertical_fov, width, height)
+    gw, gh = min(initial_grid, width), min(initial_grid, height)
+    if width % gw or height % gh:
+        raise ValueError("resolution not divisible into the frustum grid")
+    hit = np.zeros((height, width), dtype=bool)
+    t_img = np.full((height, width), np.inf)
+    steps = np.zeros((height, width))
+    if eval_points(net, cam.pos[None, :])[0] == 0.0:
+        return np.ones_like(hit), np.zeros_like(t_img), steps
+    bw, bh = width // gw, height // gh
+    # frustum record: [px0, px1, py0, py1, t, sigma, corner dirs]
+    live = [[bx * bw, bx * bw + bw, by * bh, by * bh + bh, 0.0, params.s0]
+            for by in range(gh) for bx in range(gw)]
+    singles = []
+    while live:
+        todo, live, batch = live, [], []
+        while todo:
+            f = todo.pop()
+            px0, px1, py0, py1, t, sig = f
+            nx, ny = px1 - px0, py1 - py0
+            if nx * ny == 1:
+                singles.append(f)
+                continue
+            if t >= params.t_max:
+                continue
+            r00, r10, r01, r11 = cam.corners(px0, px1, py0, py1)
+            split_x = (nx >= ny and nx > 1) or ny == 1
+            if split_x:
+                width_w = t * max(np.linalg.norm(r10 - r00), np.linalg.norm(r11 - r01))
+            else:
+                width_w = t * max(np.linalg.norm(r01 - r00), np.linalg.norm(r11 - r10))
+            if width_w > 2.0 * sig:
+                if split_x:
+                    m = px0 + nx // 2
+                    todo += [[px0, m, py0, py1, t, sig], [m, px1, py0, py1, t, sig]]
+                else:
+                    m = py0 + ny // 2
+                    todo += [[px0, px1, py0, m, t, sig], [px0, px1, m, py1, t, sig]]
+                continue
+            batch.append(f)
+        if not batch:
+            break
+        slabs = [cam.slab(f[0], f[1], f[2], f[3], f[4], f[4] + f[5]) for f in batch]
+        s = max(a.shape[0] for _, a in slabs)
+        centres = np.array([c for c, _ in slabs])
+        axes = np.zeros((len(batch), s, 3))
+        for i, (_, a) in enumerate(slabs):
+            axes[i, : a.shape[0]] = a
+        blo, bhi = bound_batch(net, centres, axes, policy)
+        for f, lo_, hi_ in zip(batch, blo, bhi):
+            steps[f[2]:f[3], f[0]:f[1]] += 1.0 / ((f[1] - f[0]) * (f[3] - f[2]))
+            if lo_ > 0.0 or hi_ < 0.0:
+                f[4] += max(params.safety * f[5], params.delta)
+                f[5] *= params.eta_plus
+            else:
+                f[5] *= params.eta_minus
+            live.append(f)
+    if singles:
+        dirs = np.array([cam.dir(f[0], f[2]) for f in singles])
+        origins = np.broadcast_to(cam.pos, dirs.shape).copy()
+        h1, t1, s1 = march(net, origins, dirs, params, policy,
+                           t_init=[f[4] for f in singles], sigma_init=[f[5] for f in singles])
+        for f, a, b, c in zip(singles, h1, t1, s1):
+            hit[f[2], f[0]] = a
+            t_img[f[2], f[0]] = b
+            steps[f[2], f[0]] += c
+    return hit, t_img, steps
+
+
 # ---------------------------------------------------------------------------
 # Marching-cubes tables (mc_tables.py:24-105): generated, not the classic table
 

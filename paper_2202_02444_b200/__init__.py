@@ -43,11 +43,14 @@ from .range_core import (
 
 from .camera import Camera
 from .rays import (
+    Frustum,
+    FrustumCastResult,
     HitResult,
     Ray,
     RayCastParams,
     cast_camera,
     cast_camera_sharded,
+    cast_frustum_image,
     cast_ray,
     cast_rays,
     march_arrays,

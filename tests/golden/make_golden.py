@@ -202,6 +202,26 @@ def gen_rays(nets, out):
     out["camera/relu_sdf/steps"] = steps
 
 
+FRONT_CAM = dict(position=np.array([0.13, 0.11, 2.4]), look_at=np.array([0.02, -0.03, 0.0]),
+                 up=np.array([0.0, 1.0, 0.0]), vertical_fov=40.0)
+
+
+def gen_frustum(nets, out):
+    """cast_frustum_image (rays.py:232-341) on the box oracle (reference
+    test_rays.py:226-242 camera) and on relu_sdf with the bench camera."""
+    cases = [
+        ("box_front64", "box", sp.Camera(resolution=(64, 64), **FRONT_CAM), sp.RayCastParams(t_max=4.0), 16),
+        ("relu_sdf_default48", "relu_sdf",
+         sp.Camera(np.array([1.6, 1.2, 2.0]), np.zeros(3), np.array([0.0, 1.0, 0.0]), 40.0, (48, 32)),
+         sp.RayCastParams(), 8),
+    ]
+    for tag, netname, cam, params, grid in cases:
+        res = sp.cast_frustum_image(nets[netname], cam, params, sp.AFFINE_FIXED, initial_grid=grid)
+        out[f"frustum/{tag}/hit"] = res.hit
+        out[f"frustum/{tag}/t"] = res.t
+        out[f"frustum/{tag}/steps"] = res.steps
+
+
 def gen_mesh(nets, out):
     bounds = sp.AABB(np.full(3, -1.0), np.full(3, 1.0))
     for tag, netname, m, pol in (
@@ -232,6 +252,7 @@ def main():
     gen_trees(nets, out)
     gen_rays(nets, out)
     gen_mesh(nets, out)
+    gen_frustum(nets, out)
     np.savez_compressed(HERE / "golden.npz", **out)
     meta = {"reference": REF_SRC, "numpy": np.__version__, "n_arrays": len(out)}
     (HERE / "golden_meta.json").write_text(json.dumps(meta, indent=1))

@@ -137,3 +137,21 @@ def test_package_mc_tables_match_reference(golden):
     np.testing.assert_array_equal(np.array(mc_tables.EDGE_TABLE), golden["mc/edge_table"])
     table, count = mc_tables.flat_tables()
     assert table.shape == (256, 15) and int(count.sum()) == 820
+
+
+# cast_frustum_image cases in make_golden.py:gen_frustum
+FRUSTA = {
+    "box_front64": ("box", ([0.13, 0.11, 2.4], [0.02, -0.03, 0.0], [0.0, 1.0, 0.0], 40.0, 64, 64),
+                    orc.MarchParams(t_max=4.0), 16),
+    "relu_sdf_default48": ("relu_sdf", ([1.6, 1.2, 2.0], [0.0, 0.0, 0.0], [0.0, 1.0, 0.0], 40.0, 48, 32),
+                           orc.MarchParams(), 8),
+}
+
+
+@pytest.mark.parametrize("tag", sorted(FRUSTA))
+def test_frustum_cast_matches_reference(golden, net_paths, tag):
+    netname, cam, params, grid = FRUSTA[tag]
+    hit, t, steps = orc.frustum_cast(orc.load_net(net_paths[netname]), *cam, params, "affine-fixed", grid)
+    np.testing.assert_array_equal(hit, golden[f"frustum/{tag}/hit"])
+    np.testing.assert_array_equal(t, golden[f"frustum/{tag}/t"])
+    np.testing.assert_array_equal(steps, golden[f"frustum/{tag}/steps"])
