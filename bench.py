@@ -11,7 +11,9 @@ At N > 1 the frontier below a redundant top cut is split across ranks (one
 process per GPU, no collective in the build): total work is fixed, so
 scaling is "strong".  `extra` carries the C5 throughput sweep point
 (16M on-device cubes, 8x256, one launch), C1 (4x32, 64^3 grid) and C3
-(SIREN 8x256 ray casting: rays/s, interval at 1024^2, truncate:16 at 256^2).
+(SIREN 8x256 ray casting: rays/s, interval at 1024^2, truncate:16 at 256^2),
+C4 (ELU 8x512 mesh at 256^3) and F1 (frustum vs per-pixel casting, 1024^2,
+on the reference's relu_sdf fixture).
 
 Timing: W untimed warm-up steps, then K steps, each bracketed by a barrier
 and torch.cuda.synchronize(), timed with CUDA events on the launching
@@ -339,6 +341,7 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_rays:
         extra["C3_siren_rays_interval_1024sq"] = bench_c3(torch, sp, synth, "interval", 1024)
         extra["C3_siren_rays_truncate16_256sq"] = bench_c3(torch, sp, synth, "affine-truncate:16", 256)
+        extra["F1_frustum_relu_sdf_1024sq"] = bench_frustum(torch, sp, 1024)
 
     # ---- e2e through the public API (host arrays out)
     e2e = bench_e2e_tree(torch, sp, spatial, net, bounds, args)
@@ -433,6 +436,37 @@ def bench_c3(torch, sp, synth, policy, res):
     return {"rays": n, "rays_per_s": n / dt, "ms": dt * 1e3, "ray_steps": st.ray_steps,
             "steps_per_ray": st.ray_steps / n, "certified_steps": st.certified_steps,
             "lockstep_rounds": st.rounds, "hit_fraction": float(hit.float().mean().item()), "policy": policy}
+
+
+def bench_frustum(torch, sp, res):
+    """§8(f1): cast_frustum_image (rays.py:232-341) vs per-pixel casting on the
+    reference's trained relu_sdf fixture (tests/golden/nets, 7x32), default
+    camera, RayCastParams() defaults, FP32 kernels, images left on the device.
+    (The random-init C3 SIREN outputs ~1e-11, so nothing certifies there and
+    every frustum dissolves into per-pixel rays -- no frustum workload.)"""
+    from paper_2202_02444_b200.camera import default_camera
+
+    net = sp.load_network(Path(__file__).resolve().parent / "tests" / "golden" / "nets" / "relu_sdf.json")
+    out = {"net": "relu_sdf (reference fixture, 7x32 ReLU)", "res": res}
+    for pol in ("affine-fixed", "interval"):
+        sp.cast_frustum_image(net, default_camera(64), sp.RayCastParams(), pol, precision="fp32", device_output=True)
+        sp.cast_camera(net, default_camera(64), sp.RayCastParams(), pol, precision="fp32")
+        torch.cuda.synchronize()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record()
+        fr = sp.cast_frustum_image(net, default_camera(res), sp.RayCastParams(), pol, precision="fp32",
+                                   device_output=True)
+        e[1].record()
+        _, _, steps, st = sp.cast_camera(net, default_camera(res), sp.RayCastParams(), pol, precision="fp32")
+        e[2].record()
+        torch.cuda.synchronize()
+        n = res * res
+        out[pol] = {"frustum_ms": e[0].elapsed_time(e[1]), "per_ray_ms": e[1].elapsed_time(e[2]),
+                    "frustum_rays_per_s": n / (e[0].elapsed_time(e[1]) / 1e3),
+                    "per_ray_rays_per_s": n / (e[1].elapsed_time(e[2]) / 1e3),
+                    "amortised_steps_per_pixel": float(fr.steps.sum().item()) / n,
+                    "per_ray_steps_per_pixel": st.ray_steps / n, **fr.stats.meta}
+    return out
 
 
 def bench_c4(torch, sp, synth, m):

@@ -186,9 +186,13 @@ int spk_camera_dirs(const double* frame9, double half_w, double half_h, int widt
  * (frustum_slab_box, camera.py:99-135) through spk_bound_batch and split
  * while their front face is wider than 2 sigma; single pixels finish via
  * spk_march.  hit (u8), t, steps (amortised per-pixel steps) are row-major
- * height x width DEVICE images.  stats (host, 4, optional): frustum rounds,
- * frustum steps, single-pixel hand-offs, their ray steps.  Returns after
- * the stream has drained. */
+ * height x width DEVICE images.  stats (host, 5, optional): frustum rounds,
+ * frustum steps, single-pixel hand-offs, their ray steps, frusta dissolved
+ * by the termination guard (an uncertified multi-pixel frustum whose sigma
+ * falls below delta * 2^-32 hands all its pixels to spk_march; the reference
+ * has no such guard and can loop forever at t = 0).  The frustum loop runs
+ * on the device (one small counter readback per round); the final hand-off
+ * march and scatter are asynchronous on `stream`. */
 int spk_frustum_cast(const spk_net* net, int policy, int n_keep, int precision, const double* position3,
                      const double* frame9, double half_w, double half_h, int width, int height,
                      int initial_grid, const double* params6, uint8_t* hit, double* t, double* steps,

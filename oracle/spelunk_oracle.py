@@ -692,6 +692,12 @@ def frustum_cast(net, position, look_at, up, vertical_fov, width, height, params
                 f[5] *= params.eta_plus
             else:
                 f[5] *= params.eta_minus
+                if f[5] < params.delta * 2.0 ** -32:
+                    # product termination guard (spk_frustum.cu), absent from
+                    # the reference; never reached in the golden cases
+                    singles += [[x, x + 1, y, y + 1, f[4], f[5]]
+                                for y in range(f[2], f[3]) for x in range(f[0], f[1])]
+                    continue
             live.append(f)
     if singles:
         dirs = np.array([cam.dir(f[0], f[2]) for f in singles])

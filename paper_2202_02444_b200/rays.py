@@ -234,7 +234,11 @@ def cast_frustum_image(net, camera: Camera, params: RayCastParams = RayCastParam
     the reference's cast_frustum_image.  Runs in the C-ABI
     (spk_frustum_cast): slab-box bounds of every marching frustum per round
     in one fused bound pass, single pixels finished by the device march.
-    stats.meta holds frustum_rounds / frustum_steps / pixel_handoffs."""
+    stats.meta holds frustum_rounds / frustum_steps / pixel_handoffs /
+    dissolved_frusta.  One guard is added to the reference's loop: an
+    uncertified multi-pixel frustum whose sigma falls below delta * 2^-32
+    dissolves into single-pixel hand-offs (the reference would loop forever
+    on a frustum at t = 0 whose bound cannot resolve |f| there)."""
     from .errors import InvalidCamera
 
     torch = dv._torch()
@@ -253,13 +257,13 @@ def cast_frustum_image(net, camera: Camera, params: RayCastParams = RayCastParam
     frame = np.ascontiguousarray(np.concatenate(camera.frame))
     hw, hh = camera.half_extents
     p6 = params.as_array()
-    stats = np.zeros(4, np.int64)
+    stats = np.zeros(5, np.int64)
     _lib.call("spk_frustum_cast", dn.ptr, pcode, n_keep, _precision_code(precision), pos.ctypes.data,
               frame.ctypes.data, hw, hh, w, h, initial_grid, p6.ctypes.data, hit.data_ptr(), t.data_ptr(),
               steps.data_ptr(), stats.ctypes.data, dv.stream_ptr(dev))
     st = MarchStats(rounds=int(stats[0]), ray_steps=int(stats[3]),
                     meta={"frustum_rounds": int(stats[0]), "frustum_steps": int(stats[1]),
-                          "pixel_handoffs": int(stats[2])})
+                          "pixel_handoffs": int(stats[2]), "dissolved_frusta": int(stats[4])})
     if device_output:
         return FrustumCastResult(hit.bool(), t, steps, st)
     return FrustumCastResult(hit.cpu().numpy().astype(bool), t.cpu().numpy(), steps.cpu().numpy(), st)

@@ -115,3 +115,21 @@ def test_frustum_device_output_and_grid_one(nets):
     # different initial grids change the frustum tree, not the contract
     both = h & b.hit
     assert np.max(np.abs(a.t.cpu().numpy()[both] - b.t[both]), initial=0.0) <= sp.RayCastParams().delta
+
+
+def test_frustum_termination_guard_siren():
+    """C3 SIREN (outputs ~1e-11): the FP32 bound cannot certify the camera
+    point, so every t = 0 frustum dissolves into pixel hand-offs instead of
+    looping; the per-ray contract still holds."""
+    from paper_2202_02444_b200 import synth
+    from paper_2202_02444_b200.camera import default_camera
+
+    net = synth.config_net("C3")
+    cam = default_camera(32)
+    p = sp.RayCastParams()
+    fr = sp.cast_frustum_image(net, cam, p, "affine-fixed", precision="fp32")
+    assert fr.stats.meta["dissolved_frusta"] > 0
+    hit, t, _, _ = sp.cast_camera(net, cam, p, "affine-fixed", precision="fp32")
+    hit, t = hit.cpu().numpy(), t.cpu().numpy()
+    np.testing.assert_array_equal(fr.hit, hit)
+    assert np.max(np.abs(fr.t[hit] - t[hit]), initial=0.0) <= p.delta
