@@ -18,6 +18,8 @@
  *   spk_tree_build                    <- build_spatial_tree (spatial.py:214-289)
  *   spk_march                         <- _march_arrays (rays.py:88-138)
  *   spk_frustum_cast                  <- cast_frustum_image (rays.py:232-341)
+ *   spk_render_shade                  <- _refine_hits / _normals / shading (render.py:59-141)
+ *   spk_fixed_step_march              <- _fixed_step_march (render.py:36-56)
  *   spk_mesh_blocks / spk_mesh_cells  <- extract_mesh (meshing.py:111-169)
  *
  * Conventions: plain pointers and sizes, no torch types.  "Device" pointers
@@ -197,6 +199,28 @@ int spk_frustum_cast(const spk_net* net, int policy, int n_keep, int precision, 
                      const double* frame9, double half_w, double half_h, int width, int height,
                      int initial_grid, const double* params6, uint8_t* hit, double* t, double* steps,
                      int64_t* stats, void* stream);
+
+/* §8(f2): render post-processing (render.py:59-141) for n pixel rays with
+ * device origins (origin_stride 0 = one shared camera origin, else 3),
+ * dirs, hit (u8) and t from a march: every hit is refined by `iters`
+ * bisections of [t, t + delta] (_refine_hits, render.py:59-76), shaded by
+ * Lambert max(0, n . light3) with the normal from central differences
+ * h = delta / 10 (_normals, render.py:79-88) and written as gray RGB into
+ * pixels (device, n x 3 u8); misses get background3.  light3 / background3
+ * are host arrays; n_hits (host, optional) receives the hit count (the call
+ * then synchronises the stream). */
+int spk_render_shade(const spk_net* net, int precision, int64_t n, const double* origins, int64_t origin_stride,
+                     const double* dirs, const uint8_t* hit, const double* t, double delta, int iters,
+                     const double* light3, const uint8_t* background3, uint8_t* pixels, int64_t* n_hits,
+                     void* stream);
+/* The uniform fixed-step baseline (_fixed_step_march, render.py:36-56):
+ * sample f at t = step, 2 step, ... (t accumulated as the reference's FP64
+ * sum) until t >= t_max; the first sign change against f(origin) reports a
+ * hit at the previous sample.  stats (host, 2, optional): rounds, point
+ * evaluations. */
+int spk_fixed_step_march(const spk_net* net, int precision, int64_t n, const double* origins, int64_t origin_stride,
+                         const double* dirs, double step, double t_max, uint8_t* hit, double* t, int64_t* stats,
+                         void* stream);
 
 /* K7: hierarchical marching cubes (extract_mesh, meshing.py:111-169) at
  * resolution 2^m over the host box lo3..hi3; prune = 1 runs the index-range

@@ -712,6 +712,77 @@ def frustum_cast(net, position, look_at, up, vertical_fov, width, height, params
 
 
 # ---------------------------------------------------------------------------
+# Rendering post-process (render.py:36-141)
+
+RENDER_BACKGROUND = np.array([24, 28, 38], dtype=np.uint8)
+RENDER_LIGHT = np.array([0.35, 0.75, 0.56]) / np.linalg.norm(np.array([0.35, 0.75, 0.56]))
+
+
+def fixed_step_march(net, origins, dirs, step, t_max):
+    """Uniform samples at t = step, 2 step, ... (t a running FP64 sum); the
+    first sign change reports a hit at the previous sample."""
+    net = as_oracle_net(net)
+    f0 = eval_points(net, origins)
+    hit = f0 == 0.0
+    t_hit = np.where(hit, 0.0, np.inf)
+    inside = f0 < 0.0
+    todo = np.flatnonzero(~hit)
+    t = step
+    while todo.size and t < t_max:
+        side = eval_points(net, origins[todo] + t * dirs[todo]) < 0.0
+        flipped = side != inside[todo]
+        hit[todo[flipped]] = True
+        t_hit[todo[flipped]] = t - step
+        todo = todo[~flipped]
+        t += step
+    return hit, t_hit
+
+
+def shade(net, origin, dirs, hit, t, delta, iters=48):
+    """Bisection refine of [t, t + delta], central-difference normal
+    (h = delta / 10), Lambert gray; background elsewhere.  (n, 3) uint8."""
+    net = as_oracle_net(net)
+    px = np.tile(RENDER_BACKGROUND, (len(dirs), 1))
+    sel = np.flatnonzero(hit)
+    if sel.size == 0:
+        return px
+    o = np.broadcast_to(origin, (sel.size, 3))
+    d = dirs[sel]
+    neg0 = eval_points(net, np.asarray(origin, dtype=np.float64)[None, :])[0] < 0.0
+    lo, hi = t[sel].copy(), t[sel] + delta
+    for _ in range(iters):
+        mid = 0.5 * (lo + hi)
+        cross = (eval_points(net, o + mid[:, None] * d) < 0.0) != neg0
+        lo, hi = np.where(cross, lo, mid), np.where(cross, mid, hi)
+    p = o + lo[:, None] * d
+    h = delta / 10.0
+    grad = np.stack([eval_points(net, p + h * e) - eval_points(net, p - h * e) for e in np.eye(3)], axis=1)
+    length = np.linalg.norm(grad, axis=1, keepdims=True)
+    length[length == 0.0] = 1.0
+    lam = np.clip((grad / length) @ RENDER_LIGHT, 0.0, 1.0)
+    px[sel] = np.rint(lam * 255.0).astype(np.uint8)[:, None]
+    return px
+
+
+def render(net, position, look_at, up, vertical_fov, width, height, params=MarchParams(),
+           policy="affine-fixed", mode="per_ray", step=None):
+    """render_image: march (per_ray / frustum / fixed_step) then shade;
+    returns the (height, width, 3) uint8 image."""
+    net = as_oracle_net(net)
+    dirs = pixel_dirs(position, look_at, up, vertical_fov, width, height).reshape(-1, 3)
+    pos = np.asarray(position, dtype=np.float64)
+    origins = np.broadcast_to(pos, dirs.shape).copy()
+    if mode == "per_ray":
+        hit, t, _ = march(net, origins, dirs, params, policy)
+    elif mode == "frustum":
+        hit, t, _ = frustum_cast(net, position, look_at, up, vertical_fov, width, height, params, policy)
+        hit, t = hit.reshape(-1), t.reshape(-1)
+    else:
+        hit, t = fixed_step_march(net, origins, dirs, step, params.t_max)
+    return shade(net, pos, dirs, hit, t, params.delta).reshape(height, width, 3)
+
+
+# ---------------------------------------------------------------------------
 # Marching-cubes tables (mc_tables.py:24-105): generated, not the classic table
 
 MC_CORNERS = np.array(

@@ -66,5 +66,6 @@ from .spatial import (
 )
 
 from .meshing import extract_mesh, extract_mesh_arrays, extract_mesh_dense
+from .render import Image, read_ppm, render_image, write_image
 
 __version__ = "0.1.0"

@@ -222,6 +222,24 @@ def gen_frustum(nets, out):
         out[f"frustum/{tag}/steps"] = res.steps
 
 
+def gen_render(nets, out):
+    """render_image (render.py:91-141) in its three modes."""
+    from spelunk.render import render_image
+
+    box_cam = sp.Camera(resolution=(48, 48), **FRONT_CAM)
+    sdf_cam = sp.Camera(np.array([1.6, 1.2, 2.0]), np.zeros(3), np.array([0.0, 1.0, 0.0]), 40.0, (40, 24))
+    cases = [
+        ("box_per_ray", "box", box_cam, sp.RayCastParams(t_max=4.0), "per_ray", None),
+        ("box_frustum", "box", box_cam, sp.RayCastParams(t_max=4.0), "frustum", None),
+        ("box_fixed", "box", box_cam, sp.RayCastParams(t_max=4.0), "fixed_step", 0.01),
+        ("relu_sdf_per_ray", "relu_sdf", sdf_cam, sp.RayCastParams(), "per_ray", None),
+        ("elu_sdf_fixed", "elu_sdf", sdf_cam, sp.RayCastParams(t_max=5.0), "fixed_step", 0.02),
+    ]
+    for tag, netname, cam, params, mode, step in cases:
+        img = render_image(nets[netname], cam, params, sp.AFFINE_FIXED, mode, step)
+        out[f"render/{tag}/pixels"] = img.pixels
+
+
 def gen_mesh(nets, out):
     bounds = sp.AABB(np.full(3, -1.0), np.full(3, 1.0))
     for tag, netname, m, pol in (
@@ -253,6 +271,7 @@ def main():
     gen_rays(nets, out)
     gen_mesh(nets, out)
     gen_frustum(nets, out)
+    gen_render(nets, out)
     np.savez_compressed(HERE / "golden.npz", **out)
     meta = {"reference": REF_SRC, "numpy": np.__version__, "n_arrays": len(out)}
     (HERE / "golden_meta.json").write_text(json.dumps(meta, indent=1))

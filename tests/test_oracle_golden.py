@@ -155,3 +155,33 @@ def test_frustum_cast_matches_reference(golden, net_paths, tag):
     np.testing.assert_array_equal(hit, golden[f"frustum/{tag}/hit"])
     np.testing.assert_array_equal(t, golden[f"frustum/{tag}/t"])
     np.testing.assert_array_equal(steps, golden[f"frustum/{tag}/steps"])
+
+
+SDF_CAM = ([1.6, 1.2, 2.0], [0.0, 0.0, 0.0], [0.0, 1.0, 0.0], 40.0, 40, 24)
+BOX_CAM = ([0.13, 0.11, 2.4], [0.02, -0.03, 0.0], [0.0, 1.0, 0.0], 40.0, 48, 48)
+RENDERS = {
+    "box_per_ray": ("box", BOX_CAM, orc.MarchParams(t_max=4.0), "per_ray", None),
+    "box_frustum": ("box", BOX_CAM, orc.MarchParams(t_max=4.0), "frustum", None),
+    "box_fixed": ("box", BOX_CAM, orc.MarchParams(t_max=4.0), "fixed_step", 0.01),
+    "relu_sdf_per_ray": ("relu_sdf", SDF_CAM, orc.MarchParams(), "per_ray", None),
+    "elu_sdf_fixed": ("elu_sdf", SDF_CAM, orc.MarchParams(t_max=5.0), "fixed_step", 0.02),
+}
+
+
+@pytest.mark.parametrize("tag", sorted(RENDERS))
+def test_render_matches_reference(golden, net_paths, tag):
+    netname, cam, params, mode, step = RENDERS[tag]
+    img = orc.render(orc.load_net(net_paths[netname]), *cam, params, "affine-fixed", mode, step)
+    np.testing.assert_array_equal(img, golden[f"render/{tag}/pixels"])
+
+
+def test_ppm_bytes_and_round_trip(tmp_path):
+    """write_image P6 layout (render.py:158-162) and read_ppm round trip."""
+    from paper_2202_02444_b200.render import Image, read_ppm, write_image
+
+    px = np.arange(2 * 3 * 3, dtype=np.uint8).reshape(2, 3, 3)
+    write_image(Image(3, 2, px), tmp_path / "a.ppm")
+    assert (tmp_path / "a.ppm").read_bytes() == b"P6\n3 2\n255\n" + px.tobytes()
+    np.testing.assert_array_equal(read_ppm(tmp_path / "a.ppm").pixels, px)
+    write_image(Image(3, 2, px), tmp_path / "a.png")
+    assert (tmp_path / "a.png").read_bytes()[:8] == b"\x89PNG\r\n\x1a\n"
