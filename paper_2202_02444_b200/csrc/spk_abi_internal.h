@@ -49,6 +49,9 @@ int launch_symbolic(const struct ::spk_net* net, int policy, int n_keep, int pre
                     cudaStream_t st);
 int launch_symbolic_in(const struct ::spk_net* net, int policy, int n_keep, int precision, const BoxInput& in,
                        const BoundOutput& o, long long n_cap, int s, cudaStream_t st);
+// affine-full beyond the register-tiled capacity (spk_full.cu); need = s + hidden widths
+int launch_full(const struct ::spk_net* net, int precision, const BoxInput& in, const BoundOutput& out,
+                long long n, int s0, int need, cudaStream_t st);
 int bound_aabb_internal(const struct ::spk_net* net, int policy, int n_keep, int precision, long long n_cap,
                         const long long* n_dev, const double* box_lo, const double* box_hi, double* lo, double* hi,
                         int8_t* cls, cudaStream_t st);

@@ -35,6 +35,10 @@ static int plan_capacity(const spk_net* net, int policy, int n_keep, int s, int*
         if (a != SPK_OP_IDENTITY) need += net->layers[l].m_out;
   }
   const int kcmax = net->mmax <= 64 ? 32 : 16;
+  if (policy == SPK_POLICY_AFFINE_FULL && need > kcmax) {
+    *kc = -need;  // beyond the register-tiled kernel: the large-capacity path (spk_full.cu)
+    return SPK_OK;
+  }
   if (need > kcmax)
     return fail(SPK_ERR_UNSUPPORTED_SHAPE,
                 "symbol capacity " + std::to_string(need) + " exceeds the compiled maximum " + std::to_string(kcmax));
@@ -51,6 +55,7 @@ static int run_sym(const spk_net* cnet, int policy, int n_keep, int precision, c
   int kc;
   SymParams P;
   if (int rc = plan_capacity(net, policy, n_keep, s, &kc, &P)) return rc;
+  if (kc < 0) return launch_full(net, precision, in, out, n, s, -kc, st);
   DeviceGuard g(net->device);
   const int sm = sm_count_for(net->device);
   if (sm <= 0) return fail(SPK_ERR_CUDA, "no CUDA device");

@@ -6,9 +6,10 @@ discrete decision: a last-ulp norm tie resolved differently would show up as
 a larger difference, and none does).  FP32 kernels: sound; |d| <= 2e-2 (S + w):
 the kept set is a discrete choice and an FP32 near-tie in the column norms
 can keep a different symbol than FP64 does (measured max 4.7e-3, elu_sdf,
-truncate:8); both enclosures are sound (test_symbolic_soundness).  affine-full is compiled for symbol capacity <= 32
-(s + sum of hidden widths), so only the small golden nets take it; the wider
-ones must raise DeviceError (never silently fall back).
+truncate:8); both enclosures are sound (test_symbolic_soundness).  affine-full
+runs the register-tiled kernel up to 32 symbols (s + sum of hidden widths)
+and the large-capacity kernel (spk_full.cu) beyond -- every golden net,
+227 symbols on the 7x32 fixtures.
 """
 
 import numpy as np
@@ -31,8 +32,7 @@ def cases(nets):
     for name in nets:
         for pol in ("affine-truncate:8", "affine-truncate:16"):
             yield name, pol
-        if name in SMALL:
-            yield name, "affine-full"
+        yield name, "affine-full"
 
 
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
@@ -57,11 +57,27 @@ def test_symbolic_matches_reference(golden, nets, precision):
         print(f"SYM fp64 worst {k}: {worst[k]:.2e}")
 
 
-def test_affine_full_capacity_error(nets, golden):
-    net = nets["relu_sdf"]  # 3 + 7*32 symbols > 32
-    c, a = golden["bounds/relu_sdf/centers"], golden["bounds/relu_sdf/axes"]
-    with pytest.raises(sp.errors.DeviceError):
-        sp.range_bound_batch(net, c, a, "affine-full")
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_affine_full_large_capacity_sound(nets, precision):
+    """Large-capacity affine-full (relu_sdf: 227 symbols, sin3x48: 147): dense
+    samples inside; on the ReLU nets at least as tight as affine-fixed."""
+    rng = np.random.default_rng(31)
+    for name in ("relu_sdf", "elu_sdf", "sin3x48", "relu4x32"):
+        net = nets[name]
+        n = 128
+        c = rng.uniform(-1.1, 1.1, (n, 3))
+        a = np.zeros((n, 3, 3))
+        a[:, np.arange(3), np.arange(3)] = (10.0 ** rng.uniform(-4, -0.5, n) / 2.0)[:, None]
+        lo, hi = sp.range_bound_batch(net, c, a, "affine-full", precision=precision)
+        eps = rng.uniform(-1, 1, (n, 32, 3))
+        pts = c[:, None, :] + np.einsum("nks,nsd->nkd", eps, a)
+        vals = orc.eval_points(orc.as_oracle_net(net), pts.reshape(-1, 3)).reshape(n, -1)
+        slack = 1e-12 * scale(lo, hi)
+        assert np.all(vals >= (lo - slack)[:, None]) and np.all(vals <= (hi + slack)[:, None]), name
+        if name.startswith("relu"):  # Chebyshev sin/ELU slopes need not shrink monotonically
+            fl, fh = sp.range_bound_batch(net, c, a, "affine-fixed", precision=precision)
+            tol = (1e-9 if precision == "fp64" else 1e-3) * scale(lo, hi)
+            assert np.all(lo >= fl - tol) and np.all(hi <= fh + tol), name
 
 
 @pytest.mark.parametrize("policy", ["affine-truncate:4", "affine-truncate:16"])
