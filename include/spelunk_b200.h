@@ -18,6 +18,7 @@
  *   spk_tree_build                    <- build_spatial_tree (spatial.py:214-289)
  *   spk_march                         <- _march_arrays (rays.py:88-138)
  *   spk_frustum_cast                  <- cast_frustum_image (rays.py:232-341)
+ *   spk_certified_radii / spk_intersect / spk_bisect <- volumetric queries (spatial.py:292-684)
  *   spk_render_shade                  <- _refine_hits / _normals / shading (render.py:59-141)
  *   spk_fixed_step_march              <- _fixed_step_march (render.py:36-56)
  *   spk_mesh_blocks / spk_mesh_cells  <- extract_mesh (meshing.py:111-169)
@@ -148,6 +149,13 @@ int spk_bound_batch_host(const spk_net* net, int policy, int n_keep, int precisi
 int spk_tree_build(const spk_net* net, int policy, int n_keep, int precision, int64_t n_roots,
                    const double* root_lo, const double* root_hi, int start_depth, int max_depth,
                    double delta, void* stream, spk_tree** out);
+/* The same build with the refinement rule of sample_near_surface
+ * (spatial.py:403-411): with band > 0 a node splits when its bound meets
+ * [-band, band] (lo <= band and hi >= -band) instead of when it is UNKNOWN;
+ * band = 0 is spk_tree_build. */
+int spk_tree_build_band(const spk_net* net, int policy, int n_keep, int precision, int64_t n_roots,
+                        const double* root_lo, const double* root_hi, int start_depth, int max_depth,
+                        double delta, double band, void* stream, spk_tree** out);
 int spk_tree_destroy(spk_tree* tree);
 int spk_tree_info(const spk_tree* tree, int* n_levels, int64_t* n_nodes, int64_t* bound_evals);
 /* copy one level into caller buffers (host or device, any may be NULL) */
@@ -221,6 +229,30 @@ int spk_render_shade(const spk_net* net, int precision, int64_t n, const double*
 int spk_fixed_step_march(const spk_net* net, int precision, int64_t n, const double* origins, int64_t origin_stride,
                          const double* dirs, double step, double t_max, uint8_t* hit, double* t, int64_t* stats,
                          void* stream);
+
+/* §8(f3): volumetric queries (spatial.py:292-684).
+ * spk_certified_radii: for n points (device, n x d, d <= 3) the largest
+ * r = r_start[i] / 2^j >= floor whose cube (centre p, axes diag(r)) has a
+ * sign-definite bound, else 0 (_certified_radii, spatial.py:318-343);
+ * radii on the device; stats (host, 2, optional): rounds, bounds. */
+int spk_certified_radii(const spk_net* net, int policy, int n_keep, int precision, int64_t n,
+                        const double* points, const double* r_start, double floor_r, double* radii,
+                        int64_t* stats, void* stream);
+/* test_intersection (spatial.py:544-588) over the host box lo..hi: kind
+ * 0 disjoint, 1 intersecting (witness_lo/hi = the first interior node in
+ * frontier order), 2 inconclusive (n_nodes delta-scale nodes, the first
+ * min(n_nodes, nodes_cap) copied to nodes_lo/hi, host, in the reference's
+ * order).  stats (host, 2, optional): levels, bounds. */
+int spk_intersect(const spk_net* net_a, const spk_net* net_b, int policy, int n_keep, int precision,
+                  const double* lo, const double* hi, double delta, int* kind, double* witness_lo,
+                  double* witness_hi, int64_t* n_nodes, double* nodes_lo, double* nodes_hi, int64_t nodes_cap,
+                  int64_t* stats, void* stream);
+/* Batched bisection between n point pairs (device, n x d): a on the f < 0
+ * side, b on the other; iters halvings (mid = (a + b) / 2, f(mid) < 0 -> a
+ * else b), out = the final midpoints (closest_point's surface witness,
+ * spatial.py:631-638).  a and b are updated in place. */
+int spk_bisect(const spk_net* net, int precision, int64_t n, double* a, double* b, int iters, double* out,
+               void* stream);
 
 /* K7: hierarchical marching cubes (extract_mesh, meshing.py:111-169) at
  * resolution 2^m over the host box lo3..hi3; prune = 1 runs the index-range

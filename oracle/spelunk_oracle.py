@@ -499,6 +499,213 @@ def node_keys(levels):
 
 
 # ---------------------------------------------------------------------------
+# Volumetric queries (spatial.py:292-684)
+
+
+def certified_radii(net, points, r_start, floor, policy="affine-full"):
+    """_certified_radii (spatial.py:318-343): per point, halve the cube
+    half-extent from r_start until the bound is sign-definite (radius) or
+    it drops below floor (0)."""
+    net = as_oracle_net(net)
+    pts = np.asarray(points, dtype=np.float64)
+    n, d = pts.shape
+    r = np.array(np.broadcast_to(np.asarray(r_start, dtype=np.float64), (n,)))
+    radius = np.zeros(n)
+    todo = np.flatnonzero(r >= floor)
+    while todo.size:
+        axes = np.zeros((todo.size, d, d))
+        axes[:, np.arange(d), np.arange(d)] = r[todo][:, None]
+        blo, bhi = bound_batch(net, pts[todo], axes, policy)
+        ok = (blo > 0.0) | (bhi < 0.0)
+        radius[todo[ok]] = r[todo[ok]]
+        rest = todo[~ok]
+        r[rest] /= 2.0
+        todo = rest[r[rest] >= floor]
+    return radius
+
+
+def walk_on_spheres_stats(net, p, boundary_fn, n_walks, rng_seed=0, delta=0.001, policy="affine-full",
+                          r_cap=1.0, max_rounds=10_000):
+    """spatial.py:346-399: each live walk jumps to a uniform point on the
+    sphere inscribed in its certified empty cube; it stops (and reads the
+    boundary data) when no clearance >= 2 delta certifies."""
+    net = as_oracle_net(net)
+    x0 = np.asarray(p, dtype=np.float64)
+    rng = np.random.default_rng(rng_seed)
+    pos = np.tile(x0, (n_walks, 1))
+    guess = np.full(n_walks, float(r_cap))
+    vals = np.empty(n_walks)
+    live = np.arange(n_walks)
+    for _ in range(max_rounds):
+        if not live.size:
+            break
+        rad = certified_radii(net, pos[live], guess[live], 2.0 * delta, policy)
+        stop = rad == 0.0
+        for w in live[stop]:
+            vals[w] = float(boundary_fn(pos[w]))
+        live, rad = live[~stop], rad[~stop]
+        if not live.size:
+            break
+        u = rng.standard_normal((live.size, x0.shape[0]))
+        u /= np.linalg.norm(u, axis=1, keepdims=True)
+        pos[live] += rad[:, None] * u
+        guess[live] = np.minimum(rad * 4.0, r_cap)
+    se = float(vals.std(ddof=1) / np.sqrt(n_walks)) if n_walks > 1 else 0.0
+    return float(vals.mean()), se
+
+
+def sample_near_surface(net, lo, hi, n_samples, band, depth, policy="affine-full", rng_seed=0, max_evals=None):
+    """spatial.py:402-451: band tree (split while the bound meets
+    [-band, band]) to `depth`, then volume-weighted rejection sampling."""
+    net = as_oracle_net(net)
+    los = np.atleast_2d(np.asarray(lo, dtype=np.float64))
+    his = np.atleast_2d(np.asarray(hi, dtype=np.float64))
+    for level in range(depth + 1):
+        blo, bhi = bound_aabbs(net, los, his, policy)
+        keep = (blo <= band) & (bhi >= -band)
+        if not keep.any():
+            raise ValueError("EmptyBand")
+        if level == depth:
+            los, his = los[keep], his[keep]
+            break
+        los, his = split_widest(los[keep], his[keep])
+    rng = np.random.default_rng(rng_seed)
+    vol = np.prod(his - los, axis=1)
+    w = vol / vol.sum()
+    budget = max_evals if max_evals is not None else max(200 * n_samples, 100_000)
+    chunk = max(1024, n_samples)
+    got, total, spent = [], 0, 0
+    while total < n_samples:
+        if spent >= budget:
+            raise ValueError("EmptyBand")
+        k = int(min(chunk, budget - spent))
+        pick = rng.choice(len(w), size=k, p=w)
+        cand = rng.uniform(los[pick], his[pick])
+        spent += k
+        ok = np.abs(eval_points(net, cand)) < band
+        got.append(cand[ok])
+        total += int(ok.sum())
+    return np.concatenate(got)[:n_samples]
+
+
+def bulk_properties(net, lo, hi, depth, samples_per_unknown_node=64, rng_seed=0, policy="affine-full"):
+    """spatial.py:454-541 -> (mass, mass_error_bound, centroid, inertia)."""
+    net = as_oracle_net(net)
+    levels = tree_levels(net, lo, hi, policy, max_depth=depth)
+    neg = [(lv["lo"][lv["label"] == -1], lv["hi"][lv["label"] == -1]) for lv in levels]
+    ilo = np.concatenate([a for a, _ in neg])
+    ihi = np.concatenate([b for _, b in neg])
+    if len(levels) == depth + 1:
+        u = levels[depth]["label"] == 0
+        ulo, uhi = levels[depth]["lo"][u], levels[depth]["hi"][u]
+    else:
+        ulo = uhi = np.zeros((0, 3))
+    mass, m1, m2 = 0.0, np.zeros(3), np.zeros((3, 3))
+    if len(ilo):
+        ext = ihi - ilo
+        vol = np.prod(ext, axis=1)
+        c = (ilo + ihi) / 2.0
+        mass += float(vol.sum())
+        m1 += vol @ c
+        m2 += np.einsum("n,ni,nj->ij", vol, c, c)
+        m2 += np.diag(np.einsum("n,ni->i", vol, (ext / 2.0) ** 2) / 3.0)
+    err = float(np.prod(uhi - ulo, axis=1).sum()) if len(ulo) else 0.0
+    if len(ulo):
+        k = max(1, round(samples_per_unknown_node ** (1.0 / 3.0)))
+        rng = np.random.default_rng(rng_seed)
+        sub = np.stack(np.meshgrid(*[np.arange(k)] * 3, indexing="ij"), axis=-1).reshape(-1, 3)
+        ext = uhi - ulo
+        vol = np.prod(ext, axis=1)
+        pts = ulo[:, None, :] + (sub[None] + rng.random((len(ulo), k ** 3, 3))) * (ext / k)[:, None, :]
+        ins = (eval_points(net, pts.reshape(-1, 3)) < 0.0).reshape(len(ulo), k ** 3)
+        w = vol / (k ** 3)
+        mass += float((w * ins.sum(axis=1)).sum())
+        m1 += np.einsum("n,nsi->i", w, pts * ins[:, :, None])
+        m2 += np.einsum("n,nsi,nsj->ij", w, pts * ins[:, :, None], pts)
+    centroid = m1 / mass if mass > 0.0 else (np.asarray(lo, float) + np.asarray(hi, float)) / 2.0
+    sc = m2 - mass * np.outer(centroid, centroid)
+    inertia = np.trace(sc) * np.eye(3) - sc
+    return mass, err, centroid, (inertia + inertia.T) / 2.0
+
+
+def test_intersection(net_a, net_b, lo, hi, delta=0.001, policy="affine-full"):
+    """spatial.py:544-588 -> ("intersecting", witness (lo, hi)) |
+    ("disjoint", None) | ("inconclusive", [(lo, hi), ...])."""
+    net_a, net_b = as_oracle_net(net_a), as_oracle_net(net_b)
+    los = np.atleast_2d(np.asarray(lo, dtype=np.float64))
+    his = np.atleast_2d(np.asarray(hi, dtype=np.float64))
+    stop = delta / np.sqrt(los.shape[1])
+    small = []
+    while len(los):
+        la, ha = bound_aabbs(net_a, los, his, policy)
+        lb, hb = bound_aabbs(net_b, los, his, policy)
+        live = (la <= 0.0) & (lb <= 0.0)
+        inside = live & (ha < 0.0) & (hb < 0.0)
+        if inside.any():
+            i = int(np.flatnonzero(inside)[0])
+            return "intersecting", (los[i], his[i])
+        tiny = live & (np.max(his - los, axis=1) < stop)
+        small += [(los[i], his[i]) for i in np.flatnonzero(tiny)]
+        go = live & ~tiny
+        los, his = split_widest(los[go], his[go])
+    return ("inconclusive", small) if small else ("disjoint", None)
+
+
+test_intersection.__test__ = False
+
+
+def closest_point(net, q, lo, hi, delta=0.001, policy="affine-fixed"):
+    """spatial.py:591-684: best-first descent ordered by the distance of q
+    to each node; spanning nodes (face centres of both signs) report their
+    centre and farthest-corner distance; a bisected surface point prunes."""
+    import heapq
+
+    net = as_oracle_net(net)
+    q = np.asarray(q, dtype=np.float64)
+    lo = np.asarray(lo, dtype=np.float64)
+    hi = np.asarray(hi, dtype=np.float64)
+    stop = delta / np.sqrt(lo.shape[0])
+    near = lambda a, b: float(np.linalg.norm(np.maximum(np.maximum(a - q, q - b), 0.0)))  # noqa: E731
+    far = lambda a, b: float(np.linalg.norm(np.maximum(np.abs(q - a), np.abs(q - b))))  # noqa: E731
+    best, prune, best_pt, tie = np.inf, np.inf, None, 0
+    heap = [(near(lo, hi), 0, lo, hi)]
+    while heap:
+        md, _, a, b = heapq.heappop(heap)
+        if md >= min(best, prune):
+            continue
+        blo, bhi = bound_aabbs(net, a[None, :], b[None, :], policy)
+        if blo[0] > 0.0 or bhi[0] < 0.0:
+            continue
+        faces = face_centres(a[None, :], b[None, :])[0]
+        v = eval_points(net, faces)
+        if np.any(v < 0.0) and not np.all(v < 0.0):
+            fd = far(a, b)
+            if fd < best:
+                best, best_pt = fd, (a + b) / 2.0
+            pn, pp = faces[np.argmin(v)], faces[np.argmax(v)]
+            for _ in range(30):
+                mid = 0.5 * (pn + pp)
+                if eval_points(net, mid[None, :])[0] < 0.0:
+                    pn = mid
+                else:
+                    pp = mid
+            prune = min(prune, float(np.linalg.norm(0.5 * (pn + pp) - q)) + 1e-6)
+        elif np.any(v == 0.0):
+            prune = min(prune, float(np.linalg.norm(faces[np.argmin(np.abs(v))] - q)) + 1e-6)
+        if np.max(b - a) < stop:
+            continue
+        kids = split_widest(a[None, :], b[None, :])
+        for c_lo, c_hi in zip(*kids):
+            cmd = near(c_lo, c_hi)
+            if cmd < min(best, prune):
+                tie += 1
+                heapq.heappush(heap, (cmd, tie, c_lo, c_hi))
+    if best_pt is None:
+        raise ValueError("NoSurfaceFound")
+    return best_pt, best
+
+
+# ---------------------------------------------------------------------------
 # Range-marching ray caster (rays.py:88-138) and pinhole camera (camera.py)
 
 

@@ -67,5 +67,20 @@ from .spatial import (
 
 from .meshing import extract_mesh, extract_mesh_arrays, extract_mesh_dense
 from .render import Image, read_ppm, render_image, write_image
+from .queries import (
+    BulkProperties,
+    EmptyRegion,
+    IntersectionResult,
+    bulk_properties,
+    certified_radii,
+    closest_point,
+    empty_box_radius,
+    sample_near_surface,
+    save_obj,
+    save_xyz,
+    test_intersection,
+    walk_on_spheres,
+    walk_on_spheres_stats,
+)
 
 __version__ = "0.1.0"

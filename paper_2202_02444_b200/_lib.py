@@ -58,12 +58,16 @@ SIGNATURES = {
     "spk_eval_batch": ([vp, i32, i64, vp, vp, vp], i32),
     "spk_bound_batch_host": ([vp, i32, i32, i32, i64, i32, vp, vp, vp, vp, vp], i32),
     "spk_tree_build": ([vp, i32, i32, i32, i64, vp, vp, i32, i32, f64, vp, vp], i32),
+    "spk_tree_build_band": ([vp, i32, i32, i32, i64, vp, vp, i32, i32, f64, f64, vp, vp], i32),
     "spk_tree_stats": ([vp, vp, vp], i32),
     "spk_tree_level_copy": ([vp, i32, vp, vp, vp, vp, vp, vp, vp], i32),
     "spk_march": ([vp, i32, i32, i32, i64, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp], i32),
     "spk_camera_dirs": ([vp, f64, f64, i32, i32, vp, vp], i32),
     "spk_render_shade": ([vp, i32, i64, vp, i64, vp, vp, vp, f64, i32, vp, vp, vp, vp, vp], i32),
     "spk_fixed_step_march": ([vp, i32, i64, vp, i64, vp, f64, f64, vp, vp, vp, vp], i32),
+    "spk_certified_radii": ([vp, i32, i32, i32, i64, vp, vp, f64, vp, vp, vp], i32),
+    "spk_intersect": ([vp, vp, i32, i32, i32, vp, vp, f64, vp, vp, vp, vp, vp, vp, i64, vp, vp], i32),
+    "spk_bisect": ([vp, i32, i64, vp, vp, i32, vp, vp], i32),
     "spk_frustum_cast": ([vp, i32, i32, i32, vp, vp, f64, f64, i32, i32, i32, vp, vp, vp, vp, vp, vp], i32),
     "spk_mesh_extract": ([vp, i32, i32, i32, vp, vp, i32, i32, i32, vp, vp, vp, vp], i32),
     "spk_mesh_info": ([vp, vp, vp, vp, vp, vp], i32),

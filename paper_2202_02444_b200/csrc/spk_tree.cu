@@ -36,14 +36,18 @@ struct TreeLevel {
 };
 
 // per-node decision: flag 1 = split, 2 = tiny UNKNOWN leaf (convergence mode)
+// band > 0 replaces "UNKNOWN" by "bound meets [-band, band]"
+// (sample_near_surface's refinement rule, spatial.py:403-411)
 __global__ void tree_mark_kernel(const long long* __restrict__ n_dev, int d, const double* __restrict__ lo,
-                                 const double* __restrict__ hi, const int8_t* __restrict__ label, int depth,
-                                 int max_depth, double stop_extent, uint8_t* __restrict__ flag,
+                                 const double* __restrict__ hi, const int8_t* __restrict__ label,
+                                 const double* __restrict__ blo, const double* __restrict__ bhi, double band,
+                                 int depth, int max_depth, double stop_extent, uint8_t* __restrict__ flag,
                                  int* __restrict__ block_split, int* __restrict__ block_small) {
   const long long n = *n_dev;
   const long long i = (long long)blockIdx.x * TB_THREADS + threadIdx.x;
   uint8_t f = 0;
-  if (i < n && label[i] == 0) {
+  const bool open = i < n && (band > 0.0 ? (blo[i] <= band && bhi[i] >= -band) : label[i] == 0);
+  if (open) {
     if (max_depth >= 0) {
       f = depth < max_depth ? 1 : 0;
     } else {
@@ -278,7 +282,15 @@ extern "C" {
 int spk_tree_build(const spk_net* net, int policy, int n_keep, int precision, int64_t n_roots,
                    const double* root_lo, const double* root_hi, int start_depth, int max_depth, double delta,
                    void* stream, spk_tree** out) {
+  return spk_tree_build_band(net, policy, n_keep, precision, n_roots, root_lo, root_hi, start_depth, max_depth,
+                             delta, 0.0, stream, out);
+}
+
+int spk_tree_build_band(const spk_net* net, int policy, int n_keep, int precision, int64_t n_roots,
+                        const double* root_lo, const double* root_hi, int start_depth, int max_depth,
+                        double delta, double band, void* stream, spk_tree** out) {
   if (!net || !out) return fail(SPK_ERR_INVALID_PARAMETER, "null argument");
+  if (!(band >= 0.0)) return fail(SPK_ERR_INVALID_PARAMETER, "band must be >= 0");
   *out = nullptr;
   const int d = net->input_dim;
   if (d > 3) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "tree build supports d <= 3");
@@ -366,8 +378,8 @@ int spk_tree_build(const spk_net* net, int policy, int n_keep, int precision, in
     }
     int* bsplit = counts;
     int* bsmall = counts + nb;
-    tree_mark_kernel<<<nb, TB_THREADS, 0, st>>>(n_dev, d, cur.lo, cur.hi, cur.label, depth, max_depth, stop, flag,
-                                                bsplit, bsmall);
+    tree_mark_kernel<<<nb, TB_THREADS, 0, st>>>(n_dev, d, cur.lo, cur.hi, cur.label, cur.blo, cur.bhi, band, depth,
+                                                max_depth, stop, flag, bsplit, bsmall);
     tree_sum_kernel<<<1, TB_THREADS, 0, st>>>(nb, bsplit, bsmall, k_dev, m_dev, d_cnt + lv + 1);
     // capacity of the next level
     const bool last_fixed = fixed && depth >= max_depth;

@@ -225,7 +225,8 @@ class _DeviceView:
                                          "version": 3, "strides": None, "stream": None}
 
 
-def _build(net, roots_lo, roots_hi, start_depth, delta, policy, max_depth, precision, to_host, device=None):
+def _build(net, roots_lo, roots_hi, start_depth, delta, policy, max_depth, precision, to_host, device=None,
+           band: float = 0.0):
     pcode, n_keep = policy_code(policy)
     dn = device_net(net, device)
     roots_lo = np.ascontiguousarray(roots_lo, dtype=np.float64)
@@ -233,9 +234,9 @@ def _build(net, roots_lo, roots_hi, start_depth, delta, policy, max_depth, preci
     handle = C.c_void_p()
     stream = dv.stream_ptr(dn.device)
     _lib.call(
-        "spk_tree_build", dn.ptr, pcode, n_keep, _precision_code(precision), roots_lo.shape[0],
+        "spk_tree_build_band", dn.ptr, pcode, n_keep, _precision_code(precision), roots_lo.shape[0],
         roots_lo.ctypes.data, roots_hi.ctypes.data, int(start_depth),
-        -1 if max_depth is None else int(max_depth), float(delta), stream, C.byref(handle),
+        -1 if max_depth is None else int(max_depth), float(delta), float(band), stream, C.byref(handle),
     )
     owner = _TreeHandle(handle)
     lib = _lib.load()
@@ -353,3 +354,22 @@ def build_spatial_tree_sharded(net, bounds: AABB, max_depth: int, policy, rank: 
     sub = _build(net, _np(last.lo)[part], _np(last.hi)[part], cut, 1.0, policy, max_depth, precision, to_host)
     sub.meta.update(cut=cut, roots=int(part.size), top_nodes=top.n_nodes, top_levels=top.levels)
     return sub
+
+
+# The volumetric queries live in queries.py; re-exported here because the
+# reference defines them in spatial.py (spatial.py:292-720).
+from .queries import (  # noqa: E402
+    BulkProperties,
+    EmptyRegion,
+    IntersectionResult,
+    bulk_properties,
+    certified_radii,
+    closest_point,
+    empty_box_radius,
+    sample_near_surface,
+    save_obj,
+    save_xyz,
+    test_intersection,
+    walk_on_spheres,
+    walk_on_spheres_stats,
+)

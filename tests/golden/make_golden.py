@@ -240,6 +240,56 @@ def gen_render(nets, out):
         out[f"render/{tag}/pixels"] = img.pixels
 
 
+def gen_queries(nets, out):
+    """Volumetric queries (spatial.py:292-684), reference default policies."""
+    from spelunk.spatial import (_certified_radii, bulk_properties, closest_point, empty_box_radius,
+                                 sample_near_surface, test_intersection, walk_on_spheres_stats)
+
+    box, sdf = nets["box"], nets["relu_sdf"]
+    cube = sp.AABB(np.full(3, -1.0), np.full(3, 1.0))
+    rng = np.random.default_rng(41)
+    # empty-box radii: single points and one batched call
+    pts = np.array([[0.9, 0.9, 0.9], [0.0, 0.0, 0.0], [0.4999, 0.0, 0.0], [0.3, -0.7, 0.2]])
+    rin = np.array([0.5, 0.25, 0.5, 1.0])
+    out["queries/ebr/box/points"] = pts
+    out["queries/ebr/box/r_init"] = rin
+    out["queries/ebr/box/radius"] = np.array([empty_box_radius(box, q, r).radius for q, r in zip(pts, rin)])
+    sp_pts = rng.uniform(-1.0, 1.0, (48, 3))
+    out["queries/radii/relu_sdf/points"] = sp_pts
+    out["queries/radii/relu_sdf/radii"] = _certified_radii(sdf, sp_pts, np.full(48, 1.0), 0.002, sp.AFFINE_FULL)
+    # walk on spheres (harmonic data x0)
+    m, se = walk_on_spheres_stats(box, [0.2, 0.0, 0.0], lambda q: q[0], 300, rng_seed=0)
+    out["queries/wos/box"] = np.array([m, se])
+    # band sampling
+    out["queries/sample/box"] = sample_near_surface(box, cube, 500, 0.01, 12, rng_seed=1)
+    out["queries/sample/relu_sdf"] = sample_near_surface(sdf, cube, 300, 0.05, 7, rng_seed=2)
+    # mass properties
+    for tag, net, depth in (("box", box, 9), ("relu_sdf", sdf, 6)):
+        bp = bulk_properties(net, cube, depth, rng_seed=0)
+        out[f"queries/bulk/{tag}"] = np.concatenate([[bp.mass, bp.mass_error_bound], bp.centroid,
+                                                     bp.inertia.reshape(-1)])
+    # intersection: overlapping / disjoint / touching
+    big = sp.AABB(np.full(3, -2.0), np.full(3, 2.0))
+    for tag, off, delta in (("overlap", 0.4, 0.01), ("disjoint", 2.0, 0.01), ("touch", 1.0, 0.05)):
+        other = sp.build_box_oracle(np.array([off, 0.0, 0.0]), 0.5)
+        bounds = sp.AABB(np.full(3, -2.0), np.full(3, 3.0)) if tag == "disjoint" else big
+        res = test_intersection(box, other, bounds, delta=delta)
+        out[f"queries/isect/{tag}/kind"] = np.array(["disjoint", "intersecting", "inconclusive"].index(res.kind))
+        if res.witness is not None:
+            out[f"queries/isect/{tag}/witness"] = np.concatenate([res.witness.lo, res.witness.hi])
+        out[f"queries/isect/{tag}/nodes"] = (np.array([np.concatenate([n.lo, n.hi]) for n in res.nodes])
+                                             if res.nodes else np.zeros((0, 6)))
+    # closest point
+    qs = rng.uniform(-1.2, 1.2, (4, 3))
+    out["queries/closest/box/q"] = qs
+    out["queries/closest/box/result"] = np.array([np.concatenate(
+        [p, [dd]]) for p, dd in (closest_point(box, q, cube, delta=0.01) for q in qs)])
+    qs2 = rng.uniform(-0.9, 0.9, (2, 3))
+    out["queries/closest/relu_sdf/q"] = qs2
+    out["queries/closest/relu_sdf/result"] = np.array([np.concatenate(
+        [p, [dd]]) for p, dd in (closest_point(sdf, q, cube, delta=0.01) for q in qs2)])
+
+
 def gen_mesh(nets, out):
     bounds = sp.AABB(np.full(3, -1.0), np.full(3, 1.0))
     for tag, netname, m, pol in (
@@ -272,6 +322,7 @@ def main():
     gen_mesh(nets, out)
     gen_frustum(nets, out)
     gen_render(nets, out)
+    gen_queries(nets, out)
     np.savez_compressed(HERE / "golden.npz", **out)
     meta = {"reference": REF_SRC, "numpy": np.__version__, "n_arrays": len(out)}
     (HERE / "golden_meta.json").write_text(json.dumps(meta, indent=1))

@@ -185,3 +185,54 @@ def test_ppm_bytes_and_round_trip(tmp_path):
     np.testing.assert_array_equal(read_ppm(tmp_path / "a.ppm").pixels, px)
     write_image(Image(3, 2, px), tmp_path / "a.png")
     assert (tmp_path / "a.png").read_bytes()[:8] == b"\x89PNG\r\n\x1a\n"
+
+
+# ---- volumetric queries (make_golden.py:gen_queries) ----
+
+def test_queries_radii_match_reference(golden, net_paths):
+    box, sdf = orc.load_net(net_paths["box"]), orc.load_net(net_paths["relu_sdf"])
+    pts, rin = golden["queries/ebr/box/points"], golden["queries/ebr/box/r_init"]
+    got = [orc.certified_radii(box, p[None, :], [r], 0.001)[0] for p, r in zip(pts, rin)]
+    np.testing.assert_array_equal(got, golden["queries/ebr/box/radius"])
+    got = orc.certified_radii(sdf, golden["queries/radii/relu_sdf/points"], 1.0, 0.002)
+    np.testing.assert_array_equal(got, golden["queries/radii/relu_sdf/radii"])
+
+
+def test_queries_walk_and_sample_match_reference(golden, net_paths):
+    box, sdf = orc.load_net(net_paths["box"]), orc.load_net(net_paths["relu_sdf"])
+    m, se = orc.walk_on_spheres_stats(box, [0.2, 0.0, 0.0], lambda q: q[0], 300, rng_seed=0)
+    np.testing.assert_array_equal([m, se], golden["queries/wos/box"])
+    lo, hi = -np.ones(3), np.ones(3)
+    np.testing.assert_array_equal(orc.sample_near_surface(box, lo, hi, 500, 0.01, 12, rng_seed=1),
+                                  golden["queries/sample/box"])
+    np.testing.assert_array_equal(orc.sample_near_surface(sdf, lo, hi, 300, 0.05, 7, rng_seed=2),
+                                  golden["queries/sample/relu_sdf"])
+
+
+def test_queries_bulk_intersection_closest_match_reference(golden, net_paths):
+    box, sdf = orc.load_net(net_paths["box"]), orc.load_net(net_paths["relu_sdf"])
+    lo, hi = -np.ones(3), np.ones(3)
+    for tag, net, depth in (("box", box, 9), ("relu_sdf", sdf, 6)):
+        mass, err, c, inertia = orc.bulk_properties(net, lo, hi, depth, rng_seed=0)
+        np.testing.assert_array_equal(np.concatenate([[mass, err], c, inertia.reshape(-1)]),
+                                      golden[f"queries/bulk/{tag}"])
+    for tag, off, delta in (("overlap", 0.4, 0.01), ("disjoint", 2.0, 0.01), ("touch", 1.0, 0.05)):
+        other = orc.as_oracle_net(build_box(np.array([off, 0.0, 0.0]), 0.5))
+        top = 3.0 if tag == "disjoint" else 2.0
+        kind, info = orc.test_intersection(box, other, np.full(3, -2.0), np.full(3, top), delta)
+        assert ["disjoint", "intersecting", "inconclusive"].index(kind) == int(golden[f"queries/isect/{tag}/kind"])
+        if kind == "intersecting":
+            np.testing.assert_array_equal(np.concatenate(info), golden[f"queries/isect/{tag}/witness"])
+        if kind == "inconclusive":
+            np.testing.assert_array_equal(np.array([np.concatenate(n) for n in info]),
+                                          golden[f"queries/isect/{tag}/nodes"])
+    for tag, net in (("box", box), ("relu_sdf", sdf)):
+        for q, want in zip(golden[f"queries/closest/{tag}/q"], golden[f"queries/closest/{tag}/result"]):
+            p, dist = orc.closest_point(net, q, lo, hi, delta=0.01)
+            np.testing.assert_array_equal(np.concatenate([p, [dist]]), want)
+
+
+def build_box(center, half):
+    from paper_2202_02444_b200.network import build_box_oracle
+
+    return build_box_oracle(center, half)
