@@ -67,6 +67,7 @@ from .spatial import (
 
 from .meshing import extract_mesh, extract_mesh_arrays, extract_mesh_dense
 from .render import Image, read_ppm, render_image, write_image
+from .bench import BenchRow, FuzzReport, FuzzViolation, bench_variants, fuzz_soundness
 from .queries import (
     BulkProperties,
     EmptyRegion,

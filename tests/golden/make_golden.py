@@ -290,6 +290,17 @@ def gen_queries(nets, out):
         [p, [dd]]) for p, dd in (closest_point(sdf, q, cube, delta=0.01) for q in qs2)])
 
 
+def gen_variants(nets, out):
+    """bench_variants region sizes and a fuzz report (bench.py:128-319)."""
+    from spelunk.bench import bench_variants, fuzz_soundness
+
+    rows = bench_variants([nets["relu_sdf"], nets["elu_sdf"]], n_regions=2000, rng_seed=0, raycast_res=16, runs=1)
+    out["variants/region_size"] = np.array([r.region_size for r in rows])
+    out["variants/dim"] = np.array([r.dim for r in rows])
+    rep = fuzz_soundness([nets["relu_sdf"], nets["sin12"]], n_regions=20_000, rng_seed=3, threads=1)
+    out["variants/fuzz"] = np.array([rep.n_regions, rep.n_checks, rep.n_violations])
+
+
 def gen_mesh(nets, out):
     bounds = sp.AABB(np.full(3, -1.0), np.full(3, 1.0))
     for tag, netname, m, pol in (
@@ -323,6 +334,7 @@ def main():
     gen_frustum(nets, out)
     gen_render(nets, out)
     gen_queries(nets, out)
+    gen_variants(nets, out)
     np.savez_compressed(HERE / "golden.npz", **out)
     meta = {"reference": REF_SRC, "numpy": np.__version__, "n_arrays": len(out)}
     (HERE / "golden_meta.json").write_text(json.dumps(meta, indent=1))
