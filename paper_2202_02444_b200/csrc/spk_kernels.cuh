@@ -110,7 +110,7 @@ SPK_DEV void emit_bounds(const BoundOutput& out, long long gb, const State<T, C,
 }
 
 template <typename T, int C, int MMAX, int MODE>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, (Cfg<T, C, MMAX>::MINB))
     bound_kernel(const NetDev<T> net, const BoxInput in, const BoundOutput out, const long long n_cap) {
   using CF = Cfg<T, C, MMAX>;
   const long long n = in.n_dev ? *in.n_dev : n_cap;
@@ -161,7 +161,8 @@ cudaError_t launch_bound(const NetDev<T>& net, const BoxInput& in, const BoundOu
   if (attr_err != cudaSuccess) return attr_err;
   if (n <= 0) return cudaSuccess;
   const long long nbt = (n + CF::NB - 1) / CF::NB;
-  const int grid = (int)(nbt < sm_count ? nbt : sm_count);
+  const long long slots = (long long)sm_count * CF::MINB;
+  const int grid = (int)(nbt < slots ? nbt : slots);
   kfn<<<grid, NT, CF::SMEM, stream>>>(net, in, out, n);
   return cudaGetLastError();
 }

@@ -33,7 +33,7 @@ struct MarchState {
 };
 
 template <typename T, int C, int MMAX, int MODE>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, (Cfg<T, C, MMAX>::MINB))
     march_round_kernel(const NetDev<T> net, const MarchState M, const MarchParamsDev P, const long long n) {
   using CF = Cfg<T, C, MMAX>;
   constexpr int NB = CF::NB, CP = CF::CP;
@@ -131,7 +131,8 @@ cudaError_t launch_march_round(const NetDev<T>& net, const MarchState& M, const 
   if (attr_err != cudaSuccess) return attr_err;
   if (n <= 0) return cudaSuccess;
   const long long nbt = (n + CF::NB - 1) / CF::NB;
-  const int grid = (int)(nbt < sm_count ? nbt : sm_count);
+  const long long slots = (long long)sm_count * CF::MINB;
+  const int grid = (int)(nbt < slots ? nbt : slots);
   kfn<<<grid, NT, CF::SMEM, stream>>>(net, M, P, n);
   return cudaGetLastError();
 }

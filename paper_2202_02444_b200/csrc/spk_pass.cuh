@@ -29,6 +29,9 @@ constexpr int MAX_LAYERS = 24;
 constexpr int MAX_ACTS = 4;
 constexpr int NT = 256;         // threads per CTA (8 warps)
 constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reduction path
+#ifndef SPK_NARROW_2CTA
+#define SPK_NARROW_2CTA 1
+#endif
 #ifndef SPK_PACKED_F32
 #define SPK_PACKED_F32 1  // FP32 K loop on FFMA2 (sm_100a packed f32x2)
 #endif
@@ -77,8 +80,14 @@ struct Cfg {
   // register tile: TI neurons x TB boxes x C columns per thread
   static constexpr int TI = C <= 6 ? (sizeof(T) == 4 ? 8 : 4)
                                    : (C <= 20 ? VEC : (VEC / 2 > 0 ? VEC / 2 : 1));
-  static constexpr int TB = C == 1 ? (sizeof(T) == 4 ? 8 : 4) : (C == 2 ? 4 : (C <= 6 ? 2 : 1));
-  static constexpr int CP = C == 1 ? 1 : (C == 2 ? 2 : (C <= 4 ? 4 : (C <= 6 ? 6 : ((C + VEC - 1) / VEC) * VEC)));
+  // narrow nets (MMAX <= 64) with affine columns: one box per thread and two
+  // CTAs per SM -- their K loops are short, so latency hiding across CTAs
+  // matters more than register reuse across boxes
+  static constexpr int MINB = (SPK_NARROW_2CTA && MMAX <= 64 && C >= 3 && C <= 6) ? 2 : 1;
+  static constexpr int TB = C == 1 ? (sizeof(T) == 4 ? 8 : 4)
+                                   : (C == 2 ? 4 : (C <= 6 ? (MINB == 2 ? 1 : 2) : 1));
+  static constexpr int CP = C == 1 ? 1 : (C == 2 ? 2 : (C <= 4 ? 4 : (C <= 6 ? (TB == 1 ? 8 : 6)
+                                                                         : ((C + VEC - 1) / VEC) * VEC)));
   static constexpr int NG = MMAX / TI;
   static constexpr int NBG = NT / NG;
   static constexpr int NB = NBG * TB;
@@ -99,7 +108,7 @@ struct Cfg {
   // W ring depth: as many KT x MMAX tiles as fit beside X (small nets keep
   // every tile of the network resident and never re-stream W)
   static constexpr long long NS_FIT =
-      ((long long)SMEM_BUDGET - (long long)sizeof(T) * (XS + NBUF) - 1024) / ((long long)sizeof(T) * TILE);
+      ((long long)SMEM_BUDGET / MINB - (long long)sizeof(T) * (XS + NBUF) - 1024) / ((long long)sizeof(T) * TILE);
   static constexpr int NS = NS_FIT < NSTAGE_MIN ? NSTAGE_MIN : (NS_FIT > 16 ? 16 : (int)NS_FIT);
   static constexpr size_t SMEM = sizeof(T) * (size_t)(XS + NS * TILE + NBUF) + 2 * 16 * 8 + 64;
   static_assert(NG >= 1 && NG <= NT && NT % NG == 0, "tile shape");
