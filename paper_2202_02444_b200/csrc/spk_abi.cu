@@ -105,7 +105,9 @@ int build_device_net(spk_net* net, DevNet<T>& dn) {
     const bool narrow = (l + 1 == net->layers.size()) && L.m_out <= NARROW_MAX;
     int n_eff;
     if (narrow) {
-      n_eff = (L.m_in + 31) / 32 + 6;
+      // warp butterfly (32 lanes; K3F) or 4-lane groups (nets of width <= 64)
+      const int lp = mmax <= 64 ? 4 : 32;
+      n_eff = std::max((L.m_in + 31) / 32 + 6, (L.m_in + lp - 1) / lp + 3);
     } else {
       const int nt = (L.m_in + KT - 1) / KT;
       const int sub = sub_for<T>(mmax);

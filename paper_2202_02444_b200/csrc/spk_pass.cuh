@@ -723,42 +723,54 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
   (void)last;
 }
 
-// Narrow layer (m_out <= NARROW_MAX, e.g. the final width-1 layer): one
-// warp per (box, neuron) item, lanes stride over k, butterfly reduction.
-// Rounding budget gamma_{ceil(m_in/32) + 6}.
+// Narrow layer (m_out <= NARROW_MAX, e.g. the final width-1 layer): LP
+// lanes per (box, neuron) item stride over k, then a butterfly over the LP
+// lanes.  LP = 32 for wide nets; narrow nets (MMAX <= 64) use LP = 4 -- 8
+// items per warp, a 2-level butterfly -- since their k loops are short.
+// Rounding budget gamma_n, n = max(ceil(m_in/32) + 6, ceil(m_in/LP) + 3)
+// (spk_abi.cu: the same budget covers the 32-lane order of K3F).
+template <int MMAX>
+constexpr int narrow_lanes() { return MMAX <= 64 ? 4 : 32; }
+
 template <typename T, int C, int MMAX, int MODE, class Emit>
 SPK_DEV void narrow_layer(const LayerDev<T>& L, T* __restrict__ X, T* __restrict__ NBUF, int tid,
                           bool last, T gamma_next, Emit&& emit) {
   using CF = Cfg<T, C, MMAX>;
   constexpr int CP = CF::CP, NB = CF::NB, KT = CF::KT;
-  const int warp = tid >> 5, lane = tid & 31;
+  constexpr int LP = narrow_lanes<MMAX>(), IPW = 32 / LP;  // lanes per item, items per warp
+  const int warp = tid >> 5, lane = tid & 31, sub = lane / LP, l = lane % LP;
   const int items = NB * L.m_out;
-  for (int it = warp; it < items; it += NT / 32) {
-    const int b = it / L.m_out, i = it % L.m_out;
+  const bool one = L.m_out == 1;
+  for (int it0 = warp * IPW; it0 < items; it0 += (NT / 32) * IPW) {
+    const int it = it0 + sub;
+    const bool live = it < items;
+    const int b = one ? it : it / L.m_out, i = one ? 0 : it % L.m_out;
     const T* wrow = L.w + (size_t)i * L.m_in;
     T p[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) p[c] = T(0);
-    for (int k = lane; k < L.m_in; k += 32) {
-      const T wk = __ldg(wrow + k);
-      const T* xk = X + (size_t)k * CF::RS + b * CP;
-      if (C == 1) {
-        p[0] = Num<T>::fma_rn(wk, xk[0], p[0]);
-      } else {
+    if (live) {
+      for (int k = l; k < L.m_in; k += LP) {
+        const T wk = __ldg(wrow + k);
+        const T* xk = X + (size_t)k * CF::RS + b * CP;
+        if (C == 1) {
+          p[0] = Num<T>::fma_rn(wk, xk[0], p[0]);
+        } else {
 #pragma unroll
-        for (int c = 0; c < C - 1; ++c) p[c] = Num<T>::fma_rn(wk, xk[c], p[c]);
-        p[C - 1] = Num<T>::fma_ru(fabs(wk), xk[C - 1], p[C - 1]);
+          for (int c = 0; c < C - 1; ++c) p[c] = Num<T>::fma_rn(wk, xk[c], p[c]);
+          p[C - 1] = Num<T>::fma_ru(fabs(wk), xk[C - 1], p[C - 1]);
+        }
       }
     }
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
+    for (int off = LP / 2; off > 0; off >>= 1) {
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         const T o = __shfl_xor_sync(0xffffffffu, p[c], off);
         p[c] = (C > 1 && c == C - 1) ? Num<T>::add_ru(p[c], o) : p[c] + o;
       }
     }
-    if (lane == 0) {
+    if (live && l == 0) {
       T* dst = NBUF + ((size_t)b * NARROW_MAX + i) * CP;
 #pragma unroll
       for (int c = 0; c < C; ++c) dst[c] = p[c];
