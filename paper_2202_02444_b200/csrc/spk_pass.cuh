@@ -29,6 +29,9 @@ constexpr int MAX_LAYERS = 24;
 constexpr int MAX_ACTS = 4;
 constexpr int NT = 256;         // threads per CTA (8 warps)
 constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reduction path
+#ifndef SPK_SUB_F32
+#define SPK_SUB_F32 32  // FP32 blocked-summation length (rounding budget gamma_{SUB + m/SUB + 1})
+#endif
 #ifndef SPK_NARROW_2CTA
 #define SPK_NARROW_2CTA 1
 #endif
@@ -93,7 +96,7 @@ struct Cfg {
   static constexpr int NB = NBG * TB;
   static constexpr int KT_RAW = 32768 / (MMAX * (int)sizeof(T));
   static constexpr int KT = KT_RAW > MMAX ? MMAX : (KT_RAW < 1 ? 1 : KT_RAW);
-  static constexpr int SUB = sizeof(T) == 4 ? 16 : 1 << 20;  // blocked-sum length (FP32)
+  static constexpr int SUB = sizeof(T) == 4 ? SPK_SUB_F32 : 1 << 20;  // blocked-sum length (FP32)
   static constexpr int TILE = KT * MMAX;                 // elements per W tile
   // X row stride (elements): 16-byte aligned rows, and an odd number of
   // 16-byte units per row so the epilogue's vector stores spread over banks
