@@ -11,7 +11,8 @@ At N > 1 the frontier below a redundant top cut is split across ranks (one
 process per GPU, no collective in the build): total work is fixed, so
 scaling is "strong".  `extra` carries the C5 throughput sweep point
 (16M on-device cubes, 8x256, one launch), C1 (4x32, 64^3 grid) and C3
-(SIREN 8x256 ray casting: rays/s, interval at 1024^2, truncate:16 at 256^2),
+(SIREN 8x256 ray casting in FP64 -- the recipe's outputs are ~1e-11, below
+FP32 noise: rays/s, interval at 256^2, truncate:16 at 128^2; 250 steps/ray),
 C4 (ELU 8x512 mesh at 256^3) and F1 (frustum vs per-pixel casting, 1024^2,
 on the reference's relu_sdf fixture).
 
@@ -339,8 +340,8 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_mesh:
         extra["C4_elu8x512_mesh_256cubed"] = bench_c4(torch, sp, synth, 8)
     if not args.no_rays:
-        extra["C3_siren_rays_interval_1024sq"] = bench_c3(torch, sp, synth, "interval", 1024)
-        extra["C3_siren_rays_truncate16_256sq"] = bench_c3(torch, sp, synth, "affine-truncate:16", 256)
+        extra["C3_siren_rays_interval_256sq_fp64"] = bench_c3(torch, sp, synth, "interval", 256)
+        extra["C3_siren_rays_truncate16_128sq_fp64"] = bench_c3(torch, sp, synth, "affine-truncate:16", 128)
         extra["F1_frustum_relu_sdf_1024sq"] = bench_frustum(torch, sp, 1024)
 
     # ---- e2e through the public API (host arrays out)
@@ -418,24 +419,28 @@ def bench_c1(torch, sp, synth, flush, peak_tf):
 
 
 def bench_c3(torch, sp, synth, policy, res):
-    """C3: SIREN 3->8x256->1 (w0 = 30 folded, recentred), default camera
-    (reference bench.py:119-126), RayCastParams() defaults, FP32 kernels."""
+    """C3: SIREN 3->8x256->1 (w0 = 30 folded into the first layer, recentred),
+    default camera (reference bench.py:119-126), RayCastParams() defaults.
+    FP64 kernels: this recipe's outputs are ~1e-11 (median |f| over [-1,1]^3),
+    below FP32 evaluation noise, so only FP64 -- the reference's arithmetic --
+    gives meaningful hit decisions (then bit-identical to the reference)."""
     from paper_2202_02444_b200.camera import default_camera
 
     net = synth.config_net("C3")
     cam = default_camera(res)
-    sp.cast_camera(net, default_camera(16), sp.RayCastParams(), policy, precision="fp32")  # warm
+    sp.cast_camera(net, default_camera(16), sp.RayCastParams(), policy, precision="fp64")  # warm
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    hit, t, steps, st = sp.cast_camera(net, cam, sp.RayCastParams(), policy, precision="fp32")
+    hit, t, steps, st = sp.cast_camera(net, cam, sp.RayCastParams(), policy, precision="fp64")
     e1.record()
     torch.cuda.synchronize()
     dt = e0.elapsed_time(e1) / 1e3
     n = res * res
     return {"rays": n, "rays_per_s": n / dt, "ms": dt * 1e3, "ray_steps": st.ray_steps,
             "steps_per_ray": st.ray_steps / n, "certified_steps": st.certified_steps,
-            "lockstep_rounds": st.rounds, "hit_fraction": float(hit.float().mean().item()), "policy": policy}
+            "lockstep_rounds": st.rounds, "hit_fraction": float(hit.float().mean().item()), "policy": policy,
+            "precision": "fp64"}
 
 
 def bench_frustum(torch, sp, res):
