@@ -29,6 +29,12 @@ constexpr int MAX_LAYERS = 24;
 constexpr int MAX_ACTS = 4;
 constexpr int NT = 256;         // threads per CTA (8 warps)
 constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reduction path
+#ifndef SPK_F64_DIRECT
+#define SPK_F64_DIRECT 1
+#endif
+#ifndef SPK_SCALAR_UNROLL
+#define SPK_SCALAR_UNROLL 8
+#endif
 #ifndef SPK_SUB_F32
 #define SPK_SUB_F32 32  // FP32 blocked-summation length (rounding budget gamma_{SUB + m/SUB + 1})
 #endif
@@ -38,6 +44,7 @@ constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reducti
 #ifndef SPK_PACKED_F32
 #define SPK_PACKED_F32 1  // FP32 K loop on FFMA2 (sm_100a packed f32x2)
 #endif
+constexpr int kScalarUnroll = SPK_SCALAR_UNROLL;  // FP64 K loop unroll (A/B knob)
 constexpr int NSTAGE_MIN = 3;   // W tile ring depth floor (deeper when tiles are small)
 constexpr size_t SMEM_BUDGET = 210 * 1024;  // leaves room for the symbolic kernel's extras
 
@@ -376,11 +383,22 @@ SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, W
   using CF = Cfg<T, C, MMAX>;
   constexpr int TI = CF::TI, TB = CF::TB, CP = CF::CP, KT = CF::KT;
   const int ng = tid % CF::NG, bg = tid / CF::NG;
+  // RN columns accumulate in SUB-step partial sums (blocked summation, the
+  // blocks may span W tiles): rounding budget gamma_{SUB + ceil(m_in/SUB) + 1}
+  // instead of gamma_{m_in + 1}.  The RU error column needs no blocking.
+  // With one block (FP64: SUB = 2^20) the partials ARE the accumulators: the
+  // dot product accumulates in place and the bias is added last -- the same
+  // operation order as flushing one block onto the bias, 2 x TI x TB x (C-1)
+  // fewer registers.
+  constexpr bool DIRECT = SPK_F64_DIRECT && CF::SUB >= (1 << 20);
+  constexpr int CR = C > 1 ? C - 1 : 1;
+  constexpr int SUBIN = KT < CF::SUB ? KT : CF::SUB;
+  constexpr int PTI = DIRECT ? 1 : TI, PTB = DIRECT ? 1 : TB;
 
 #pragma unroll
   for (int ti = 0; ti < TI; ++ti) {
     const int i = CF::neuron(ng, ti);
-    const T b0 = (i < L.m_out) ? L.bias[i] : T(0);
+    const T b0 = (!DIRECT && i < L.m_out) ? L.bias[i] : T(0);
 #pragma unroll
     for (int tb = 0; tb < TB; ++tb) {
       acc[ti][tb][0] = b0;
@@ -388,25 +406,20 @@ SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, W
       for (int c = 1; c < C; ++c) acc[ti][tb][c] = (c == BIAS2) ? b0 : T(0);
     }
   }
-
-  // RN columns accumulate in SUB-step partial sums (blocked summation, the
-  // blocks may span W tiles): rounding budget gamma_{SUB + ceil(m_in/SUB) + 1}
-  // instead of gamma_{m_in + 1}.  The RU error column needs no blocking.
-  constexpr int CR = C > 1 ? C - 1 : 1;
-  constexpr int SUBIN = KT < CF::SUB ? KT : CF::SUB;
-  T part[TI][TB][CR];
+  T part[PTI][PTB][CR];
 #pragma unroll
-  for (int ti = 0; ti < TI; ++ti)
+  for (int ti = 0; ti < PTI; ++ti)
 #pragma unroll
-    for (int tb = 0; tb < TB; ++tb)
+    for (int tb = 0; tb < PTB; ++tb)
 #pragma unroll
       for (int c = 0; c < CR; ++c) part[ti][tb][c] = T(0);
   int since = 0;
   auto flush = [&]() {
+    if (DIRECT) return;
 #pragma unroll
-    for (int ti = 0; ti < TI; ++ti)
+    for (int ti = 0; ti < PTI; ++ti)
 #pragma unroll
-      for (int tb = 0; tb < TB; ++tb)
+      for (int tb = 0; tb < PTB; ++tb)
 #pragma unroll
         for (int c = 0; c < CR; ++c) {
           acc[ti][tb][c] += part[ti][tb][c];
@@ -431,12 +444,12 @@ SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, W
     for (int ti = 0; ti < TI; ++ti) {
 #pragma unroll
       for (int tb = 0; tb < TB; ++tb) {
+        T* dst = DIRECT ? acc[ti][tb] : part[DIRECT ? 0 : ti][DIRECT ? 0 : tb];
         if (C == 1) {
-          part[ti][tb][0] = Num<T>::fma_rn(w[ti], x[tb * CP], part[ti][tb][0]);
+          dst[0] = Num<T>::fma_rn(w[ti], x[tb * CP], dst[0]);
         } else {
 #pragma unroll
-          for (int c = 0; c < C - 1; ++c)
-            part[ti][tb][c] = Num<T>::fma_rn(w[ti], x[tb * CP + c], part[ti][tb][c]);
+          for (int c = 0; c < C - 1; ++c) dst[c] = Num<T>::fma_rn(w[ti], x[tb * CP + c], dst[c]);
           acc[ti][tb][C - 1] = Num<T>::fma_ru(fabs(w[ti]), x[tb * CP + C - 1], acc[ti][tb][C - 1]);
         }
       }
@@ -453,10 +466,11 @@ SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, W
 #pragma unroll 1
     for (int k0 = 0; k0 < k_end; k0 += SUBIN) {
       const int k1 = k0 + SUBIN < k_end ? k0 + SUBIN : k_end;
-      // register double buffering: fragments of step kk+1 load while step kk computes
+      // register double buffering: fragments of step kk+1 load while step kk
+      // computes (FP64: unroll 8 measured fastest; unroll 1 is 1.7x slower)
       T w0[TI], x0[TB * CP], w1[TI], x1[TB * CP];
       load_frag(Ws, Xt, k0, w0, x0);
-#pragma unroll 2
+#pragma unroll kScalarUnroll
       for (int kk = k0; kk < k1; kk += 2) {
         load_frag(Ws, Xt, kk + 1, w1, x1);
         fma_step(w0, x0);
@@ -472,6 +486,18 @@ SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, W
     ring.release(tid);  // this warp is done with the stage
   }
   if (since > 0) flush();
+  if (DIRECT) {
+#pragma unroll
+    for (int ti = 0; ti < TI; ++ti) {
+      const int i = CF::neuron(ng, ti);
+      const T b0 = (i < L.m_out) ? L.bias[i] : T(0);
+#pragma unroll
+      for (int tb = 0; tb < TB; ++tb) {
+        acc[ti][tb][0] = acc[ti][tb][0] + b0;
+        if (BIAS2 > 0 && BIAS2 < C - 1) acc[ti][tb][BIAS2 > 0 && BIAS2 < C ? BIAS2 : 0] += b0;
+      }
+    }
+  }
   csync();  // every warp finished reading X before any epilogue rewrites it
 }
 
