@@ -29,6 +29,9 @@ constexpr int MAX_LAYERS = 24;
 constexpr int MAX_ACTS = 4;
 constexpr int NT = 256;         // threads per CTA (8 warps)
 constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reduction path
+#ifndef SPK_INLINE_POINT_ACT
+#define SPK_INLINE_POINT_ACT 1
+#endif
 #ifndef SPK_F64_DIRECT
 #define SPK_F64_DIRECT 1
 #endif
@@ -712,7 +715,9 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
           for (int tb = 0; tb < TB; ++tb) out[tb * CP] = fmax(out[tb * CP], T(0));
         } else if (act != ACT_IDENTITY) {
 #pragma unroll 1
-          for (int tb = 0; tb < TB; ++tb) out[tb * CP] = act_value_slow<T>(act, out[tb * CP]);
+          for (int tb = 0; tb < TB; ++tb)
+            out[tb * CP] = SPK_INLINE_POINT_ACT ? act_value_inline<T>(act, out[tb * CP])
+                                                : act_value_slow<T>(act, out[tb * CP]);
         }
       }
       if (i >= L.m_out) {

@@ -252,6 +252,16 @@ SPK_RULE T act_value_slow(int act, T x) {  // float / double overloads of the CU
     default: return x;
   }
 }
+// Inline twin of act_value_slow for rolled loops (no call, no ABI spills).
+template <typename T>
+SPK_DEV T act_value_inline(int act, T x) {
+  switch (act) {
+    case ACT_ELU: return x >= T(0) ? x : expm1(x);
+    case ACT_SIN: return sin(x);
+    case ACT_TANH: return tanh(x);
+    default: return x;
+  }
+}
 template <typename T>
 SPK_DEV T act_value(int act, T x) {
   if (act == ACT_RELU) return fmax(x, T(0));
