@@ -158,6 +158,8 @@ def gen_trees(nets, out):
         ("relu_sdf_d7_interval", "relu_sdf", dict(policy=sp.INTERVAL_ONLY, max_depth=7)),
         ("relu4x32_d9_fixed", "relu4x32", dict(policy=sp.AFFINE_FIXED, max_depth=9)),
         ("elu_sdf_conv_trunc", "elu_sdf", dict(policy=sp.affine_truncate(8), delta=0.15)),
+        # the reference's DEFAULT policy on a 227-symbol net (large-capacity affine-full)
+        ("relu_sdf_d7_full", "relu_sdf", dict(policy=sp.AFFINE_FULL, max_depth=7)),
     ]
     for tag, netname, kw in cases:
         root = sp.build_spatial_tree(nets[netname], bounds, **kw)
@@ -308,6 +310,7 @@ def gen_mesh(nets, out):
         ("offset_box_m5_full", "offset_box", 5, sp.AFFINE_FULL),
         ("relu_sdf_m5_fixed", "relu_sdf", 5, sp.AFFINE_FIXED),
         ("elu_sdf_m5_fixed", "elu_sdf", 5, sp.AFFINE_FIXED),
+        ("relu_sdf_m5_full", "relu_sdf", 5, sp.AFFINE_FULL),  # extract_mesh's default policy
     ):
         mesh = sp.extract_mesh(nets[netname], bounds, m, policy=pol)
         out[f"mesh/{tag}/vertices"] = mesh.vertices

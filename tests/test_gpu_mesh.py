@@ -22,6 +22,7 @@ MESHES = {
     "offset_box_m5_full": ("offset_box", 5, "affine-full"),
     "relu_sdf_m5_fixed": ("relu_sdf", 5, "affine-fixed"),
     "elu_sdf_m5_fixed": ("elu_sdf", 5, "affine-fixed"),
+    "relu_sdf_m5_full": ("relu_sdf", 5, "affine-full"),
 }
 
 

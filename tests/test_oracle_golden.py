@@ -51,6 +51,7 @@ TREES = {
     "relu_sdf_d7_interval": ("relu_sdf", dict(policy="interval", max_depth=7)),
     "relu4x32_d9_fixed": ("relu4x32", dict(policy="affine-fixed", max_depth=9)),
     "elu_sdf_conv_trunc": ("elu_sdf", dict(policy="affine-truncate:8", delta=0.15)),
+    "relu_sdf_d7_full": ("relu_sdf", dict(policy="affine-full", max_depth=7)),
 }
 
 
@@ -110,6 +111,7 @@ MESHES = {
     "offset_box_m5_full": ("offset_box", 5, "affine-full"),
     "relu_sdf_m5_fixed": ("relu_sdf", 5, "affine-fixed"),
     "elu_sdf_m5_fixed": ("elu_sdf", 5, "affine-fixed"),
+    "relu_sdf_m5_full": ("relu_sdf", 5, "affine-full"),
 }
 
 
