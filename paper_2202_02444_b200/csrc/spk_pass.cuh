@@ -29,6 +29,9 @@ constexpr int MAX_LAYERS = 24;
 constexpr int MAX_ACTS = 4;
 constexpr int NT = 256;         // threads per CTA (8 warps)
 constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reduction path
+#ifndef SPK_SPEC_PREFETCH
+#define SPK_SPEC_PREFETCH 1  // unconditional 2-ahead fragment prefetch (see Cfg::SMEM)
+#endif
 #ifndef SPK_INLINE_POINT_ACT
 #define SPK_INLINE_POINT_ACT 1
 #endif
@@ -123,7 +126,10 @@ struct Cfg {
   static constexpr long long NS_FIT =
       ((long long)SMEM_BUDGET / MINB - (long long)sizeof(T) * (XS + NBUF) - 1024) / ((long long)sizeof(T) * TILE);
   static constexpr int NS = NS_FIT < NSTAGE_MIN ? NSTAGE_MIN : (NS_FIT > 16 ? 16 : (int)NS_FIT);
-  static constexpr size_t SMEM = sizeof(T) * (size_t)(XS + NS * TILE + NBUF) + 2 * 16 * 8 + 64;
+  // + one W row of slack: the K loops prefetch the fragment two rows ahead
+  // unconditionally (a predicated prefetch made ptxas copy fragments), so the
+  // last step may read one row past the last ring stage (values unused)
+  static constexpr size_t SMEM = sizeof(T) * (size_t)(XS + NS * TILE + NBUF + MMAX) + 2 * 16 * 8 + 64;
   static_assert(NG >= 1 && NG <= NT && NT % NG == 0, "tile shape");
   static_assert((TB * CP * sizeof(T)) % 16 == 0, "vector loads of X");
   static_assert(TI % G == 0, "W vector groups");
@@ -477,7 +483,7 @@ SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, W
       for (int kk = k0; kk < k1; kk += 2) {
         load_frag(Ws, Xt, kk + 1, w1, x1);
         fma_step(w0, x0);
-        if (kk + 2 < k1) load_frag(Ws, Xt, kk + 2, w0, x0);
+        if (SPK_SPEC_PREFETCH || kk + 2 < k1) load_frag(Ws, Xt, kk + 2, w0, x0);  // row k1 <= KT: in bounds
         fma_step(w1, x1);
       }
       since += SUBIN;
@@ -645,7 +651,7 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
       for (int kk = k0; kk < k1; kk += 2) {
         load_frag(Ws, Xt, kk + 1, w1, x1);
         fma_step(w0, x0);
-        if (kk + 2 < k1) load_frag(Ws, Xt, kk + 2, w0, x0);
+        if (SPK_SPEC_PREFETCH || kk + 2 < k1) load_frag(Ws, Xt, kk + 2, w0, x0);  // row k1 <= KT: in bounds
         fma_step(w1, x1);
       }
       since += SUBIN;
