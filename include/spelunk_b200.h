@@ -186,6 +186,14 @@ int spk_march(const spk_net* net, int policy, int n_keep, int precision, int64_t
 int spk_camera_dirs(const double* frame9, double half_w, double half_h, int width, int height,
                     double* dirs, void* stream);
 
+/* The activation rules alone (AFFINE_RULES, range_core.py:213-366): for n
+ * per-neuron bounds [lo, hi] (host arrays) the sound (alpha, beta, gamma) of
+ * op `act` with |h(x) - alpha x - beta| <= gamma on [lo, hi], computed by the
+ * kernels' own rule code in `precision`.  Backs the single-form
+ * affine_nonlinear of the Python layer. */
+int spk_affine_rule(int act, int precision, int64_t n, const double* lo, const double* hi, double* alpha,
+                    double* beta, double* gamma);
+
 /* §8(f1): frustum range-marching of a whole camera image
  * (cast_frustum_image, rays.py:232-341).  position3, frame9 (forward, right,
  * true_up), params6 (RayCastParams: t_max, sigma0, eta+, eta-, delta,

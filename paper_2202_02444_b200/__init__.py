@@ -21,6 +21,14 @@ from .network import (
     save_network,
 )
 from .range_core import (
+    AffineForm,
+    affine_linear,
+    affine_nonlinear,
+    affine_rule,
+    box_to_affine,
+    condense,
+    interval_of,
+    truncate,
     AFFINE_FIXED,
     AFFINE_FULL,
     INTERVAL_ONLY,

@@ -312,3 +312,129 @@ def interval_forward(net, box: QueryBox, precision: str = "fp32") -> Interval:
     _check_box(net, box)
     lo, hi = interval_forward_batch(net, box.center[None, :], _stack_axes([box.axes], net.input_dim), precision)
     return Interval(float(lo[0]), float(hi[0]))
+
+
+# ---------------------------------------------------------------------------
+# Single-form operations (range_core.py:61-110, 369-464): the definitional
+# semantics the batched kernels are tested against.  Bookkeeping on one small
+# form; the activation rules come from the device (spk_affine_rule), the
+# same rule code the kernels run.
+
+_OP_CODE = {"relu": _lib.OP_RELU, "elu": _lib.OP_ELU, "sin": _lib.OP_SIN, "tanh": _lib.OP_TANH,
+            "identity": _lib.OP_IDENTITY}
+
+
+@dataclass(frozen=True)
+class AffineForm:
+    """Vector affine form x_k = base_k + sum_j coeffs_kj eps_j + [-err_k, err_k]."""
+
+    base: np.ndarray
+    coeffs: np.ndarray
+    err: np.ndarray
+
+    def __post_init__(self):
+        base = np.asarray(self.base, dtype=np.float64)
+        coeffs = np.asarray(self.coeffs, dtype=np.float64)
+        err = np.asarray(self.err, dtype=np.float64)
+        if base.ndim != 1:
+            raise DimensionMismatch("base must be 1-d")
+        m = base.shape[0]
+        if coeffs.ndim != 2 or coeffs.shape[0] != m:
+            raise DimensionMismatch(f"coeffs must have shape ({m}, n)")
+        if err.shape != (m,):
+            raise DimensionMismatch(f"err must have shape ({m},)")
+        if np.any(err < 0.0):
+            raise InvalidParameter("err must be non-negative")
+        object.__setattr__(self, "base", base)
+        object.__setattr__(self, "coeffs", coeffs)
+        object.__setattr__(self, "err", err)
+
+    @property
+    def dim(self) -> int:
+        return self.base.shape[0]
+
+    @property
+    def n_symbols(self) -> int:
+        return self.coeffs.shape[1]
+
+
+def interval_of(a: AffineForm) -> Interval:
+    """Per-component [base - r, base + r], r = sum |coeffs| + err."""
+    r = np.abs(a.coeffs).sum(axis=1) + a.err
+    return Interval(a.base - r, a.base + r)
+
+
+def box_to_affine(box: QueryBox) -> AffineForm:
+    """One noise symbol per box axis."""
+    return AffineForm(base=box.center.copy(), coeffs=box.axes.T.copy(), err=np.zeros(box.dim))
+
+
+def affine_linear(a: AffineForm, layer) -> AffineForm:
+    """Through a dense layer: exact, no new uncertainty."""
+    w = np.asarray(layer.weights, dtype=np.float64)
+    if w.shape[1] != a.dim:
+        raise DimensionMismatch(f"layer expects {w.shape[1]} inputs, form has {a.dim}")
+    return AffineForm(base=w @ a.base + np.asarray(layer.bias, dtype=np.float64), coeffs=w @ a.coeffs,
+                      err=np.abs(w) @ a.err)
+
+
+def affine_rule(kind, lo, hi, precision: str = "fp64"):
+    """(alpha, beta, gamma) of an activation over per-neuron bounds, from the
+    device rule code (spk_affine_rule)."""
+    from .errors import UnsupportedActivation
+
+    name = getattr(kind, "value", kind)
+    if name not in _OP_CODE:
+        raise UnsupportedActivation(f"no affine rule for {kind!r}")
+    lo = np.ascontiguousarray(lo, dtype=np.float64)
+    hi = np.ascontiguousarray(hi, dtype=np.float64)
+    out = [np.empty(lo.shape) for _ in range(3)]
+    _lib.call("spk_affine_rule", _OP_CODE[name], _precision_code(precision), lo.size, lo.ctypes.data, hi.ctypes.data,
+              *[o.ctypes.data for o in out])
+    return tuple(out)
+
+
+def affine_nonlinear(a: AffineForm, kind, policy: CondensationPolicy) -> AffineForm:
+    """Through an elementwise activation under a policy: rule from the current
+    bounds, base/coefficients scaled by alpha, gamma folded into err (fixed)
+    or appended as a diagonal block of new symbols (full / truncate)."""
+    if policy.kind is PolicyKind.INTERVAL:
+        raise InvalidParameter("affine_nonlinear needs an affine policy")
+    b = interval_of(a)
+    alpha, beta, gamma = affine_rule(kind, b.lo, b.hi)
+    base = alpha * a.base + beta
+    coeffs = alpha[:, None] * a.coeffs
+    err = np.abs(alpha) * a.err
+    if policy.kind is PolicyKind.AFFINE_FIXED:
+        err = err + gamma
+    else:
+        coeffs = np.concatenate([coeffs, np.diag(gamma)], axis=1)
+    out = AffineForm(base, coeffs, err)
+    if policy.kind is PolicyKind.AFFINE_TRUNCATE and out.n_symbols > policy.n_keep:
+        out = truncate(out, policy.n_keep)
+    return out
+
+
+def condense(a: AffineForm, indices) -> AffineForm:
+    """Fold the named symbol columns into err (interval_of unchanged)."""
+    from .errors import IndexOutOfRange
+
+    idx = np.array(sorted({int(i) for i in indices}), dtype=np.intp)
+    if idx.size == 0:
+        return a
+    if idx[0] < 0 or idx[-1] >= a.n_symbols:
+        raise IndexOutOfRange(f"column index out of range 0..{a.n_symbols - 1}")
+    keep = np.ones(a.n_symbols, dtype=bool)
+    keep[idx] = False
+    return AffineForm(a.base.copy(), a.coeffs[:, keep], a.err + np.abs(a.coeffs[:, idx]).sum(axis=1))
+
+
+def truncate(a: AffineForm, n_keep: int) -> AffineForm:
+    """Keep the n_keep symbols of largest L1 norm (ties to the lower index,
+    kept order preserved); condense the rest."""
+    if n_keep < 1:
+        raise InvalidParameter("n_keep must be >= 1")
+    if a.n_symbols <= n_keep:
+        return a
+    order = np.argsort(-np.abs(a.coeffs).sum(axis=0), kind="stable")
+    return condense(a, order[n_keep:])

@@ -53,3 +53,27 @@ def test_width_limit_reported():
     net = NetworkSpec(3, (DenseLayer(np.zeros((600, 3)), np.zeros(600)), DenseLayer(np.zeros((1, 600)), np.zeros(1))))
     with pytest.raises(errors.DeviceError):
         DeviceNet(net, 0)
+
+
+def test_single_form_bookkeeping():
+    """condense / truncate / interval_of / box_to_affine semantics
+    (range_core.py:369-464); pure bookkeeping, no device needed."""
+    import numpy as np
+
+    import paper_2202_02444_b200 as sp
+
+    a = sp.AffineForm(np.array([1.0, -2.0]), np.array([[3.0, -1.0, 0.5], [0.0, 2.0, -2.0]]), np.array([0.1, 0.0]))
+    iv = sp.interval_of(a)
+    np.testing.assert_allclose(iv.lo, [1 - 4.6, -2 - 4.0])
+    c = sp.condense(a, [1])
+    assert c.n_symbols == 2 and np.allclose(c.err, [1.1, 2.0])
+    np.testing.assert_allclose(sp.interval_of(c).lo, iv.lo)          # condense keeps the interval
+    t = sp.truncate(a, 2)  # norms 3, 3, 2.5 -> ties keep the lower index: columns 0, 1
+    np.testing.assert_array_equal(t.coeffs, a.coeffs[:, :2])
+    box = sp.QueryBox(np.zeros(3), np.diag([0.1, 0.2, 0.3]))
+    f = sp.box_to_affine(box)
+    assert f.n_symbols == 3 and np.allclose(f.coeffs, np.diag([0.1, 0.2, 0.3]))
+    with pytest.raises(sp.errors.IndexOutOfRange):
+        sp.condense(a, [5])
+    with pytest.raises(sp.errors.InvalidParameter):
+        sp.truncate(a, 0)
