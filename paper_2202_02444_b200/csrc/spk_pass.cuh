@@ -96,10 +96,11 @@ struct Cfg {
   // register tile: TI neurons x TB boxes x C columns per thread
   static constexpr int TI = C <= 6 ? (sizeof(T) == 4 ? 8 : 4)
                                    : (C <= 20 ? VEC : (VEC / 2 > 0 ? VEC / 2 : 1));
-  // narrow nets (MMAX <= 64) with affine columns: one box per thread and two
+  // narrow nets (MMAX = 32) with affine columns: one box per thread and two
   // CTAs per SM -- their K loops are short, so latency hiding across CTAs
-  // matters more than register reuse across boxes
-  static constexpr int MINB = (SPK_NARROW_2CTA && MMAX <= 64 && C >= 3 && C <= 6) ? 2 : 1;
+  // matters more than register reuse across boxes (measured: 4x32 -19%
+  // time; at width 64 the 1-CTA, 2-box tile is 17% faster)
+  static constexpr int MINB = (SPK_NARROW_2CTA && MMAX <= 32 && C >= 3 && C <= 6) ? 2 : 1;
   static constexpr int TB = C == 1 ? (sizeof(T) == 4 ? 8 : 4)
                                    : (C == 2 ? 4 : (C <= 6 ? (MINB == 2 ? 1 : 2) : 1));
   static constexpr int CP = C == 1 ? 1 : (C == 2 ? 2 : (C <= 4 ? 4 : (C <= 6 ? (TB == 1 ? 8 : 6)
