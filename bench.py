@@ -454,8 +454,9 @@ def bench_frustum(torch, sp, res):
     net = sp.load_network(Path(__file__).resolve().parent / "tests" / "golden" / "nets" / "relu_sdf.json")
     out = {"net": "relu_sdf (reference fixture, 7x32 ReLU)", "res": res}
     for pol in ("affine-fixed", "interval"):
-        sp.cast_frustum_image(net, default_camera(64), sp.RayCastParams(), pol, precision="fp32", device_output=True)
-        sp.cast_camera(net, default_camera(64), sp.RayCastParams(), pol, precision="fp32")
+        # warm both arms at the measured resolution (pool growth, first launches)
+        sp.cast_frustum_image(net, default_camera(res), sp.RayCastParams(), pol, precision="fp32", device_output=True)
+        sp.cast_camera(net, default_camera(res), sp.RayCastParams(), pol, precision="fp32")
         torch.cuda.synchronize()
         e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         e[0].record()
