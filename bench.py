@@ -317,9 +317,25 @@ def run_ours(args, rank, world, local_rank):
         n_cert = sum(int((l != 0).sum().item()) for l in labs)
         certified = n_cert / max(1, arr.n_nodes)
 
-    total_time, units = reduce_time_units(float(np.sum(times)), float(units_local),
-                                          device=dev if args.dist_backend == "nccl" else "cpu")
+    coll_dev = dev if args.dist_backend == "nccl" else "cpu"
+    total_time, units = reduce_time_units(float(np.sum(times)), float(units_local), device=coll_dev)
     value = units / total_time
+
+    sharded = {}
+    if world > 1:
+        # final gather of the last build (the one collective of the tree path,
+        # outside the timed region): every rank receives the unsharded tree
+        barrier()
+        g0 = time.perf_counter()
+        tree = spatial.gather_spatial_tree(arr, device=coll_dev)
+        barrier()
+        sharded["tree_gather"] = {"ms": 1e3 * (time.perf_counter() - g0), "nodes": tree.n_nodes,
+                                  "levels": tree.n_levels, "complete": tree.n_nodes == 2 ** (DEPTH + 1) - 1,
+                                  "collective": f"all_gather ({args.dist_backend})"}
+        del tree
+        if not args.no_rays:
+            sharded["C3_siren_rays_interval_256sq_fp64"] = bench_c3_sharded(torch, sp, synth, 256, rank, world,
+                                                                            coll_dev, barrier)
 
     if rank != 0:
         return None
@@ -374,6 +390,7 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": int(launches / args.steps),
         "clocks": ck,
         "extra": extra,
+        "sharded": sharded or None,
     }
 
 
@@ -441,6 +458,34 @@ def bench_c3(torch, sp, synth, policy, res):
             "steps_per_ray": st.ray_steps / n, "certified_steps": st.certified_steps,
             "lockstep_rounds": st.rounds, "hit_fraction": float(hit.float().mean().item()), "policy": policy,
             "precision": "fp64"}
+
+
+def bench_c3_sharded(torch, sp, synth, res, rank, world, coll_dev, barrier):
+    """C3 interval rays sharded over ranks (interleaved 16x16 pixel tiles, no
+    collective in the march), rays/s over the max rank time, then the NCCL
+    final gather of the image (gather_camera_image)."""
+    from paper_2202_02444_b200.camera import default_camera
+    from paper_2202_02444_b200.shard import reduce_time_units
+
+    net = synth.config_net("C3")
+    cam = default_camera(res)
+    sp.cast_camera(net, default_camera(16), sp.RayCastParams(), "interval", precision="fp64")  # warm
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    pix, hit, t, steps, st = sp.cast_camera_sharded(net, cam, rank, world, sp.RayCastParams(), "interval",
+                                                    precision="fp64")
+    e1.record()
+    torch.cuda.synchronize()
+    dt, n = reduce_time_units(e0.elapsed_time(e1) / 1e3, float(pix.numel()), device=coll_dev)
+    barrier()
+    g0 = time.perf_counter()
+    img_hit, img_t, img_steps = sp.gather_camera_image(pix, hit, t, steps, res * res, device=coll_dev)
+    barrier()
+    return {"rays": int(n), "rays_per_s": n / dt, "ms": dt * 1e3, "gather_ms": 1e3 * (time.perf_counter() - g0),
+            "hit_fraction": float(img_hit.mean()), "steps_per_ray": float(img_steps.mean()),
+            "parallelism": f"pixel tiles 16x16 interleaved x{world}"}
 
 
 def bench_frustum(torch, sp, res):

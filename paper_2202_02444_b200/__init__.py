@@ -58,6 +58,7 @@ from .rays import (
     RayCastParams,
     cast_camera,
     cast_camera_sharded,
+    gather_camera_image,
     cast_frustum_image,
     cast_ray,
     cast_rays,
@@ -70,6 +71,8 @@ from .spatial import (
     build_spatial_tree,
     build_spatial_tree_arrays,
     build_spatial_tree_sharded,
+    gather_spatial_tree,
+    merge_sharded_trees,
     iter_leaves,
 )
 

@@ -186,6 +186,34 @@ def cast_camera_sharded(net, camera: Camera, rank: int, world: int, params: RayC
     return pix, hit, t, steps, st
 
 
+def gather_camera_image(pix, hit, t, steps, n_pixels: int, device=None):
+    """Final gather of cast_camera_sharded results (one all_gather per field
+    group after the march: NCCL on GPUs, gloo on CPU).  Returns full-image
+    NumPy arrays (hit bool, t FP64 with inf on misses, steps int64), pixel i
+    at row-major index i, on every rank.  Single process: a scatter."""
+    import torch.distributed as dist
+
+    from .shard import allgather_rows
+
+    def host(x):
+        return x.cpu().numpy() if dv.is_tensor(x) else np.asarray(x)
+
+    ints = np.stack([host(pix).astype(np.int64), host(hit).astype(np.int64), host(steps).astype(np.int64)], axis=1)
+    flts = host(t).astype(np.float64).reshape(-1, 1)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        ints = np.concatenate(allgather_rows(ints, device), axis=0)
+        flts = np.concatenate(allgather_rows(flts, device), axis=0)
+    out_hit = np.zeros(n_pixels, dtype=bool)
+    out_t = np.full(n_pixels, np.inf)
+    out_steps = np.zeros(n_pixels, dtype=np.int64)
+    if np.unique(ints[:, 0]).size != ints.shape[0]:
+        raise InvalidParameter("pixel shards overlap")
+    out_hit[ints[:, 0]] = ints[:, 1] != 0
+    out_t[ints[:, 0]] = flts[:, 0]
+    out_steps[ints[:, 0]] = ints[:, 2]
+    return out_hit, out_t, out_steps
+
+
 @dataclass
 class Frustum:
     """A rectangle of pixel rays marching together (rays.py:187-209)."""

@@ -49,3 +49,90 @@ def reduce_time_units(local_time: float, local_units: float, device=None):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dist.all_reduce(u, op=dist.ReduceOp.SUM)
     return float(t.item()), float(u.item())
+
+
+def interleaved_roots(n_open: int, rank: int, world: int) -> np.ndarray:
+    """Positions (into the frontier) of this rank's roots when the cut frontier
+    is dealt round-robin: spatially adjacent roots land on different ranks, so
+    convergence-mode builds (whose refinement depth varies over space) stay
+    balanced without a data-path collective."""
+    return np.arange(rank, int(n_open), int(world), dtype=np.int64)
+
+
+# --------------------------------------------------------------------------
+# Final gather of a frontier-sharded tree.
+#
+# Level order of the unsharded tree (spatial.py:246-256, reproduced by the
+# device builder): level k+1 lists the low children of level k's split nodes
+# in level-k order, then their high children.  Below a cut whose split nodes
+# (the roots) are numbered g = 0..R-1 in frontier order, the position of a
+# node is therefore lexicographic in (b_j, b_{j-1}, ..., b_1, g) where b_i is
+# its low/high choice i levels below the cut -- the integer
+#     key_j = b_j * 2^(j-1) * R + key_{j-1}(parent),   key_0 = g.
+# Every rank computes the keys of its own sub-tree; sorting the union of the
+# ranks' level-j nodes by key gives the unsharded level j, and the parent of
+# a node is the position of key mod 2^(j-1)R in level j-1.
+
+def subtree_keys(parents, root_ids, n_roots: int):
+    """Order keys of a sub-build's levels.  `parents[j]` is level j's parent
+    index array (j >= 1; parents[0] is ignored), `root_ids` the global frontier
+    positions of the sub-build's level-0 nodes."""
+    keys = [np.asarray(root_ids, dtype=np.int64)]
+    for j in range(1, len(parents)):
+        par = np.asarray(parents[j], dtype=np.int64)
+        k = len(par) // 2
+        bit = np.zeros(len(par), dtype=np.int64)
+        bit[k:] = 1
+        keys.append(bit * ((1 << (j - 1)) * int(n_roots)) + keys[j - 1][par])
+    return keys
+
+
+def merge_shard_levels(parts, open_idx, n_fields_f64: int):
+    """Merge the ranks' sub-tree levels into the unsharded levels below the cut.
+
+    parts: per rank, a list over levels j = 1..J of (f64 rows (n, F), i64 rows
+    (n, 3) = [key, label, face]).  open_idx: the cut level's split-node
+    indices (frontier order; root g is node open_idx[g]).  Returns a list over
+    j of (f64 rows, label, face, parent) in the unsharded order."""
+    open_idx = np.asarray(open_idx, dtype=np.int64)
+    n_roots = len(open_idx)
+    depth = max((len(p) for p in parts), default=0)
+    out = []
+    prev_keys = None
+    for j in range(1, depth + 1):
+        fs = [p[j - 1][0] for p in parts if len(p) >= j]
+        ks = [p[j - 1][1] for p in parts if len(p) >= j]
+        f = np.concatenate(fs, axis=0) if fs else np.zeros((0, n_fields_f64))
+        k = np.concatenate(ks, axis=0) if ks else np.zeros((0, 3), dtype=np.int64)
+        order = np.argsort(k[:, 0], kind="stable")
+        f, k = f[order], k[order]
+        span = (1 << (j - 1)) * n_roots
+        pkey = k[:, 0] % span
+        if j == 1:
+            parent = open_idx[pkey]
+        else:
+            parent = np.searchsorted(prev_keys, pkey)
+        out.append((f, k[:, 1].astype(np.int8), k[:, 2].astype(np.int8), parent.astype(np.int64)))
+        prev_keys = k[:, 0]
+    return out
+
+
+def allgather_rows(rows: np.ndarray, device=None):
+    """all_gather of a per-rank (n_r, F) array with n_r varying by rank
+    (sizes first, then one padded all_gather).  Returns the list over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size()
+    rows = np.ascontiguousarray(rows)
+    n = torch.tensor([rows.shape[0]], dtype=torch.int64, device=device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n)
+    sizes = [int(s.item()) for s in sizes]
+    cap = max(sizes) if sizes else 0
+    t = torch.zeros((cap,) + rows.shape[1:], dtype=torch.from_numpy(rows[:0]).dtype, device=device)
+    if rows.shape[0]:
+        t[: rows.shape[0]] = torch.from_numpy(rows).to(device)
+    bufs = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(bufs, t)
+    return [b[:s].cpu().numpy() for b, s in zip(bufs, sizes)]

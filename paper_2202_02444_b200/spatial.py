@@ -325,19 +325,24 @@ def materialize(arrays: TreeArrays) -> TreeNode:
 
 def build_spatial_tree_sharded(net, bounds: AABB, max_depth: int, policy, rank: int, world: int,
                                precision: str = "fp32", min_roots_per_rank: int = 64,
-                               to_host: bool = False) -> TreeArrays:
+                               to_host: bool = False, roots: str = "contiguous") -> TreeArrays:
     """Fixed-depth build split across `world` ranks (one per GPU).
 
     Every rank builds the top levels redundantly until the UNKNOWN frontier
     holds >= min_roots_per_rank * world nodes (or max_depth is reached), then
-    refines its contiguous slice of that frontier to max_depth.  No
-    collective runs inside the build; the union of the ranks' levels below
-    the cut equals the unsharded tree (node AABBs are bit-identical because
-    splits are exact FP64 midpoints).
+    refines its share of that frontier to max_depth -- a contiguous slice
+    (`roots="contiguous"`) or every world-th root (`"interleaved"`, static
+    balance for builds whose depth varies over space).  No collective runs
+    inside the build; the union of the ranks' levels below the cut equals the
+    unsharded tree (node AABBs are bit-identical because splits are exact
+    FP64 midpoints) and `gather_spatial_tree` reassembles it in the
+    reference's level order.
     """
-    from .shard import first_cut, split_frontier
+    from .shard import first_cut, interleaved_roots, split_frontier
 
     _check_domain(net, bounds)
+    if roots not in ("contiguous", "interleaved"):
+        raise InvalidParameter(f"unknown root assignment {roots!r}")
     cut = first_cut(world, min_roots_per_rank, max_depth)
     while True:
         top = build_spatial_tree_arrays(net, bounds, 1.0, policy, cut, precision, to_host=True)
@@ -347,13 +352,88 @@ def build_spatial_tree_sharded(net, bounds: AABB, max_depth: int, policy, rank: 
         cut = min(max_depth, cut + 1)
     last = top.levels[-1]
     open_idx = np.flatnonzero(_np(last.label) == 0)
-    part = split_frontier(open_idx, rank, world)
+    if roots == "contiguous":
+        root_ids = split_frontier(np.arange(len(open_idx)), rank, world)
+    else:
+        root_ids = interleaved_roots(len(open_idx), rank, world)
+    part = open_idx[root_ids]
+    meta = dict(cut=cut, roots=int(part.size), top_nodes=top.n_nodes, top=top.levels, open_idx=open_idx,
+                root_ids=np.asarray(root_ids, dtype=np.int64), rank=rank, world=world)
     if cut >= max_depth or part.size == 0:
-        top.meta.update(cut=cut, roots=int(part.size), top_nodes=top.n_nodes)
+        top.meta.update(meta)
+        top.meta["own_sub"] = False
         return top
     sub = _build(net, _np(last.lo)[part], _np(last.hi)[part], cut, 1.0, policy, max_depth, precision, to_host)
-    sub.meta.update(cut=cut, roots=int(part.size), top_nodes=top.n_nodes, top_levels=top.levels)
+    sub.meta.update(meta, top_levels=top.levels, own_sub=True)
     return sub
+
+
+def _pack_subtree(arr: TreeArrays):
+    """A sharded build's own levels below the cut as (level sizes (J, 1),
+    f64 rows [lo, hi, bound_lo, bound_hi], i64 rows [key, label, face])."""
+    from .shard import subtree_keys
+
+    meta = arr.meta
+    if "open_idx" not in meta:
+        raise InvalidParameter("not a build_spatial_tree_sharded result")
+    d = _np(meta["top"][0].lo).shape[1]
+    f_rows, i_rows, sizes = [], [], []
+    if meta.get("own_sub"):
+        lv = arr.levels
+        keys = subtree_keys([_np(l.parent) for l in lv], meta["root_ids"], len(meta["open_idx"]))
+        for j in range(1, len(lv)):
+            l = lv[j]
+            f_rows.append(np.concatenate([_np(l.lo), _np(l.hi), _np(l.bound_lo)[:, None],
+                                          _np(l.bound_hi)[:, None]], axis=1))
+            i_rows.append(np.stack([keys[j], _np(l.label).astype(np.int64), _np(l.face).astype(np.int64)], axis=1))
+            sizes.append(len(l))
+    f_all = np.concatenate(f_rows, axis=0) if f_rows else np.zeros((0, 2 * d + 2))
+    i_all = np.concatenate(i_rows, axis=0) if i_rows else np.zeros((0, 3), dtype=np.int64)
+    return np.asarray(sizes, dtype=np.int64).reshape(-1, 1), f_all, i_all
+
+
+def _assemble(meta, packed) -> TreeArrays:
+    from .shard import merge_shard_levels
+
+    top = meta["top"]
+    d = _np(top[0].lo).shape[1]
+    parts = []
+    for sz, fr, ir in packed:
+        edges = np.cumsum(np.r_[0, sz[:, 0]]).astype(np.int64)
+        parts.append([(fr[edges[j]:edges[j + 1]], ir[edges[j]:edges[j + 1]]) for j in range(len(sz))])
+    levels = [TreeLevel(*[_np(getattr(l, f)) for f in ("lo", "hi", "bound_lo", "bound_hi", "label", "face",
+                                                       "parent")]) for l in top]
+    for f, lab, face, parent in merge_shard_levels(parts, meta["open_idx"], 2 * d + 2):
+        levels.append(TreeLevel(np.ascontiguousarray(f[:, :d]), np.ascontiguousarray(f[:, d:2 * d]),
+                                f[:, 2 * d].copy(), f[:, 2 * d + 1].copy(), lab, face, parent))
+    return TreeArrays(levels, 0, meta={"cut": meta["cut"], "gathered_from": len(packed)})
+
+
+def merge_sharded_trees(parts) -> TreeArrays:
+    """The unsharded tree from every rank's build_spatial_tree_sharded result
+    (held in one process); the level order is the reference's."""
+    parts = list(parts)
+    if not parts:
+        raise InvalidParameter("no shards")
+    return _assemble(parts[0].meta, [_pack_subtree(p) for p in parts])
+
+
+def gather_spatial_tree(arr: TreeArrays, device=None) -> TreeArrays:
+    """Final gather of a frontier-sharded build -- the one collective step,
+    after the build (torch.distributed all_gather: NCCL over NVLink on GPUs,
+    gloo on CPU).  Every rank receives the whole tree as host level arrays in
+    the unsharded (reference) order: the redundant top levels, then each
+    deeper level merged by order key (shard.subtree_keys)."""
+    import torch.distributed as dist
+
+    from .shard import allgather_rows
+
+    mine = _pack_subtree(arr)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        packed = list(zip(*[allgather_rows(x, device) for x in mine]))
+    else:
+        packed = [mine]
+    return _assemble(arr.meta, packed)
 
 
 # The volumetric queries live in queries.py; re-exported here because the

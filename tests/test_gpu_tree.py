@@ -140,3 +140,24 @@ def test_sharded_union_equals_full(net_paths):
         want = np.concatenate([ref.lo, ref.hi, ref.label[:, None].astype(float)], axis=1)
         assert got.shape == want.shape
         np.testing.assert_array_equal(np.unique(got, axis=0), np.unique(want, axis=0))
+
+
+@pytest.mark.parametrize("roots,world,precision", [("contiguous", 4, "fp32"), ("interleaved", 3, "fp64"),
+                                                   ("interleaved", 8, "fp32")])
+def test_sharded_merge_equals_full(net_paths, roots, world, precision):
+    """Final gather (merge_sharded_trees, the local form of gather_spatial_tree):
+    the merged shards equal the unsharded device tree array-for-array, in the
+    reference's level order -- AABBs, bounds, labels, faces, parents."""
+    net = sp.load_network(net_paths["relu4x32"])
+    full = spatial.build_spatial_tree_arrays(net, BOUNDS, policy="affine-fixed", max_depth=10,
+                                             precision=precision)
+    parts = [spatial.build_spatial_tree_sharded(net, BOUNDS, 10, "affine-fixed", r, world, precision=precision,
+                                                min_roots_per_rank=2, to_host=True, roots=roots)
+             for r in range(world)]
+    merged = spatial.merge_sharded_trees(parts)
+    assert merged.n_levels == full.n_levels and merged.n_nodes == full.n_nodes
+    for d, (g, f) in enumerate(zip(merged.levels, full.levels)):
+        for k in ("lo", "hi", "bound_lo", "bound_hi", "label", "face"):
+            np.testing.assert_array_equal(getattr(g, k), getattr(f, k), err_msg=f"{k} at depth {d}")
+        if d:
+            np.testing.assert_array_equal(g.parent, f.parent, err_msg=f"parent at depth {d}")

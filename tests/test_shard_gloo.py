@@ -92,3 +92,88 @@ def test_shard_range_partition():
 def test_pixel_tiles_cover_image():
     tiles = [t for r in range(3) for t in shard.pixel_tiles(64, 48, 16, r, 3)]
     assert sorted(tiles) == sorted((y, x) for y in range(0, 48, 16) for x in range(0, 64, 16))
+
+
+def _oracle_shard(net, depth, rank, world, roots):
+    """A rank's build_spatial_tree_sharded result with the oracle standing in
+    for the device builder (same cut, same root assignment, same level layout)."""
+    from paper_2202_02444_b200.spatial import TreeArrays, TreeLevel
+
+    cut = shard.first_cut(world, 2, depth)
+    top = orc.tree_levels(net, -np.ones(3), np.ones(3), "affine-fixed", max_depth=cut)
+
+    def level(l):
+        blo, bhi = orc.bound_aabbs(net, l["lo"], l["hi"], "affine-fixed")
+        return TreeLevel(l["lo"], l["hi"], blo, bhi, l["label"], l["face"], l["parent"])
+
+    open_idx = np.flatnonzero(top[-1]["label"] == 0)
+    if roots == "contiguous":
+        root_ids = shard.split_frontier(np.arange(len(open_idx)), rank, world)
+    else:
+        root_ids = shard.interleaved_roots(len(open_idx), rank, world)
+    part = open_idx[root_ids]
+    sub = orc.tree_levels(net, top[-1]["lo"][part], top[-1]["hi"][part], "affine-fixed", max_depth=depth,
+                          start_depth=cut) if part.size else []
+    meta = dict(cut=cut, top=[level(l) for l in top], open_idx=open_idx, root_ids=np.asarray(root_ids),
+                own_sub=bool(part.size), world=world)
+    return TreeArrays([level(l) for l in sub] if sub else [level(l) for l in top], cut, meta=meta)
+
+
+def _gather_worker(rank, world, port, depth, roots, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2202_02444_b200 import gather_camera_image, gather_spatial_tree
+
+        net = orc.load_net(NET)
+        tree = gather_spatial_tree(_oracle_shard(net, depth, rank, world, roots))
+        # camera image: this rank's interleaved tiles with synthetic results
+        w, h = 40, 24
+        pix = np.concatenate([(np.arange(ty, min(ty + 16, h))[:, None] * w
+                               + np.arange(tx, min(tx + 16, w))[None, :]).ravel()
+                              for ty, tx in shard.pixel_tiles(w, h, 16, rank, world)])
+        img = gather_camera_image(pix, pix % 3 == 0, np.where(pix % 3 == 0, pix * 0.5, np.inf), pix % 7,
+                                  w * h)
+        if rank == 0:
+            out_q.put(([(l.lo, l.hi, l.label, l.face, l.parent) for l in tree.levels], img))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("roots", ["contiguous", "interleaved"])
+def test_gather_sharded_tree_gloo(roots):
+    """The final gather of a frontier-sharded build reproduces the unsharded
+    tree in the reference's level order (AABBs, labels, faces, parents)."""
+    depth, world = 9, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, depth, roots, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    levels, (hit, t, steps) = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    full = orc.tree_levels(orc.load_net(NET), -np.ones(3), np.ones(3), "affine-fixed", max_depth=depth)
+    assert len(levels) == len(full)
+    for got, ref in zip(levels, full):
+        for g, k in zip(got, ("lo", "hi", "label", "face", "parent")):
+            if k == "parent" and ref["parent"][0] < 0:
+                continue  # root
+            np.testing.assert_array_equal(g, ref[k])
+    idx = np.arange(40 * 24)
+    np.testing.assert_array_equal(hit, idx % 3 == 0)
+    np.testing.assert_array_equal(t, np.where(idx % 3 == 0, idx * 0.5, np.inf))
+    np.testing.assert_array_equal(steps, idx % 7)
+
+
+def test_subtree_keys_order():
+    """Keys of two complete sub-trees interleave into the unsharded order."""
+    # 2 roots, each split fully for 2 levels: level 1 = [lo(r0), lo(r1), hi(r0), hi(r1)]
+    par1 = np.array([0, 0])
+    k = shard.subtree_keys([None, par1], [1], 2)
+    assert list(k[1]) == [1, 3]
+    k0 = shard.subtree_keys([None, par1], [0], 2)
+    assert sorted(list(k0[1]) + list(k[1])) == [0, 1, 2, 3]
