@@ -749,6 +749,18 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
   using CF = Cfg<T, C, MMAX>;
   constexpr int TI = CF::TI, TB = CF::TB, CP = CF::CP;
   const int ng = tid % CF::NG, bg = tid / CF::NG;
+  // layer parameters the epilogue needs, read before the K loop so their
+  // latency hides behind it (dynamically indexed parameter / global reads at
+  // the epilogue stalled every warp at once); the common single-ReLU layer
+  // takes a constant-folded rule
+  const int nact = L.n_act;
+  const bool relu_only = nact == 1 && L.act[0] == ACT_RELU;
+  T be_r[TI];
+#pragma unroll
+  for (int ti = 0; ti < TI; ++ti) {
+    const int i = CF::neuron(ng, ti);
+    be_r[ti] = (MODE != MODE_POINT && i < L.m_out) ? L.berr[i] : T(0);
+  }
   T acc[TI][TB][C];
   dense_kloop<T, C, MMAX, (MODE >= MODE_MI ? 1 : -1)>(L, X, ring, tid, acc);
 
@@ -763,8 +775,8 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
       T out[TB * CP];
 #pragma unroll
       for (int tb = 0; tb < TB; ++tb) out[tb * CP] = i < L.m_out ? acc[ti][tb][0] : T(0);
-      for (int a = 0; a < L.n_act; ++a) {
-        const int act = L.act[a];
+      for (int a = 0; a < nact; ++a) {
+        const int act = relu_only ? ACT_RELU : L.act[a];
         if (act == ACT_RELU) {
 #pragma unroll
           for (int tb = 0; tb < TB; ++tb) out[tb * CP] = fmax(out[tb * CP], T(0));
@@ -791,7 +803,7 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
   for (int ti = 0; ti < TI; ++ti) {
     const int i = CF::neuron(ng, ti);
     const bool valid = i < L.m_out;
-    const T be = valid ? L.berr[i] : T(0);
+    const T be = be_r[ti];
     T out[TB * CP];
 #pragma unroll
     for (int c = 0; c < TB * CP; ++c) out[c] = T(0);
@@ -799,7 +811,11 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
     for (int tb = 0; tb < TB; ++tb) {
       if (valid) {
         State<T, C, MODE> st = state_from<T, C, MODE>(acc[ti][tb], be);
-        for (int a = 0; a < L.n_act; ++a) apply_act<T, C, MODE>(st, L.act[a]);
+        if (relu_only) {
+          apply_act<T, C, MODE>(st, ACT_RELU);
+        } else {
+          for (int a = 0; a < nact; ++a) apply_act<T, C, MODE>(st, L.act[a]);
+        }
         pack_next<T, C, MODE>(st, gamma_next, out + tb * CP);
       }
     }
