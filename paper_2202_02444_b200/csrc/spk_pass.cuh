@@ -470,6 +470,34 @@ SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, W
     }
   };
 
+  // element-wise fragment loads (no type-punned register arrays: punning
+  // FP64 fragments through float4 made ptxas stage them in local memory)
+  auto load_frag_e = [&](const T* __restrict__ Ws, const T* __restrict__ Xt, int kk, T* w, T* x) {
+    using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
+#pragma unroll
+    for (int q = 0; q < TI / CF::G; ++q) {
+      const T* src = Ws + kk * MMAX + q * (CF::NG * CF::G) + ng * CF::G;
+#pragma unroll
+      for (int e = 0; e < CF::G; e += 2) {
+        const V2 v = *reinterpret_cast<const V2*>(src + e);
+        w[q * CF::G + e] = v.x;
+        w[q * CF::G + e + 1] = v.y;
+      }
+    }
+    const V2* xp = reinterpret_cast<const V2*>(Xt + (size_t)kk * CF::RS);
+#pragma unroll
+    for (int q = 0; q < TB * CP / 2; ++q) {
+      const V2 v = xp[q];
+      x[2 * q] = v.x;
+      x[2 * q + 1] = v.y;
+    }
+  };
+  // one block (DIRECT): every full chunk of CH k-steps fully unrolled with
+  // statically indexed double-buffered fragments (no register rotation)
+  constexpr int CH = KT < 32 ? KT : 32;
+  constexpr bool UNROLLED = SPK_UNROLL_BLOCK && DIRECT && (KT % CH) == 0 && (CF::G % 2) == 0 &&
+                            ((TB * CP) % 2) == 0;
+
   for (int t = 0; t < L.ntiles; ++t) {
     const T* __restrict__ Ws = ring.acquire();
     const T* __restrict__ Xt = X + (size_t)(t * KT) * CF::RS + bg * TB * CP;
@@ -477,6 +505,20 @@ SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, W
     // double-buffer pair), e.g. 4 k-steps instead of KT for the 3-input layer
     int k_end = L.m_in - t * KT;
     k_end = k_end > KT ? KT : ((k_end + 1) & ~1);
+    if (UNROLLED && k_end == KT) {
+#pragma unroll 1
+      for (int k0 = 0; k0 < KT; k0 += CH) {
+        T wf[2][TI], xf[2][TB * CP];
+        load_frag_e(Ws, Xt, k0, wf[0], xf[0]);
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          if (j + 1 < CH) load_frag_e(Ws, Xt, k0 + j + 1, wf[(j + 1) & 1], xf[(j + 1) & 1]);
+          fma_step(wf[j & 1], xf[j & 1]);
+        }
+      }
+      ring.release(tid);
+      continue;
+    }
 #pragma unroll 1
     for (int k0 = 0; k0 < k_end; k0 += SUBIN) {
       const int k1 = k0 + SUBIN < k_end ? k0 + SUBIN : k_end;
