@@ -138,6 +138,7 @@ __global__ void __launch_bounds__(NT, (Cfg<T, C, MMAX>::MINB))
 
   for (long long tile = blockIdx.x; tile < nbt; tile += gridDim.x) {
     const long long g0 = tile * NB;
+    if (CF::TEAMSYNC) csync();  // every team is done with the previous tile's X
     prep_inputs<T, C, MMAX, MODE>(net, in, n, g0, X, tid, true);
     csync();
     auto emit = [&](int b, const State<T, C, MODE>& st) {

@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(NT, (Cfg<T, C, MMAX>::MINB))
 
   for (long long tile = blockIdx.x; tile < nbt; tile += gridDim.x) {
     const long long g0 = tile * NB;
+    if (CF::TEAMSYNC) csync();  // every team is done with the previous tile's X
     // ---- probe point + segment box of every ray in the tile -> X rows 0..3
     for (int q = tid; q < 4 * NB; q += NT) {
       const int k = q / NB, b = q % NB;

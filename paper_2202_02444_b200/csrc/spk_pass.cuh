@@ -51,6 +51,9 @@ constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reducti
 #ifndef SPK_UNROLL_BLOCK
 #define SPK_UNROLL_BLOCK 1  // FP32 K loop: each full blocked-summation chunk fully unrolled
 #endif
+#ifndef SPK_TEAM_SYNC
+#define SPK_TEAM_SYNC 1  // layer boundaries synchronise teams, not the CTA (Cfg::TEAMSYNC)
+#endif
 #ifndef SPK_PACKED_F32
 #define SPK_PACKED_F32 1  // FP32 K loop on FFMA2 (sm_100a packed f32x2)
 #endif
@@ -139,6 +142,21 @@ struct Cfg {
   static_assert((TB * CP * sizeof(T)) % 16 == 0, "vector loads of X");
   static_assert(TI % G == 0, "W vector groups");
   SPK_DEV static int neuron(int ng, int ti) { return (ti / G) * (NG * G) + ng * G + (ti % G); }
+  // A box group's X columns are read (K loop) and rewritten (epilogue) only
+  // by the threads that own it: the NG threads tid in [bg*NG, (bg+1)*NG).
+  // Those form a "team" -- TEAM = NG/32 whole warps, or (NG <= 32) one warp
+  // holding 32/NG box groups -- which is all a layer boundary has to
+  // synchronise (named barrier per team, or __syncwarp); the W ring keeps the
+  // teams within NS tiles of each other.
+  static constexpr int TEAM = NG >= 32 ? NG / 32 : 1;            // warps per team
+  static constexpr int TEAM_BOXES = NG >= 32 ? TB : (32 / NG) * TB;  // boxes per team
+  static constexpr int NTEAMS = NT / (32 * TEAM);
+  static_assert(TEAM == 1 || NTEAMS <= 14, "named barriers 2..15");
+  // Team-local layer boundaries pay off when the W ring is deep enough to
+  // absorb the teams' drift (measured: +4-5% with >= 4 stages; with the
+  // 3-stage ring of 8x256 affine tiles a leading team stalls on refills that
+  // wait for the slowest one, -3%), so shallow rings keep the CTA barrier.
+  static constexpr bool TEAMSYNC = SPK_TEAM_SYNC && NS >= 4;
 };
 
 // copy N bytes (N in {4, 8, 16}) between 16/8/4-aligned addresses as one access
@@ -173,6 +191,16 @@ SPK_DEV void mbar_arrive(uint64_t* bar) {
 }
 // barrier among the NT compute threads only (the producer warp never joins)
 SPK_DEV void csync() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
+// barrier among the warps of one team (see Cfg::TEAM)
+template <int TEAM>
+SPK_DEV void team_sync(int tid) {
+  if (TEAM == 1) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(2 + (tid >> 5) / TEAM), "n"(TEAM * 32) : "memory");
+  }
+}
+
 
 SPK_DEV void tma_bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
@@ -391,7 +419,7 @@ SPK_DEV State<T, C, MODE> state_from(const T* col, T be) {
 // round-to-nearest columns are summed in blocks of SUB k-steps (fresh
 // partials added to the running sums), so the rounding budget is
 // gamma_{SUB + ceil(m_in/SUB) + 1} instead of gamma_{m_in + 1}.
-template <typename T, int C, int MMAX, int BIAS2 = -1>
+template <typename T, int C, int MMAX, int BIAS2 = -1, bool TEAMS = false>
 SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, WRing<T, C, MMAX>& ring, int tid,
                                 T (&acc)[Cfg<T, C, MMAX>::TI][Cfg<T, C, MMAX>::TB][C]) {
   using CF = Cfg<T, C, MMAX>;
@@ -554,7 +582,12 @@ SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, W
       }
     }
   }
-  csync();  // every warp finished reading X before any epilogue rewrites it
+  // every thread of the team finished reading X before its epilogue rewrites it
+  if (TEAMS) {
+    team_sync<CF::TEAM>(tid);
+  } else {
+    csync();
+  }
 }
 
 
@@ -591,7 +624,7 @@ SPK_DEV f32x2 f2_pack(float lo, float hi) {
 // pairs, an optional odd RN column, and the round-up error column (scalar
 // FFMA.RP with the |W| operand modifier).  Point evaluation (C == 1) pairs
 // adjacent boxes instead.  Same blocked-summation budget as the scalar loop.
-template <int C, int MMAX, int BIAS2 = -1>
+template <int C, int MMAX, int BIAS2 = -1, bool TEAMS = false>
 SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__ X, WRing<float, C, MMAX>& ring,
                              int tid, float (&acc)[Cfg<float, C, MMAX>::TI][Cfg<float, C, MMAX>::TB][C]) {
   using CF = Cfg<float, C, MMAX>;
@@ -754,7 +787,11 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
     ring.release(tid);
   }
   if (since > 0) flush();
-  csync();
+  if (TEAMS) {
+    team_sync<CF::TEAM>(tid);
+  } else {
+    csync();
+  }
   // unpack into the scalar accumulator layout of the epilogue
 #pragma unroll
   for (int ti = 0; ti < TI; ++ti) {
@@ -775,13 +812,13 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
 
 // BIAS2 >= 0: a second column that also starts from the bias (march modes:
 // the point value in column 0 and the bound's base in column 1)
-template <typename T, int C, int MMAX, int BIAS2 = -1>
+template <typename T, int C, int MMAX, int BIAS2 = -1, bool TEAMS = false>
 SPK_DEV void dense_kloop(const LayerDev<T>& L, const T* __restrict__ X, WRing<T, C, MMAX>& ring, int tid,
                          T (&acc)[Cfg<T, C, MMAX>::TI][Cfg<T, C, MMAX>::TB][C]) {
   if constexpr (sizeof(T) == 4 && SPK_PACKED_F32) {
-    dense_kloop_f32<C, MMAX, BIAS2>(L, X, ring, tid, acc);
+    dense_kloop_f32<C, MMAX, BIAS2, TEAMS>(L, X, ring, tid, acc);
   } else {
-    dense_kloop_scalar<T, C, MMAX, BIAS2>(L, X, ring, tid, acc);
+    dense_kloop_scalar<T, C, MMAX, BIAS2, TEAMS>(L, X, ring, tid, acc);
   }
 }
 
@@ -804,7 +841,7 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
     be_r[ti] = (MODE != MODE_POINT && i < L.m_out) ? L.berr[i] : T(0);
   }
   T acc[TI][TB][C];
-  dense_kloop<T, C, MMAX, (MODE >= MODE_MI ? 1 : -1)>(L, X, ring, tid, acc);
+  dense_kloop<T, C, MMAX, (MODE >= MODE_MI ? 1 : -1), CF::TEAMSYNC>(L, X, ring, tid, acc);
 
   // epilogue: activation rules, write next X in place (one contiguous
   // TB*CP vector per neuron: the thread's boxes are adjacent in the row)
@@ -838,7 +875,11 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
 #pragma unroll
       for (int q = 0; q < (int)(TB * CP * sizeof(T) / 16); ++q) dst[q] = srcv[q];
     }
-    csync();
+    if (CF::TEAMSYNC) {
+      team_sync<CF::TEAM>(tid);
+    } else {
+      csync();
+    }
     return;
   }
 #pragma unroll
@@ -866,7 +907,11 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
 #pragma unroll
     for (int q = 0; q < (int)(TB * CP * sizeof(T) / 16); ++q) dst[q] = srcv[q];
   }
-  csync();
+  if (CF::TEAMSYNC) {
+    team_sync<CF::TEAM>(tid);
+  } else {
+    csync();
+  }
   (void)last;
 }
 
@@ -883,15 +928,31 @@ template <typename T, int C, int MMAX, int MODE, class Emit>
 SPK_DEV void narrow_layer(const LayerDev<T>& L, T* __restrict__ X, T* __restrict__ NBUF, int tid,
                           bool last, T gamma_next, Emit&& emit) {
   using CF = Cfg<T, C, MMAX>;
-  constexpr int CP = CF::CP, NB = CF::NB, KT = CF::KT;
+  constexpr int CP = CF::CP, KT = CF::KT;
   constexpr int LP = narrow_lanes<MMAX>(), IPW = 32 / LP;  // lanes per item, items per warp
+  // team mode: a team reduces and finishes only its own boxes (the X columns
+  // it owns); otherwise the whole CTA shares the tile's boxes
+  constexpr bool TM = CF::TEAMSYNC;
+  constexpr int NW = TM ? CF::TEAM : NT / 32;            // warps sharing the items
   const int warp = tid >> 5, lane = tid & 31, sub = lane / LP, l = lane % LP;
-  const int items = NB * L.m_out;
+  const int team = TM ? warp / CF::TEAM : 0;
+  const int tw = TM ? warp % CF::TEAM : warp;             // warp index within the team
+  const int tl = TM ? tid - team * CF::TEAM * 32 : tid;   // thread index within the team
+  const int b0 = TM ? team * CF::TEAM_BOXES : 0;
+  const int nbox = TM ? CF::TEAM_BOXES : CF::NB;
+  auto sync = [&]() {
+    if (TM) {
+      team_sync<CF::TEAM>(tid);
+    } else {
+      csync();
+    }
+  };
+  const int items = nbox * L.m_out;
   const bool one = L.m_out == 1;
-  for (int it0 = warp * IPW; it0 < items; it0 += (NT / 32) * IPW) {
+  for (int it0 = tw * IPW; it0 < items; it0 += NW * IPW) {
     const int it = it0 + sub;
     const bool live = it < items;
-    const int b = one ? it : it / L.m_out, i = one ? 0 : it % L.m_out;
+    const int b = b0 + (one ? it : it / L.m_out), i = one ? 0 : it % L.m_out;
     const T* wrow = L.w + (size_t)i * L.m_in;
     T p[C];
 #pragma unroll
@@ -923,10 +984,10 @@ SPK_DEV void narrow_layer(const LayerDev<T>& L, T* __restrict__ X, T* __restrict
       for (int c = 0; c < C; ++c) dst[c] = p[c];
     }
   }
-  csync();
+  sync();
   // epilogue
-  for (int it = tid; it < items; it += NT) {
-    const int b = it / L.m_out, i = it % L.m_out;
+  for (int it = tl; it < items; it += NW * 32) {
+    const int b = b0 + it / L.m_out, i = it % L.m_out;
     const T* src = NBUF + ((size_t)b * NARROW_MAX + i) * CP;
     T col[C];
 #pragma unroll
@@ -948,13 +1009,13 @@ SPK_DEV void narrow_layer(const LayerDev<T>& L, T* __restrict__ X, T* __restrict
     }
   }
   if (!last) {
-    // zero the rows a following generic layer reads beyond m_out
+    // zero the rows a following generic layer reads beyond m_out (own columns)
     const int r_end = ((L.m_out + KT - 1) / KT) * KT;
-    const int n = (r_end - L.m_out) * CF::RS;
-    T* base = X + (size_t)L.m_out * CF::RS;
-    for (int q = tid; q < n; q += NT) base[q] = T(0);
+    const int w = nbox * CP;
+    const int n = (r_end - L.m_out) * w;
+    for (int q = tl; q < n; q += NW * 32) X[(size_t)(L.m_out + q / w) * CF::RS + b0 * CP + q % w] = T(0);
   }
-  csync();
+  sync();
 }
 
 // ---------------------------------------------------------------- the pass

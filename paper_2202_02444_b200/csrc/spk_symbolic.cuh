@@ -310,6 +310,7 @@ __global__ void __launch_bounds__(NT, 1)
 
   for (long long tile = blockIdx.x; tile < nbt; tile += gridDim.x) {
     const long long g0 = tile * NB;
+    if (CF::TEAMSYNC) csync();  // the final (team-local) layer of the previous tile is done
     prep_inputs<T, C, MMAX, MODE_AFFINE>(net, in, n, g0, X, tid, true);
     csync();
     int nsym = P.s0;
