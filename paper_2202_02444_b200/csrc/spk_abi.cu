@@ -235,12 +235,14 @@ static int check_policy(int policy, int n_keep, int* mode);
 // launch, *n_dev (when given) is the live count the kernels read.
 int bound_aabb_internal(const spk_net* net, int policy, int n_keep, int precision, long long n_cap,
                         const long long* n_dev, const double* box_lo, const double* box_hi, double* lo, double* hi,
-                        int8_t* cls, cudaStream_t st) {
+                        int8_t* cls, cudaStream_t st, int pair_order) {
   int mode;
   if (int rc = check_policy(policy, n_keep, &mode)) return rc;
   if (net->input_dim > 3) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "AABB path supports d <= 3");
   if (n_cap <= 0) return n_cap < 0 ? fail(SPK_ERR_DIMENSION, "negative batch") : SPK_OK;
   BoxInput in{IN_AABB, net->input_dim, box_lo, box_hi, 0, 0, 0.0, n_dev};
+  // sibling-pair processing order: fused pass only (K3F reads its own inputs)
+  in.pair_order = (pair_order && mode >= 0) ? 1 : 0;
   BoundOutput o{lo, hi, cls};
   if (mode < 0) return launch_symbolic_in(net, -mode, n_keep, precision, in, o, n_cap, net->input_dim, st);
   return run_pass(net, mode, net->input_dim, precision, in, o, n_cap, st);

@@ -54,7 +54,7 @@ int launch_full(const struct ::spk_net* net, int precision, const BoxInput& in, 
                 long long n, int s0, int need, cudaStream_t st);
 int bound_aabb_internal(const struct ::spk_net* net, int policy, int n_keep, int precision, long long n_cap,
                         const long long* n_dev, const double* box_lo, const double* box_hi, double* lo, double* hi,
-                        int8_t* cls, cudaStream_t st);
+                        int8_t* cls, cudaStream_t st, int pair_order = 0);
 int eval_internal(const struct ::spk_net* net, int precision, long long n_cap, const long long* n_dev,
                   const double* xs, double* out, cudaStream_t st);
 

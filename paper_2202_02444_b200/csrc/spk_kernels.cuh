@@ -18,7 +18,15 @@ struct BoxInput {
   unsigned long long seed; // IN_RANDOM
   double half;             // IN_RANDOM: cube half-extent
   const long long* n_dev;  // optional device-side count (<= the launch's n): sync-free loops
+  int pair_order = 0;      // tree levels [low halves; high halves]: slot 2p+c processes node p + c*n/2,
+                           // so a box group holds two sibling boxes (coherent live-row masks)
 };
+
+// Node processed by slot `gb` of a launch over n boxes (identity unless pair_order).
+SPK_DEV long long node_of(const BoxInput& in, long long gb, long long n) {
+  if (!in.pair_order || (n & 1)) return gb;
+  return (gb >> 1) + (gb & 1) * (n >> 1);
+}
 
 struct BoundOutput {
   double* lo;   // bounds (or point values)
@@ -50,7 +58,7 @@ SPK_DEV void prep_inputs(const NetDev<T>& net, const BoxInput& in, long long n, 
   const int rows = ((d + 1) & ~1) < MMAX ? ((d + 1) & ~1) : MMAX;
   for (int q = tid; q < rows * NB; q += NT) {
     const int k = q / NB, b = q % NB;
-    const long long gb = g0 + b;
+    const long long gb = node_of(in, g0 + b, n);
     T packed[CP];
 #pragma unroll
     for (int c = 0; c < CP; ++c) packed[c] = T(0);
@@ -134,6 +142,7 @@ __global__ void __launch_bounds__(NT, (Cfg<T, C, MMAX>::MINB))
   }
   __syncthreads();
   WRing<T, C, MMAX> ring{Wst, full, released, net.wtiles, net.tiles_per_pass, mine * net.tiles_per_pass, 0};
+  if (CF::LIVE) ring.live = reinterpret_cast<uint32_t*>(released + 16);
   ring.prologue(tid);
 
   for (long long tile = blockIdx.x; tile < nbt; tile += gridDim.x) {
@@ -142,7 +151,7 @@ __global__ void __launch_bounds__(NT, (Cfg<T, C, MMAX>::MINB))
     prep_inputs<T, C, MMAX, MODE>(net, in, n, g0, X, tid, true);
     csync();
     auto emit = [&](int b, const State<T, C, MODE>& st) {
-      if (g0 + b < n) emit_bounds<T, C, MODE>(out, g0 + b, st);
+      if (g0 + b < n) emit_bounds<T, C, MODE>(out, node_of(in, g0 + b, n), st);
     };
     run_layers<T, C, MMAX, MODE>(net, X, NBUF, ring, tid, emit);
   }

@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(NT, (Cfg<T, C, MMAX>::MINB))
   }
   __syncthreads();
   WRing<T, C, MMAX> ring{Wst, full, released, net.wtiles, net.tiles_per_pass, mine * net.tiles_per_pass, 0};
+  if (CF::LIVE) ring.live = reinterpret_cast<uint32_t*>(released + 16);
   ring.prologue(tid);
 
   for (long long tile = blockIdx.x; tile < nbt; tile += gridDim.x) {

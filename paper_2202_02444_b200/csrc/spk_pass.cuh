@@ -51,6 +51,9 @@ constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reducti
 #ifndef SPK_UNROLL_BLOCK
 #define SPK_UNROLL_BLOCK 1  // FP32 K loop: each full blocked-summation chunk fully unrolled
 #endif
+#ifndef SPK_LIVE_ROWS
+#define SPK_LIVE_ROWS 1  // skip all-zero X rows (ReLU-inactive neurons) in the FP32 K loop (Cfg::LIVE)
+#endif
 #ifndef SPK_TEAM_SYNC
 #define SPK_TEAM_SYNC 1  // layer boundaries synchronise teams, not the CTA (Cfg::TEAMSYNC)
 #endif
@@ -137,7 +140,17 @@ struct Cfg {
   // + one W row of slack: the K loops prefetch the fragment two rows ahead
   // unconditionally (a predicated prefetch made ptxas copy fragments), so the
   // last step may read one row past the last ring stage (values unused)
-  static constexpr size_t SMEM = sizeof(T) * (size_t)(XS + NS * TILE + NBUF + MMAX) + 2 * 16 * 8 + 64;
+  // Live-row masks: one bit per X row per box group, set by the epilogue when
+  // any of the group's columns for that neuron is nonzero.  A ReLU-inactive
+  // neuron (slope 0) leaves an all-zero row, and FMAs with an exact zero
+  // change neither the round-to-nearest sums nor the round-up error column,
+  // so the K loop may skip those rows with identical results.  FP32 wide nets
+  // (a warp-uniform box group: NG >= 32) with 32-row W tiles (at width 512 the
+  // 16-row tiles measured 10% slower masked on random cubes).
+  static constexpr bool LIVE = SPK_LIVE_ROWS && sizeof(T) == 4 && NG >= 32 && KT == 32 && C >= 2;
+  static constexpr int LW = MMAX / 32;  // mask words per box group
+  static constexpr size_t LIVE_BYTES = LIVE ? (size_t)2 * NBG * LW * 4 : 0;
+  static constexpr size_t SMEM = sizeof(T) * (size_t)(XS + NS * TILE + NBUF + MMAX) + 2 * 16 * 8 + 64 + LIVE_BYTES;
   static_assert(NG >= 1 && NG <= NT && NT % NG == 0, "tile shape");
   static_assert((TB * CP * sizeof(T)) % 16 == 0, "vector loads of X");
   static_assert(TI % G == 0, "W vector groups");
@@ -232,6 +245,7 @@ struct WRing {
   long long next;   // next tile to consume
   int st = 0;        // ring stage of `next` (next % NS, or next % per_pass when resident)
   uint32_t ph = 0;   // mbarrier phase parity of `next` ((next / NS) & 1)
+  uint32_t* live = nullptr;  // live-row masks [2][NBG][LW] (Cfg::LIVE), set by the kernel
 
   SPK_DEV bool resident() const { return per_pass <= CF::NS; }
   SPK_DEV void issue(long long g) const {
@@ -626,7 +640,8 @@ SPK_DEV f32x2 f2_pack(float lo, float hi) {
 // adjacent boxes instead.  Same blocked-summation budget as the scalar loop.
 template <int C, int MMAX, int BIAS2 = -1, bool TEAMS = false>
 SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__ X, WRing<float, C, MMAX>& ring,
-                             int tid, float (&acc)[Cfg<float, C, MMAX>::TI][Cfg<float, C, MMAX>::TB][C]) {
+                             int tid, float (&acc)[Cfg<float, C, MMAX>::TI][Cfg<float, C, MMAX>::TB][C],
+                             const uint32_t* live = nullptr) {
   using CF = Cfg<float, C, MMAX>;
   constexpr int TI = CF::TI, TB = CF::TB, CP = CF::CP, KT = CF::KT;
   constexpr bool POINT = C == 1;
@@ -755,6 +770,39 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
     const float* __restrict__ Xt = X + (size_t)(t * KT) * CF::RS + bg * TB * CP;
     int k_end = L.m_in - t * KT;
     k_end = k_end > KT ? KT : ((k_end + 1) & ~1);
+    if (CF::LIVE && live != nullptr) {
+      // live rows of this tile only (bits past m_in are never set); KT <= 32
+      const uint32_t word = live[(t * KT) >> 5];
+      uint32_t m = KT == 32 ? word : ((word >> ((t * KT) & 31)) & ((1u << (KT & 31)) - 1u));
+      if (since == 0) zero_parts();
+      if (m != 0u) {
+        // an odd count gets one exactly-zero row (one exists: KT is even), so
+        // the loop runs over pairs with the original single-exit shape and
+        // an unconditional prefetch (no fragment register copies)
+        if (__popc(m) & 1) m |= ~m & (m + 1u);
+        const int npairs = __popc(m) >> 1;
+        float w0[TI], w1[TI];
+        f32x2 x0[XQ], x1[XQ];
+        load_frag(Ws, Xt, __ffs(m) - 1, w0, x0);
+        m &= m - 1u;
+#pragma unroll 1
+        for (int p = 0; p < npairs; ++p) {
+          load_frag(Ws, Xt, __ffs(m) - 1, w1, x1);
+          m &= m - 1u;
+          fma_step(w0, x0, F0{});
+          load_frag(Ws, Xt, m ? __ffs(m) - 1 : 0, w0, x0);  // past the last pair: row 0, unused
+          m &= m - 1u;
+          fma_step(w1, x1, F0{});
+        }
+      }
+      since += KT;
+      if (since >= CF::SUB) {
+        flush();
+        since = 0;
+      }
+      ring.release(tid);
+      continue;
+    }
 #pragma unroll 1
     for (int k0 = 0; k0 < k_end; k0 += SUBIN) {
       const int k1 = k0 + SUBIN < k_end ? k0 + SUBIN : k_end;
@@ -814,9 +862,9 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
 // the point value in column 0 and the bound's base in column 1)
 template <typename T, int C, int MMAX, int BIAS2 = -1, bool TEAMS = false>
 SPK_DEV void dense_kloop(const LayerDev<T>& L, const T* __restrict__ X, WRing<T, C, MMAX>& ring, int tid,
-                         T (&acc)[Cfg<T, C, MMAX>::TI][Cfg<T, C, MMAX>::TB][C]) {
+                         T (&acc)[Cfg<T, C, MMAX>::TI][Cfg<T, C, MMAX>::TB][C], const uint32_t* live = nullptr) {
   if constexpr (sizeof(T) == 4 && SPK_PACKED_F32) {
-    dense_kloop_f32<C, MMAX, BIAS2, TEAMS>(L, X, ring, tid, acc);
+    dense_kloop_f32<C, MMAX, BIAS2, TEAMS>(L, X, ring, tid, acc, live);
   } else {
     dense_kloop_scalar<T, C, MMAX, BIAS2, TEAMS>(L, X, ring, tid, acc);
   }
@@ -824,10 +872,22 @@ SPK_DEV void dense_kloop(const LayerDev<T>& L, const T* __restrict__ X, WRing<T,
 
 template <typename T, int C, int MMAX, int MODE>
 SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, MMAX>& ring, int tid,
-                           bool last, T gamma_next) {
+                           bool last, T gamma_next, int lidx) {
   using CF = Cfg<T, C, MMAX>;
   constexpr int TI = CF::TI, TB = CF::TB, CP = CF::CP;
   const int ng = tid % CF::NG, bg = tid / CF::NG;
+  // live-row masks (Cfg::LIVE; bound modes): this layer reads parity lidx&1
+  // (written by the previous epilogue; the first layer reads every row) and
+  // its epilogue fills the other parity, cleared here -- its last reader
+  // (the previous layer's K loop) finished before the previous epilogue
+  constexpr bool LV = CF::LIVE && (MODE == MODE_AFFINE || MODE == MODE_INTERVAL);
+  uint32_t* m_nxt = nullptr;
+  const uint32_t* m_cur = nullptr;
+  if (LV && ring.live != nullptr) {
+    m_nxt = ring.live + (size_t)(((lidx + 1) & 1) * CF::NBG + bg) * CF::LW;
+    if (lidx > 0) m_cur = ring.live + (size_t)((lidx & 1) * CF::NBG + bg) * CF::LW;
+    if (ng < CF::LW) m_nxt[ng] = 0u;
+  }
   // layer parameters the epilogue needs, read before the K loop so their
   // latency hides behind it (dynamically indexed parameter / global reads at
   // the epilogue stalled every warp at once); the common single-ReLU layer
@@ -841,7 +901,7 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
     be_r[ti] = (MODE != MODE_POINT && i < L.m_out) ? L.berr[i] : T(0);
   }
   T acc[TI][TB][C];
-  dense_kloop<T, C, MMAX, (MODE >= MODE_MI ? 1 : -1), CF::TEAMSYNC>(L, X, ring, tid, acc);
+  dense_kloop<T, C, MMAX, (MODE >= MODE_MI ? 1 : -1), CF::TEAMSYNC>(L, X, ring, tid, acc, m_cur);
 
   // epilogue: activation rules, write next X in place (one contiguous
   // TB*CP vector per neuron: the thread's boxes are adjacent in the row)
@@ -882,6 +942,7 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
     }
     return;
   }
+  uint32_t live_bits = 0u;
 #pragma unroll
   for (int ti = 0; ti < TI; ++ti) {
     const int i = CF::neuron(ng, ti);
@@ -906,6 +967,17 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
     const float4* srcv = reinterpret_cast<const float4*>(out);
 #pragma unroll
     for (int q = 0; q < (int)(TB * CP * sizeof(T) / 16); ++q) dst[q] = srcv[q];
+    if (LV) {
+      bool nz = false;
+#pragma unroll
+      for (int c = 0; c < TB * CP; ++c) nz |= out[c] != T(0);
+      live_bits |= (nz ? 1u : 0u) << (ti % CF::G);
+      if (ti % CF::G == CF::G - 1) {  // a group of G consecutive neurons: one word, one atomic
+        const int i0 = i - (CF::G - 1);
+        if (m_nxt != nullptr && live_bits != 0u) atomicOr(&m_nxt[i0 >> 5], live_bits << (i0 & 31));
+        live_bits = 0u;
+      }
+    }
   }
   if (CF::TEAMSYNC) {
     team_sync<CF::TEAM>(tid);
@@ -1031,7 +1103,7 @@ SPK_DEV void run_layers(const NetDev<T>& net, T* X, T* NBUF, WRing<T, C, MMAX>& 
     if (L.narrow) {
       narrow_layer<T, C, MMAX, MODE>(L, X, NBUF, tid, last, L.gamma_next, emit);
     } else {
-      generic_layer<T, C, MMAX, MODE>(L, X, ring, tid, last, L.gamma_next);
+      generic_layer<T, C, MMAX, MODE>(L, X, ring, tid, last, L.gamma_next, l);
     }
   }
 }

@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(NT, 1)
         // final width-1 layer: activations after it only widen the error
         // channel, which leaves lo/hi identical to appending a symbol
         auto emit = [&](int b, const State<T, C, MODE_AFFINE>& st) {
-          if (g0 + b < n) emit_bounds<T, C, MODE_AFFINE>(out, g0 + b, st);
+          if (g0 + b < n) emit_bounds<T, C, MODE_AFFINE>(out, node_of(in, g0 + b, n), st);
         };
         narrow_layer<T, C, MMAX, MODE_AFFINE>(L, X, NBUF, tid, true, T(0), emit);
       } else {

@@ -20,6 +20,10 @@
 #include "spk_kernels.cuh"
 #include "spk_abi_internal.h"
 
+#ifndef SPK_PAIR_ORDER
+#define SPK_PAIR_ORDER 1  // bound tree levels in sibling-pair order (BoxInput::pair_order)
+#endif
+
 namespace spk {
 
 constexpr int TB_THREADS = 256;
@@ -358,8 +362,10 @@ int spk_tree_build_band(const spk_net* net, int policy, int n_keep, int precisio
     bound_ev.push_back(e0);
     bound_ev.push_back(e1);
     cudaEventRecord(e0, st);
+    // levels below the roots are [low children; high children]: bound them in
+    // sibling-pair order (identical results; coherent live-row masks)
     rc = bound_aabb_internal(net, policy, n_keep, precision, cur_cap, n_dev, cur.lo, cur.hi, cur.blo, cur.bhi,
-                             cur.label, st);
+                             cur.label, st, (SPK_PAIR_ORDER && lv > 0) ? 1 : 0);
     cudaEventRecord(e1, st);
     if (rc != SPK_OK) break;
     tree->launches += 4;

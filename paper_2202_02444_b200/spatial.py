@@ -212,7 +212,10 @@ class _TreeHandle:
 
     def __del__(self):
         if self.ptr:
-            _lib.load().spk_tree_destroy(self.ptr)
+            try:
+                _lib.load().spk_tree_destroy(self.ptr)
+            except (AttributeError, TypeError):  # interpreter shutdown: module globals already gone
+                pass
             self.ptr = None
 
 
