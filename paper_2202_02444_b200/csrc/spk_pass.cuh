@@ -152,7 +152,8 @@ struct Cfg {
   // 16-row tiles measured 10% slower masked on random cubes).
   static constexpr bool LIVE = SPK_LIVE_ROWS && sizeof(T) == 4 && NG >= 32 && KT == 32 && C >= 2;
   static constexpr int LW = MMAX / 32;  // mask words per box group
-  static constexpr size_t LIVE_BYTES = LIVE ? (size_t)2 * NBG * LW * 4 : 0;
+  static constexpr int LLIST = 40;  // per-warp live-row list (<= 32 rows + 2 pad entries)
+  static constexpr size_t LIVE_BYTES = LIVE ? (size_t)2 * NBG * LW * 4 + (size_t)(NT / 32) * LLIST * 4 : 0;
   static constexpr size_t SMEM = sizeof(T) * (size_t)(XS + NS * TILE + NBUF + MMAX) + 2 * 16 * 8 + 64 + LIVE_BYTES;
   static_assert(NG >= 1 && NG <= NT && NT % NG == 0, "tile shape");
   static_assert((TB * CP * sizeof(T)) % 16 == 0, "vector loads of X");
@@ -783,23 +784,29 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
     if (CF::LIVE && live != nullptr && __popc(m) <= SPK_LIVE_DENSE) {
       if (since == 0) zero_parts();
       if (m != 0u) {
-        // an odd count gets one exactly-zero row (one exists: KT is even), so
-        // the loop runs over pairs with the original single-exit shape and
-        // an unconditional prefetch (no fragment register copies)
+        // an odd count gets one exactly-zero row (one exists: KT is even); the
+        // warp writes the tile's live rows as a list (lane l holds bit l) and
+        // the loop runs over row pairs read from it (broadcast LDS.64), with
+        // the single-exit shape and unconditional prefetch of the dense loop
         if (__popc(m) & 1) m |= ~m & (m + 1u);
-        const int npairs = __popc(m) >> 1;
+        const int cnt = __popc(m), lane = tid & 31;
+        int* lst = reinterpret_cast<int*>(ring.live + 2 * CF::NBG * CF::LW) + (tid >> 5) * CF::LLIST;
+        __syncwarp();
+        if ((m >> lane) & 1u) lst[__popc(m & ((1u << lane) - 1u))] = lane;
+        if (lane < 2) lst[cnt + lane] = 0;  // prefetch past the last pair reads row 0 (unused)
+        __syncwarp();
         float w0[TI], w1[TI];
         f32x2 x0[XQ], x1[XQ];
-        load_frag(Ws, Xt, __ffs(m) - 1, w0, x0);
-        m &= m - 1u;
+        int2 kk = *reinterpret_cast<const int2*>(lst);
+        load_frag(Ws, Xt, kk.x, w0, x0);
 #pragma unroll 1
-        for (int p = 0; p < npairs; ++p) {
-          load_frag(Ws, Xt, __ffs(m) - 1, w1, x1);
-          m &= m - 1u;
+        for (int p = 0; p < cnt; p += 2) {
+          load_frag(Ws, Xt, kk.y, w1, x1);
+          const int2 nx = *reinterpret_cast<const int2*>(lst + p + 2);
           fma_step(w0, x0, F0{});
-          load_frag(Ws, Xt, m ? __ffs(m) - 1 : 0, w0, x0);  // past the last pair: row 0, unused
-          m &= m - 1u;
+          load_frag(Ws, Xt, nx.x, w0, x0);
           fma_step(w1, x1, F0{});
+          kk = nx;
         }
       }
       since += KT;
