@@ -384,6 +384,10 @@ def run_ours(args, rank, world, local_rank):
                      "kernel": "spk::bound_kernel<float,5,256,AFFINE> (all tree levels)",
                      "flop_per_box": flop_box,
                      "peak_source": "measured FFMA probe (spk_ffma_peak) on this GPU at run time",
+                     "flop_counting": "algorithmic (dense) FLOPs; the kernel skips X rows that are exactly zero "
+                                      "(ReLU-inactive neurons of both boxes of a sibling pair) with identical "
+                                      "results -- it executes ~69% of the dense FMAs on the depth-18 level "
+                                      "(tools/live_rows_estimate.py), so the FFMA pipe itself runs at ~0.69 x frac",
                      "kernel_ms_per_step": kernel_ms / args.steps},
         "e2e": e2e,
         "cpu_baseline": cpu,
