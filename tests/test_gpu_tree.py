@@ -161,3 +161,30 @@ def test_sharded_merge_equals_full(net_paths, roots, world, precision):
             np.testing.assert_array_equal(getattr(g, k), getattr(f, k), err_msg=f"{k} at depth {d}")
         if d:
             np.testing.assert_array_equal(g.parent, f.parent, err_msg=f"parent at depth {d}")
+
+
+@pytest.mark.parametrize("policy", ["affine-fixed", "interval"])
+def test_live_row_skipping_is_exact(policy):
+    """Live-row masks skip all-zero (ReLU-inactive) X rows of a box group.
+    The tree bounds its levels in sibling-pair order (coherent box groups,
+    many rows skipped); bounding the same AABBs in level order pairs
+    unrelated boxes (other rows skipped).  Skipping exact zeros must not
+    change a single bit of the FP32 bounds, and the tree must stay the
+    reference's topology."""
+    import torch
+
+    from paper_2202_02444_b200 import synth
+
+    net = synth.random_mlp(256, 6, "relu", "torch-uniform", seed=5)
+    arr = spatial.build_spatial_tree_arrays(net, BOUNDS, policy=policy, max_depth=12, precision="fp32",
+                                            to_host=True)
+    for d in range(1, arr.n_levels):
+        lv = arr.levels[d]
+        lo, hi, _ = sp.bound_aabb(net, torch.from_numpy(lv.lo).cuda(), torch.from_numpy(lv.hi).cuda(), policy)
+        np.testing.assert_array_equal(lo.cpu().numpy(), lv.bound_lo, err_msg=f"lo at depth {d}")
+        np.testing.assert_array_equal(hi.cpu().numpy(), lv.bound_hi, err_msg=f"hi at depth {d}")
+    # and an odd-sized batch (no pair order possible) through the same kernels
+    lv = arr.levels[-1]
+    m = len(lv) - 1
+    lo, hi, _ = sp.bound_aabb(net, torch.from_numpy(lv.lo[:m]).cuda(), torch.from_numpy(lv.hi[:m]).cuda(), policy)
+    np.testing.assert_array_equal(lo.cpu().numpy(), lv.bound_lo[:m])
