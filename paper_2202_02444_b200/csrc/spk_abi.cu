@@ -13,6 +13,10 @@
 #include "spk_kernels.cuh"
 #include "spk_abi_internal.h"
 
+#ifndef SPK_SPATIAL_ORDER
+#define SPK_SPATIAL_ORDER 1  // Morton order for large batches (spk_order.cu)
+#endif
+
 namespace spk {
 
 thread_local std::string g_last_error;
@@ -223,7 +227,27 @@ int run_pass(const spk_net* cnet, int mode, int S, int precision, const BoxInput
     const NetDev<float>* nd;
     int rc = get_dev<float>(net, &nd);
     if (rc) return rc;
-    e = dispatch_any<float>(net->mmax, mode, S, *nd, in, out, n, sm, st);
+    // large batches of independent boxes on wide nets: Morton processing
+    // order, so box groups hold neighbouring boxes and the live-row masks
+    // skip more ReLU-inactive rows (identical results; spk_order.cu)
+    const bool order = SPK_SPATIAL_ORDER && (mode == MODE_AFFINE || mode == MODE_INTERVAL) && net->mmax >= 256 &&
+                       n >= (1ll << 16) && in.n_dev == nullptr && !in.pair_order && in.perm == nullptr &&
+                       (in.kind == IN_RANDOM || in.kind == IN_BOXES || in.kind == IN_AABB);
+    if (order) {
+      int* perm = nullptr;
+      void* scratch = nullptr;
+      rc = spatial_order(in, net->input_dim, n, sm, st, &perm, &scratch);
+      if (rc) return rc;
+      BoxInput in2 = in;
+      in2.perm = perm;
+      e = dispatch_any<float>(net->mmax, mode, S, *nd, in2, out, n, sm, st);
+      if (scratch) {
+        const cudaError_t ef = cudaFreeAsync(scratch, st);
+        if (e == cudaSuccess) e = ef;
+      }
+    } else {
+      e = dispatch_any<float>(net->mmax, mode, S, *nd, in, out, n, sm, st);
+    }
   }
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return SPK_OK;

@@ -55,6 +55,9 @@ int launch_full(const struct ::spk_net* net, int precision, const BoxInput& in, 
 int bound_aabb_internal(const struct ::spk_net* net, int policy, int n_keep, int precision, long long n_cap,
                         const long long* n_dev, const double* box_lo, const double* box_hi, double* lo, double* hi,
                         int8_t* cls, cudaStream_t st, int pair_order = 0);
+// Morton processing order of a large batch (spk_order.cu); *perm lives in
+// *scratch, released by the caller with cudaFreeAsync after the kernel.
+int spatial_order(const BoxInput& in, int d, long long n, int sm, cudaStream_t st, int** perm, void** scratch);
 int eval_internal(const struct ::spk_net* net, int precision, long long n_cap, const long long* n_dev,
                   const double* xs, double* out, cudaStream_t st);
 

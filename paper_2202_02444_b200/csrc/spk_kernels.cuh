@@ -20,10 +20,14 @@ struct BoxInput {
   const long long* n_dev;  // optional device-side count (<= the launch's n): sync-free loops
   int pair_order = 0;      // tree levels [low halves; high halves]: slot 2p+c processes node p + c*n/2,
                            // so a box group holds two sibling boxes (coherent live-row masks)
+  const int* perm = nullptr;  // optional processing order: slot gb processes box perm[gb] (spk_order.cu)
 };
 
-// Node processed by slot `gb` of a launch over n boxes (identity unless pair_order).
+// Node processed by slot `gb` of a launch over n boxes (identity unless a
+// processing order is given).  Every box's bound is independent of the others,
+// so the order never changes a result.
 SPK_DEV long long node_of(const BoxInput& in, long long gb, long long n) {
+  if (in.perm) return in.perm[gb];
   if (!in.pair_order || (n & 1)) return gb;
   return (gb >> 1) + (gb & 1) * (n >> 1);
 }
