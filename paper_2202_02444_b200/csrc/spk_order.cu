@@ -34,7 +34,9 @@ SPK_DEV double centre_of(const BoxInput& in, long long gb, int k, int d) {
 }
 
 // per-axis min / max of the centres (ordered-integer atomics)
-__global__ void centre_range_kernel(BoxInput in, int d, long long n, unsigned long long* mn, unsigned long long* mx) {
+__global__ void centre_range_kernel(BoxInput in, int d, long long n_cap, unsigned long long* mn,
+                                    unsigned long long* mx) {
+  const long long n = in.n_dev ? (*in.n_dev < n_cap ? *in.n_dev : n_cap) : n_cap;
   unsigned long long lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0ull, 0ull, 0ull};
   for (long long gb = blockIdx.x * (long long)blockDim.x + threadIdx.x; gb < n; gb += (long long)gridDim.x * blockDim.x) {
     for (int k = 0; k < d; ++k) {
@@ -66,15 +68,23 @@ SPK_DEV unsigned int spread3(unsigned int v) {  // 10 bits -> every third bit
   return v;
 }
 
-__global__ void morton_kernel(BoxInput in, int d, long long n, const unsigned long long* mn,
+__global__ void morton_kernel(BoxInput in, int d, long long n_cap, const unsigned long long* mn,
                               const unsigned long long* mx, unsigned int* keys, int* idx) {
+  // slots past a device-side count sort last (key above every 30-bit code)
+  const long long n = in.n_dev ? (*in.n_dev < n_cap ? *in.n_dev : n_cap) : n_cap;
   double lo[3], inv[3];
   for (int k = 0; k < d; ++k) {
     lo[k] = from_ordered(mn[k]);
     const double w = from_ordered(mx[k]) - lo[k];
     inv[k] = w > 0.0 ? 1023.999 / w : 0.0;
   }
-  for (long long gb = blockIdx.x * (long long)blockDim.x + threadIdx.x; gb < n; gb += (long long)gridDim.x * blockDim.x) {
+  for (long long gb = blockIdx.x * (long long)blockDim.x + threadIdx.x; gb < n_cap;
+       gb += (long long)gridDim.x * blockDim.x) {
+    if (gb >= n) {
+      keys[gb] = 0xFFFFFFFFu;
+      idx[gb] = (int)gb;
+      continue;
+    }
     unsigned int key = 0u;
     for (int k = 0; k < d; ++k) {
       double q = (centre_of(in, gb, k, d) - lo[k]) * inv[k];
@@ -88,15 +98,16 @@ __global__ void morton_kernel(BoxInput in, int d, long long n, const unsigned lo
 
 }  // namespace
 
-// Morton processing order of a batch (n < 2^31).  *perm points into *scratch,
-// which the caller releases with cudaFreeAsync on `st` after the kernel.
+// Morton processing order of a batch of n (capacity; in.n_dev, when given, is
+// the live count: the other slots sort last) boxes, n < 2^31.  *perm points
+// into *scratch, which the caller releases with cudaFreeAsync on `st`.
 int spatial_order(const BoxInput& in, int d, long long n, int sm, cudaStream_t st, int** perm, void** scratch) {
   *perm = nullptr;
   *scratch = nullptr;
   if (n <= 0 || n >= (1ll << 31) || d < 1 || d > 3) return SPK_OK;
   size_t tmp_bytes = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, (unsigned int*)nullptr, (unsigned int*)nullptr,
-                                  (int*)nullptr, (int*)nullptr, (int)n, 0, 30, st);
+                                  (int*)nullptr, (int*)nullptr, (int)n, 0, 32, st);
   const size_t nb = (size_t)n;
   const size_t bytes = 64 + 2 * nb * 4 + 2 * nb * 4 + tmp_bytes + 256;
   char* base = nullptr;
@@ -115,7 +126,7 @@ int spatial_order(const BoxInput& in, int d, long long n, int sm, cudaStream_t s
   const int grid = (int)std::min<long long>((n + 255) / 256, (long long)(sm > 0 ? sm : 148) * 8);
   centre_range_kernel<<<grid, 256, 0, st>>>(in, d, n, mn, mx);
   morton_kernel<<<grid, 256, 0, st>>>(in, d, n, mn, mx, k0, i0);
-  e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, i0, i1, (int)n, 0, 30, st);
+  e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, i0, i1, (int)n, 0, 32, st);
   if (e != cudaSuccess) return cuda_fail(e, "spatial order sort");
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "spatial order kernels");

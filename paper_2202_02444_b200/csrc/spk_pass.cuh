@@ -60,6 +60,9 @@ constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reducti
 #ifndef SPK_TEAM_SYNC
 #define SPK_TEAM_SYNC 1  // layer boundaries synchronise teams, not the CTA (Cfg::TEAMSYNC)
 #endif
+#ifndef SPK_TEAM_MIN_NS
+#define SPK_TEAM_MIN_NS 4  // ring depth from which layer boundaries are team-local
+#endif
 #ifndef SPK_PACKED_F32
 #define SPK_PACKED_F32 1  // FP32 K loop on FFMA2 (sm_100a packed f32x2)
 #endif
@@ -173,7 +176,7 @@ struct Cfg {
   // absorb the teams' drift (measured: +4-5% with >= 4 stages; with the
   // 3-stage ring of 8x256 affine tiles a leading team stalls on refills that
   // wait for the slowest one, -3%), so shallow rings keep the CTA barrier.
-  static constexpr bool TEAMSYNC = SPK_TEAM_SYNC && NS >= 4;
+  static constexpr bool TEAMSYNC = SPK_TEAM_SYNC && NS >= SPK_TEAM_MIN_NS;
 };
 
 // copy N bytes (N in {4, 8, 16}) between 16/8/4-aligned addresses as one access
