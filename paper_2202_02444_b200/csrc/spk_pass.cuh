@@ -900,10 +900,13 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
   constexpr bool LV = CF::LIVE && (MODE == MODE_AFFINE || MODE == MODE_INTERVAL);
   uint32_t* m_nxt = nullptr;
   const uint32_t* m_cur = nullptr;
+  // one warp per box group holding 4-neuron groups at 4*lane (NG == 32, G == 4):
+  // the masks are assembled with shuffles and stored whole, no clearing/atomics
+  constexpr bool WMASK = LV && CF::NG == 32 && CF::G == 4;
   if (LV && ring.live != nullptr) {
     m_nxt = ring.live + (size_t)(((lidx + 1) & 1) * CF::NBG + bg) * CF::LW;
     if (lidx > 0) m_cur = ring.live + (size_t)((lidx & 1) * CF::NBG + bg) * CF::LW;
-    if (ng < CF::LW) m_nxt[ng] = 0u;
+    if (!WMASK && ng < CF::LW) m_nxt[ng] = 0u;
   }
   // layer parameters the epilogue needs, read before the K loop so their
   // latency hides behind it (dynamically indexed parameter / global reads at
@@ -991,7 +994,17 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
       live_bits |= (nz ? 1u : 0u) << (ti % CF::G);
       if (ti % CF::G == CF::G - 1) {  // a group of G consecutive neurons: one word, one atomic
         const int i0 = i - (CF::G - 1);
-        if (m_nxt != nullptr && live_bits != 0u) atomicOr(&m_nxt[i0 >> 5], live_bits << (i0 & 31));
+        if (WMASK) {
+          // the warp owns every neuron of its box group: OR the nibbles of the
+          // 8 lanes sharing a 32-bit word with shuffles, one plain store each
+          uint32_t v = live_bits << (i0 & 31);
+          v |= __shfl_xor_sync(0xffffffffu, v, 1);
+          v |= __shfl_xor_sync(0xffffffffu, v, 2);
+          v |= __shfl_xor_sync(0xffffffffu, v, 4);
+          if (m_nxt != nullptr && (ng & 7) == 0) m_nxt[i0 >> 5] = v;
+        } else if (m_nxt != nullptr && live_bits != 0u) {
+          atomicOr(&m_nxt[i0 >> 5], live_bits << (i0 & 31));
+        }
         live_bits = 0u;
       }
     }
