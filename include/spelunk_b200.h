@@ -98,6 +98,12 @@ int spk_ffma_peak(int iters, double* flops_per_s, void* stream);
 int spk_net_create(int input_dim, int n_ops, const int* op_kind, const int* op_out_dim,
                    const double* params, int64_t n_params, int device, spk_net** out);
 int spk_net_destroy(spk_net* net);
+/* TEST HOOK, not for production: on != 0 makes every ReLU of this net use an
+ * affine rule with a negated remainder (gamma -> -gamma), so bounds stop
+ * enclosing the range; the soundness fuzz must detect it.  Mirrors the
+ * reference's mutation test (tests/test_cli.py:150-164, monkeypatching
+ * range_core.AFFINE_RULES).  Point values and interval images stay exact. */
+int spk_net_debug_corrupt_relu(spk_net* net, int on);
 /* widest layer, number of dense layers, and sum_l m_in*m_out (FLOP model) */
 int spk_net_info(const spk_net* net, int* max_width, int* n_dense, int64_t* macs);
 

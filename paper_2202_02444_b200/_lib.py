@@ -52,6 +52,7 @@ SIGNATURES = {
     "spk_net_create": ([i32, i32, vp, vp, vp, i64, i32, vp], i32),
     "spk_net_destroy": ([vp], i32),
     "spk_net_info": ([vp, vp, vp, vp], i32),
+    "spk_net_debug_corrupt_relu": ([vp, i32], i32),
     "spk_bound_batch": ([vp, i32, i32, i32, i64, i32, vp, vp, vp, vp, vp, vp], i32),
     "spk_bound_aabb": ([vp, i32, i32, i32, i64, vp, vp, vp, vp, vp, vp], i32),
     "spk_bound_random_cubes": ([vp, i32, i32, i32, i64, i64, u64, f64, vp, vp, vp, vp], i32),

@@ -83,6 +83,20 @@ static T round_up_to(double x) {
   return t;
 }
 
+// Activation code as the kernels see it (the test hook swaps ReLU for the
+// rule with a negated remainder).
+static int act_code(const spk_net* net, int act) {
+  return (net->corrupt_relu && act == ACT_RELU) ? (int)ACT_RELU_BROKEN : act;
+}
+
+template <typename T>
+static void recode_acts(spk_net* net, DevNet<T>& dn) {
+  if (!dn.ready) return;
+  for (int i = 0; i < dn.nd.n_pre; ++i) dn.nd.pre_act[i] = act_code(net, net->pre_acts[i]);
+  for (size_t l = 0; l < net->layers.size(); ++l)
+    for (int a = 0; a < dn.nd.L[l].n_act; ++a) dn.nd.L[l].act[a] = act_code(net, net->layers[l].acts[a]);
+}
+
 // Build the device program for one precision (lazily, once per net).
 template <typename T>
 int build_device_net(spk_net* net, DevNet<T>& dn) {
@@ -94,7 +108,7 @@ int build_device_net(spk_net* net, DevNet<T>& dn) {
   std::memset(&nd, 0, sizeof(nd));
   nd.d = net->input_dim;
   nd.n_pre = (int)net->pre_acts.size();
-  for (int i = 0; i < nd.n_pre; ++i) nd.pre_act[i] = net->pre_acts[i];
+  for (int i = 0; i < nd.n_pre; ++i) nd.pre_act[i] = act_code(net, net->pre_acts[i]);
   nd.n_layers = (int)net->layers.size();
 
   std::vector<T> tiles;
@@ -171,7 +185,7 @@ int build_device_net(spk_net* net, DevNet<T>& dn) {
     D.narrow = (l + 1 == net->layers.size()) && L.m_out <= NARROW_MAX;
     D.ntiles = D.narrow ? 0 : (L.m_in + KT - 1) / KT;
     D.n_act = (int)L.acts.size();
-    for (int a = 0; a < D.n_act; ++a) D.act[a] = L.acts[a];
+    for (int a = 0; a < D.n_act; ++a) D.act[a] = act_code(net, L.acts[a]);
     D.w = D.narrow ? d_small + offs[l].w : nullptr;
     D.bias = d_small + offs[l].b;
     D.berr = d_small + offs[l].be;
@@ -371,6 +385,15 @@ int spk_net_destroy(spk_net* net) {
     if (net->f64.ready) { cudaFree(net->f64.tiles); cudaFree(net->f64.small); }
   }
   delete net;
+  return SPK_OK;
+}
+
+int spk_net_debug_corrupt_relu(spk_net* net, int on) {
+  if (!net) return fail(SPK_ERR_INVALID_PARAMETER, "null net");
+  std::lock_guard<std::mutex> lk(net->mu);
+  net->corrupt_relu = on ? 1 : 0;
+  recode_acts<float>(net, net->f32);
+  recode_acts<double>(net, net->f64);
   return SPK_OK;
 }
 

@@ -73,6 +73,7 @@ struct spk_net {
   int mmax = 0;
   int max_width = 0;
   int64_t macs = 0;
+  int corrupt_relu = 0;  // test hook (spk_net_debug_corrupt_relu)
   std::vector<int> pre_acts;
   std::vector<spk::HostLayer> layers;
   std::mutex mu;

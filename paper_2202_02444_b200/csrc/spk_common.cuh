@@ -18,6 +18,10 @@ enum Act : int {
   ACT_SIN = SPK_OP_SIN,
   ACT_TANH = SPK_OP_TANH,
   ACT_IDENTITY = SPK_OP_IDENTITY,
+  // test hook only (spk_net_debug_corrupt_relu): ReLU whose affine remainder
+  // is negated -- the reference's mutation test (test_cli.py:150-164); point
+  // values and interval images stay ReLU's
+  ACT_RELU_BROKEN = 1000,
 };
 
 // Directed-rounding arithmetic.  Every error-channel update is an upper

@@ -164,6 +164,11 @@ template <typename T>
 SPK_DEV int affine_rule(int act, T lo, T hi, T& alpha, T& beta, T& gamma) {
   switch (act) {
     case ACT_RELU: return relu_affine<T>(lo, hi, alpha, beta, gamma);
+    case ACT_RELU_BROKEN: {
+      const int k = relu_affine<T>(lo, hi, alpha, beta, gamma);
+      gamma = -gamma;
+      return k;
+    }
     case ACT_ELU: return elu_affine<T>(lo, hi, alpha, beta, gamma);
     case ACT_SIN: return sin_affine<T>(lo, hi, alpha, beta, gamma);
     case ACT_TANH: return tanh_affine<T>(lo, hi, alpha, beta, gamma);
@@ -197,7 +202,7 @@ SPK_DEV bool sin_image_f32(float lo, float hi, float& out_lo, float& out_hi) {
 
 template <typename T>
 SPK_DEV void interval_image(int act, T lo, T hi, T& out_lo, T& out_hi) {
-  if (act == ACT_RELU) {
+  if (act == ACT_RELU || act == ACT_RELU_BROKEN) {
     out_lo = fmax(lo, T(0));
     out_hi = fmax(hi, T(0));
     return;
@@ -246,6 +251,7 @@ SPK_RULE void interval_image_slow(int act, T lo, T hi, T& out_lo, T& out_hi) {
 template <typename T>
 SPK_RULE T act_value_slow(int act, T x) {  // float / double overloads of the CUDA math library
   switch (act) {
+    case ACT_RELU_BROKEN: return fmax(x, T(0));
     case ACT_ELU: return x >= T(0) ? x : expm1(x);
     case ACT_SIN: return sin(x);
     case ACT_TANH: return tanh(x);
@@ -256,6 +262,7 @@ SPK_RULE T act_value_slow(int act, T x) {  // float / double overloads of the CU
 template <typename T>
 SPK_DEV T act_value_inline(int act, T x) {
   switch (act) {
+    case ACT_RELU_BROKEN: return fmax(x, T(0));
     case ACT_ELU: return x >= T(0) ? x : expm1(x);
     case ACT_SIN: return sin(x);
     case ACT_TANH: return tanh(x);
@@ -264,7 +271,7 @@ SPK_DEV T act_value_inline(int act, T x) {
 }
 template <typename T>
 SPK_DEV T act_value(int act, T x) {
-  if (act == ACT_RELU) return fmax(x, T(0));
+  if (act == ACT_RELU || act == ACT_RELU_BROKEN) return fmax(x, T(0));
   return act_value_slow<T>(act, x);
 }
 

@@ -55,3 +55,28 @@ def test_million_region_fuzz(net_paths, netname):
             assert n_bad == 0, (netname, pol, n_bad)
             checks += chunk
     assert checks == N_REGIONS * len(policies)
+
+
+def test_corrupted_rule_detected(net_paths):
+    """Mutation test (reference test_cli.py:150-164): with the ReLU affine
+    remainder negated the bounds stop enclosing the range and the reference
+    fuzz harness (fuzz_soundness, FP32 production kernels) must report
+    violations; restored, the same regions pass.  A private copy of the net
+    carries the corrupted device program."""
+    import copy
+
+    from paper_2202_02444_b200.network import device_net
+
+    net = copy.deepcopy(sp.load_network(net_paths["box"]))
+    dn = device_net(net)
+    dn.debug_corrupt_relu(True)
+    try:
+        report = sp.fuzz_soundness([net], n_regions=3000, rng_seed=0, policies=[sp.AFFINE_FIXED])
+        assert not report.ok
+        assert report.violations
+        first = report.violations[0]
+        assert first.value < first.lo or first.value > first.hi
+    finally:
+        dn.debug_corrupt_relu(False)
+    report = sp.fuzz_soundness([net], n_regions=3000, rng_seed=0, policies=[sp.AFFINE_FIXED])
+    assert report.ok and report.n_violations == 0
