@@ -13,6 +13,9 @@
 #include "spk_kernels.cuh"
 #include "spk_abi_internal.h"
 
+#ifndef SPK_SPREAD_SMALL
+#define SPK_SPREAD_SMALL 1  // small FP32 batches on wide nets: one box group per SM sub-partition
+#endif
 #ifndef SPK_SPATIAL_ORDER
 #define SPK_SPATIAL_ORDER 1  // Morton order for large batches (spk_order.cu)
 #endif
@@ -249,7 +252,17 @@ int run_pass(const spk_net* cnet, int mode, int S, int precision, const BoxInput
     const bool order = SPK_SPATIAL_ORDER && (mode == MODE_AFFINE || mode == MODE_INTERVAL) && net->mmax >= 256 &&
                        n >= (1ll << 16) && in.n_dev == nullptr && !in.pair_order && in.perm == nullptr &&
                        (in.kind == IN_RANDOM || in.kind == IN_BOXES || in.kind == IN_AABB);
-    if (order) {
+    // small batches (fewer boxes than 8 per SM, e.g. the top tree levels) are
+    // spread over every SM, one box group per SM sub-partition first
+    // (spread_node); empty groups skip their K loops through the live-row masks
+    const bool spread = SPK_SPREAD_SMALL && (mode == MODE_AFFINE || mode == MODE_INTERVAL) && net->mmax >= 256 &&
+                        n <= (long long)sm * 8 && in.perm == nullptr;
+    if (spread) {
+      BoxInput in2 = in;
+      in2.spread = 1;
+      in2.spread_n = n;
+      e = dispatch_any<float>(net->mmax, mode, S, *nd, in2, out, n, sm, st);
+    } else if (order) {
       int* perm = nullptr;
       void* scratch = nullptr;
       rc = spatial_order(in, net->input_dim, n, sm, st, &perm, &scratch);

@@ -21,15 +21,40 @@ struct BoxInput {
   int pair_order = 0;      // tree levels [low halves; high halves]: slot 2p+c processes node p + c*n/2,
                            // so a box group holds two sibling boxes (coherent live-row masks)
   const int* perm = nullptr;  // optional processing order: slot gb processes box perm[gb] (spk_order.cu)
+  int spread = 0;             // small batch spread over every SM (see spread_node)
+  long long spread_n = 0;     // spread: host-side box count (capacity when n_dev is given)
 };
 
 // Node processed by slot `gb` of a launch over n boxes (identity unless a
 // processing order is given).  Every box's bound is independent of the others,
 // so the order never changes a result.
 SPK_DEV long long node_of(const BoxInput& in, long long gb, long long n) {
+  if (gb >= n) return -1;
   if (in.perm) return in.perm[gb];
   if (!in.pair_order || (n & 1)) return gb;
   return (gb >> 1) + (gb & 1) * (n >> 1);
+}
+
+// Spread mode (a batch with fewer box groups than the grid has): the kernel
+// runs one tile per CTA over grid x NB slots and box group p (TB boxes) goes
+// to CTA p mod grid, group slot p / grid -- the first groups land on warp 0 of
+// every CTA, i.e. one SM sub-partition each, instead of filling a few CTAs.
+// Empty slots return -1 (their groups skip the K loops through the live-row
+// masks).  Boxes of a group: siblings (p, p + n/2) under pair_order, else
+// p*TB + c.
+template <int TB, int NBG>
+SPK_DEV long long spread_node(const BoxInput& in, long long slot, long long n, int grid) {
+  constexpr int NB = TB * NBG;
+  const long long cta = slot / NB;
+  const int r = (int)(slot % NB), grp = r / TB, c = r % TB;
+  const long long p = (long long)grp * grid + cta;
+  long long node;
+  if (in.pair_order && TB == 2 && !(n & 1)) {
+    node = p < (n >> 1) ? p + c * (n >> 1) : -1;
+  } else {
+    node = p * TB + c;
+  }
+  return (node >= 0 && node < n) ? node : -1;
 }
 
 struct BoundOutput {
@@ -62,11 +87,12 @@ SPK_DEV void prep_inputs(const NetDev<T>& net, const BoxInput& in, long long n, 
   const int rows = ((d + 1) & ~1) < MMAX ? ((d + 1) & ~1) : MMAX;
   for (int q = tid; q < rows * NB; q += NT) {
     const int k = q / NB, b = q % NB;
-    const long long gb = node_of(in, g0 + b, n);
+    const long long gb = in.spread ? spread_node<CF::TB, CF::NBG>(in, g0 + b, n, (int)gridDim.x)
+                                   : node_of(in, g0 + b, n);
     T packed[CP];
 #pragma unroll
     for (int c = 0; c < CP; ++c) packed[c] = T(0);
-    if (k < d && gb < n) {
+    if (k < d && gb >= 0) {
       State<T, C, MODE> st;
       double centre;
       double ax[3] = {0.0, 0.0, 0.0};
@@ -125,7 +151,8 @@ template <typename T, int C, int MMAX, int MODE>
 __global__ void __launch_bounds__(NT, (Cfg<T, C, MMAX>::MINB))
     bound_kernel(const NetDev<T> net, const BoxInput in, const BoundOutput out, const long long n_cap) {
   using CF = Cfg<T, C, MMAX>;
-  const long long n = in.n_dev ? *in.n_dev : n_cap;
+  // real box count; spread mode runs over grid x NB slots
+  const long long n = in.n_dev ? *in.n_dev : (in.spread ? in.spread_n : n_cap);
   constexpr int NB = CF::NB;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* X = reinterpret_cast<T*>(smem_raw);
@@ -134,7 +161,8 @@ __global__ void __launch_bounds__(NT, (Cfg<T, C, MMAX>::MINB))
   uint64_t* full = reinterpret_cast<uint64_t*>(NBUF + CF::NBUF);
   const int tid = threadIdx.x;
 
-  const long long nbt = (n + NB - 1) / NB;
+  const long long n_slots = in.spread ? (long long)gridDim.x * NB : n;
+  const long long nbt = (n_slots + NB - 1) / NB;
   const long long mine = blockIdx.x < nbt ? (nbt - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   unsigned* released = reinterpret_cast<unsigned*>(full + 16);
   if (tid == 0) {
@@ -153,9 +181,15 @@ __global__ void __launch_bounds__(NT, (Cfg<T, C, MMAX>::MINB))
     const long long g0 = tile * NB;
     if (CF::TEAMSYNC) csync();  // every team is done with the previous tile's X
     prep_inputs<T, C, MMAX, MODE>(net, in, n, g0, X, tid, true);
+    auto node = [&](int b) -> long long {
+      return in.spread ? spread_node<CF::TB, CF::NBG>(in, g0 + b, n, (int)gridDim.x) : node_of(in, g0 + b, n);
+    };
+    // a box group without boxes (spread padding, the tail tile) marks no live rows
+    if (CF::LIVE) ring.group_empty = node((tid / CF::NG) * CF::TB) < 0;
     csync();
     auto emit = [&](int b, const State<T, C, MODE>& st) {
-      if (g0 + b < n) emit_bounds<T, C, MODE>(out, node_of(in, g0 + b, n), st);
+      const long long nd = node(b);
+      if (nd >= 0) emit_bounds<T, C, MODE>(out, nd, st);
     };
     run_layers<T, C, MMAX, MODE>(net, X, NBUF, ring, tid, emit);
   }
@@ -176,7 +210,7 @@ cudaError_t launch_bound(const NetDev<T>& net, const BoxInput& in, const BoundOu
   if (n <= 0) return cudaSuccess;
   const long long nbt = (n + CF::NB - 1) / CF::NB;
   const long long slots = (long long)sm_count * CF::MINB;
-  const int grid = (int)(nbt < slots ? nbt : slots);
+  const int grid = in.spread ? sm_count : (int)(nbt < slots ? nbt : slots);
   kfn<<<grid, NT, CF::SMEM, stream>>>(net, in, out, n);
   return cudaGetLastError();
 }

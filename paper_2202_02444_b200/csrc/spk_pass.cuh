@@ -253,6 +253,7 @@ struct WRing {
   int st = 0;        // ring stage of `next` (next % NS, or next % per_pass when resident)
   uint32_t ph = 0;   // mbarrier phase parity of `next` ((next / NS) & 1)
   uint32_t* live = nullptr;  // live-row masks [2][NBG][LW] (Cfg::LIVE), set by the kernel
+  bool group_empty = false;  // this thread's box group holds no box in the current tile
 
   SPK_DEV bool resident() const { return per_pass <= CF::NS; }
   SPK_DEV void issue(long long g) const {
@@ -991,6 +992,7 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
       bool nz = false;
 #pragma unroll
       for (int c = 0; c < TB * CP; ++c) nz |= out[c] != T(0);
+      nz = nz && !ring.group_empty;
       live_bits |= (nz ? 1u : 0u) << (ti % CF::G);
       if (ti % CF::G == CF::G - 1) {  // a group of G consecutive neurons: one word, one atomic
         const int i0 = i - (CF::G - 1);
