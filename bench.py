@@ -551,6 +551,7 @@ def bench_e2e_tree(torch, sp, spatial, net, bounds, args):
     arr = spatial.build_spatial_tree_arrays(net, bounds, policy=sp.AFFINE_FIXED, max_depth=DEPTH, to_host=True)
     ts = []
     for _ in range(max(1, min(args.steps, 3))):
+        del arr  # the previous result is released outside the timed call
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         arr = spatial.build_spatial_tree_arrays(net, bounds, policy=sp.AFFINE_FIXED, max_depth=DEPTH, to_host=True)

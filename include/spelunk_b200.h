@@ -162,6 +162,14 @@ int spk_tree_build(const spk_net* net, int policy, int n_keep, int precision, in
 int spk_tree_build_band(const spk_net* net, int policy, int n_keep, int precision, int64_t n_roots,
                         const double* root_lo, const double* root_hi, int start_depth, int max_depth,
                         double delta, double band, void* stream, spk_tree** out);
+/* spk_tree_build_band with flags: SPK_TREE_HOST_MIRROR also copies every
+ * level to host memory while the next level computes (a second stream; the
+ * copies overlap the build), readable with spk_tree_level_host -- the
+ * to_host=True path of build_spatial_tree_arrays. */
+#define SPK_TREE_HOST_MIRROR 1
+int spk_tree_build_ex(const spk_net* net, int policy, int n_keep, int precision, int64_t n_roots,
+                      const double* root_lo, const double* root_hi, int start_depth, int max_depth,
+                      double delta, double band, int flags, void* stream, spk_tree** out);
 int spk_tree_destroy(spk_tree* tree);
 int spk_tree_info(const spk_tree* tree, int* n_levels, int64_t* n_nodes, int64_t* bound_evals);
 /* copy one level into caller buffers (host or device, any may be NULL) */
@@ -172,6 +180,14 @@ int spk_tree_stats(const spk_tree* tree, int64_t* launches, double* bound_ms);
 /* device pointers of one level (valid until spk_tree_destroy): AABB corners
  * (n x d), the bound, the sign label (+1/-1/0), the face-sign annotation
  * (+1/-1, 0 = none) and the parent index into the previous level (-1). */
+/* host pointers of one level of a SPK_TREE_HOST_MIRROR build (same arrays
+ * as spk_tree_level, valid until spk_tree_destroy) */
+int spk_tree_level_host(const spk_tree* tree, int level, int64_t* n, const double** lo, const double** hi,
+                        const double** bound_lo, const double** bound_hi, const int8_t** label,
+                        const int8_t** face, const int64_t** parent);
+/* free the device levels of a SPK_TREE_HOST_MIRROR build (the host mirror
+ * and the level sizes stay; spk_tree_level then only reports sizes) */
+int spk_tree_release_device(spk_tree* tree);
 int spk_tree_level(const spk_tree* tree, int level, int64_t* n, const double** lo, const double** hi,
                    const double** bound_lo, const double** bound_hi, const int8_t** label,
                    const int8_t** face, const int64_t** parent);

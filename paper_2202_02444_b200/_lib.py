@@ -60,6 +60,9 @@ SIGNATURES = {
     "spk_bound_batch_host": ([vp, i32, i32, i32, i64, i32, vp, vp, vp, vp, vp], i32),
     "spk_tree_build": ([vp, i32, i32, i32, i64, vp, vp, i32, i32, f64, vp, vp], i32),
     "spk_tree_build_band": ([vp, i32, i32, i32, i64, vp, vp, i32, i32, f64, f64, vp, vp], i32),
+    "spk_tree_build_ex": ([vp, i32, i32, i32, i64, vp, vp, i32, i32, f64, f64, i32, vp, vp], i32),
+    "spk_tree_level_host": ([vp, i32, vp, vp, vp, vp, vp, vp, vp, vp], i32),
+    "spk_tree_release_device": ([vp], i32),
     "spk_tree_stats": ([vp, vp, vp], i32),
     "spk_tree_level_copy": ([vp, i32, vp, vp, vp, vp, vp, vp, vp], i32),
     "spk_march": ([vp, i32, i32, i32, i64, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp], i32),

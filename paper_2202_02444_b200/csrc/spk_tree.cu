@@ -18,6 +18,8 @@
 #include <vector>
 
 #include "spk_kernels.cuh"
+#include <cstdlib>
+
 #include "spk_abi_internal.h"
 
 #ifndef SPK_PAIR_ORDER
@@ -219,6 +221,11 @@ struct spk_tree {
   cudaStream_t stream = nullptr;  // frees are ordered on the build stream
   long long launches = 0;   // kernels launched by the build
   double bound_ms = 0.0;    // CUDA-event time of the bound kernels
+  // host mirror (SPK_TREE_HOST_MIRROR): per level one malloc block holding
+  // lo, hi (n x d), bound_lo, bound_hi, label, face, parent back to back
+  std::vector<char*> host;
+  std::vector<long long> host_n;
+  bool device_released = false;  // spk_tree_release_device: only the host mirror remains
 };
 
 namespace spk {
@@ -277,6 +284,48 @@ void keep_pool_memory(int device) {
   done[device] = 1;
 }
 
+// Copy level `lv` of the build into host memory on the copy stream `cst`
+// once the compute stream has passed event `done`: the host thread blocks on
+// the (pageable) copy while the GPU already runs the next level's kernels.
+static int mirror_level(spk_tree* tree, int lv, const TreeLevel& L, const long long* d_count, cudaEvent_t done,
+                        cudaStream_t cst) {
+  cudaStreamWaitEvent(cst, done, 0);
+  long long n = 0;
+  cudaError_t e = cudaMemcpyAsync(&n, d_count, sizeof(long long), cudaMemcpyDeviceToHost, cst);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cst);
+  if (e != cudaSuccess) return cuda_fail(e, "tree mirror count");
+  const size_t d = (size_t)tree->d, m = (size_t)n;
+  const size_t sz[7] = {m * d * 8, m * d * 8, m * 8, m * 8, m, m, m * 8};
+  size_t total = 0;
+  for (size_t b : sz) total += b;
+  char* h = static_cast<char*>(std::malloc(std::max<size_t>(total, 1)));
+  if (!h) return fail(SPK_ERR_OUT_OF_MEMORY, "tree host mirror");
+  const void* src[7] = {L.lo, L.hi, L.blo, L.bhi, L.label, L.face, L.parent};
+  size_t off = 0;
+  for (int q = 0; q < 7; ++q) {
+    if (sz[q] && (e = cudaMemcpyAsync(h + off, src[q], sz[q], cudaMemcpyDeviceToHost, cst)) != cudaSuccess) break;
+    off += sz[q];
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cst);
+  if (e != cudaSuccess) {
+    std::free(h);
+    return cuda_fail(e, "tree mirror copy");
+  }
+  if ((int)tree->host.size() <= lv) {
+    tree->host.resize(lv + 1, nullptr);
+    tree->host_n.resize(lv + 1, 0);
+  }
+  tree->host[lv] = h;
+  tree->host_n[lv] = n;
+  return SPK_OK;
+}
+
+static void free_mirror(spk_tree* tree) {
+  for (char* h : tree->host) std::free(h);
+  tree->host.clear();
+  tree->host_n.clear();
+}
+
 }  // namespace spk
 
 using namespace spk;
@@ -293,6 +342,13 @@ int spk_tree_build(const spk_net* net, int policy, int n_keep, int precision, in
 int spk_tree_build_band(const spk_net* net, int policy, int n_keep, int precision, int64_t n_roots,
                         const double* root_lo, const double* root_hi, int start_depth, int max_depth,
                         double delta, double band, void* stream, spk_tree** out) {
+  return spk_tree_build_ex(net, policy, n_keep, precision, n_roots, root_lo, root_hi, start_depth, max_depth,
+                           delta, band, 0, stream, out);
+}
+
+int spk_tree_build_ex(const spk_net* net, int policy, int n_keep, int precision, int64_t n_roots,
+                      const double* root_lo, const double* root_hi, int start_depth, int max_depth,
+                      double delta, double band, int flags, void* stream, spk_tree** out) {
   if (!net || !out) return fail(SPK_ERR_INVALID_PARAMETER, "null argument");
   if (!(band >= 0.0)) return fail(SPK_ERR_INVALID_PARAMETER, "band must be >= 0");
   *out = nullptr;
@@ -351,6 +407,13 @@ int spk_tree_build_band(const spk_net* net, int policy, int n_keep, int precisio
   long long cap = 0, fcap = 0;
   std::vector<long long> caps;
   long long cur_cap = n_roots;  // capacity bound of the current level
+  const bool mirror = (flags & SPK_TREE_HOST_MIRROR) != 0;
+  cudaStream_t cst = nullptr;   // mirror copies
+  std::vector<cudaEvent_t> level_done;
+  if (mirror && cudaStreamCreateWithFlags(&cst, cudaStreamNonBlocking) != cudaSuccess) {
+    delete tree;
+    return fail(SPK_ERR_CUDA, "tree mirror stream");
+  }
   for (int depth = start_depth, lv = 0; rc == SPK_OK; ++depth, ++lv) {
     if (lv >= kMaxLevels) { rc = fail(SPK_ERR_DEPTH_OVERFLOW, "more than 64 tree levels"); break; }
     long long* n_dev = d_cnt + lv;
@@ -430,11 +493,28 @@ int spk_tree_build_band(const spk_net* net, int policy, int n_keep, int precisio
     caps.push_back(cur_cap);
     tree->levels.push_back(cur);
     cur = TreeLevel();
+    if (mirror) {
+      // this level is final once its kernels ran; copy the PREVIOUS level
+      // now, while the GPU works on this one
+      cudaEvent_t ev;
+      cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      cudaEventRecord(ev, st);
+      level_done.push_back(ev);
+      if (lv >= 1 && (rc = mirror_level(tree, lv - 1, tree->levels[lv - 1], d_cnt + lv - 1, level_done[lv - 1],
+                                        cst)) != SPK_OK)
+        break;
+    }
     if (next_cap == 0) break;  // no splits (exact) or last fixed depth
     cur = next;
     cur_cap = next_cap;
     (void)k_exact;
   }
+  if (mirror && rc == SPK_OK && !tree->levels.empty()) {
+    const int last = (int)tree->levels.size() - 1;
+    rc = mirror_level(tree, last, tree->levels[last], d_cnt + last, level_done[last], cst);
+  }
+  for (auto ev : level_done) cudaEventDestroy(ev);
+  if (cst) cudaStreamDestroy(cst);
   // live sizes of every level, one copy
   if (rc == SPK_OK) {
     std::vector<long long> sizes(tree->levels.size());
@@ -452,6 +532,11 @@ int spk_tree_build_band(const spk_net* net, int policy, int n_keep, int precisio
     while (rc == SPK_OK && !tree->levels.empty() && tree->levels.back().n == 0) {
       free_level(tree->levels.back(), st);
       tree->levels.pop_back();
+      if (tree->host.size() > tree->levels.size()) {
+        std::free(tree->host.back());
+        tree->host.pop_back();
+        tree->host_n.pop_back();
+      }
     }
   }
   for (auto ev : bound_ev) cudaEventDestroy(ev);
@@ -464,6 +549,7 @@ int spk_tree_build_band(const spk_net* net, int policy, int n_keep, int precisio
   cudaEventDestroy(ev1);
   if (rc != SPK_OK) {
     for (auto& L : tree->levels) free_level(L, st);
+    free_mirror(tree);
     delete tree;
     return rc;
   }
@@ -475,7 +561,42 @@ int spk_tree_destroy(spk_tree* tree) {
   if (!tree) return SPK_OK;
   DeviceGuard g(tree->device);
   for (auto& L : tree->levels) free_level(L, tree->stream);
+  free_mirror(tree);
   delete tree;
+  return SPK_OK;
+}
+
+int spk_tree_release_device(spk_tree* tree) {
+  if (!tree) return fail(SPK_ERR_INVALID_PARAMETER, "null tree");
+  if (tree->host.size() != tree->levels.size())
+    return fail(SPK_ERR_INVALID_PARAMETER, "tree built without SPK_TREE_HOST_MIRROR");
+  DeviceGuard g(tree->device);
+  for (auto& L : tree->levels) {
+    const long long n = L.n;
+    free_level(L, tree->stream);
+    L.n = n;  // sizes stay readable; device pointers are gone
+  }
+  tree->device_released = true;
+  return SPK_OK;
+}
+
+int spk_tree_level_host(const spk_tree* tree, int level, int64_t* n, const double** lo, const double** hi,
+                        const double** bound_lo, const double** bound_hi, const int8_t** label,
+                        const int8_t** face, const int64_t** parent) {
+  if (!tree || level < 0 || level >= (int)tree->levels.size())
+    return fail(SPK_ERR_INVALID_PARAMETER, "bad tree level");
+  if (level >= (int)tree->host.size() || !tree->host[level])
+    return fail(SPK_ERR_INVALID_PARAMETER, "tree built without SPK_TREE_HOST_MIRROR");
+  const size_t m = (size_t)tree->host_n[level], d = (size_t)tree->d;
+  const char* h = tree->host[level];
+  if (n) *n = (int64_t)m;
+  if (lo) *lo = reinterpret_cast<const double*>(h);
+  if (hi) *hi = reinterpret_cast<const double*>(h + m * d * 8);
+  if (bound_lo) *bound_lo = reinterpret_cast<const double*>(h + 2 * m * d * 8);
+  if (bound_hi) *bound_hi = reinterpret_cast<const double*>(h + 2 * m * d * 8 + m * 8);
+  if (label) *label = reinterpret_cast<const int8_t*>(h + 2 * m * d * 8 + 2 * m * 8);
+  if (face) *face = reinterpret_cast<const int8_t*>(h + 2 * m * d * 8 + 2 * m * 8 + m);
+  if (parent) *parent = reinterpret_cast<const int64_t*>(h + 2 * m * d * 8 + 2 * m * 8 + 2 * m);
   return SPK_OK;
 }
 
@@ -493,6 +614,7 @@ int spk_tree_level_copy(const spk_tree* tree, int level, double* lo, double* hi,
                         double* bound_hi, int8_t* label, int8_t* face, int64_t* parent) {
   if (!tree || level < 0 || level >= (int)tree->levels.size())
     return fail(SPK_ERR_INVALID_PARAMETER, "bad tree level");
+  if (tree->device_released) return fail(SPK_ERR_INVALID_PARAMETER, "device levels released (host mirror only)");
   DeviceGuard g(tree->device);
   const TreeLevel& L = tree->levels[level];
   const size_t n = (size_t)L.n, d = (size_t)tree->d;
@@ -522,6 +644,8 @@ int spk_tree_level(const spk_tree* tree, int level, int64_t* n, const double** l
     return fail(SPK_ERR_INVALID_PARAMETER, "bad tree level");
   const TreeLevel& L = tree->levels[level];
   if (n) *n = L.n;
+  if (tree->device_released && (lo || hi || bound_lo || bound_hi || label || face || parent))
+    return fail(SPK_ERR_INVALID_PARAMETER, "device levels released (host mirror only)");
   if (lo) *lo = L.lo;
   if (hi) *hi = L.hi;
   if (bound_lo) *bound_lo = L.blo;

@@ -236,10 +236,13 @@ def _build(net, roots_lo, roots_hi, start_depth, delta, policy, max_depth, preci
     roots_hi = np.ascontiguousarray(roots_hi, dtype=np.float64)
     handle = C.c_void_p()
     stream = dv.stream_ptr(dn.device)
+    # to_host: the library mirrors every level to host memory while the next
+    # level computes (overlapped copies) and the levels are NumPy views of it
     _lib.call(
-        "spk_tree_build_band", dn.ptr, pcode, n_keep, _precision_code(precision), roots_lo.shape[0],
+        "spk_tree_build_ex", dn.ptr, pcode, n_keep, _precision_code(precision), roots_lo.shape[0],
         roots_lo.ctypes.data, roots_hi.ctypes.data, int(start_depth),
-        -1 if max_depth is None else int(max_depth), float(delta), float(band), stream, C.byref(handle),
+        -1 if max_depth is None else int(max_depth), float(delta), float(band), _HOST_MIRROR if to_host else 0,
+        stream, C.byref(handle),
     )
     owner = _TreeHandle(handle)
     lib = _lib.load()
@@ -258,7 +261,8 @@ def _build(net, roots_lo, roots_hi, start_depth, delta, policy, max_depth, preci
     arr = TreeArrays(None, int(start_depth), be.value, la.value, ms.value, loader=loader, n_levels=nl.value,
                      n_nodes=nn.value, first_level_len=n0.value)
     if to_host:
-        arr.levels  # copy out now; the library tree is released with `owner`
+        arr.levels  # NumPy views of the host mirror; the device levels go now
+        _lib.call("spk_tree_release_device", handle)
     return arr
 
 
@@ -266,17 +270,33 @@ _LEVEL_SPECS = (("lo", "<f8", 2), ("hi", "<f8", 2), ("bound_lo", "<f8", 1), ("bo
                 ("label", "|i1", 1), ("face", "|i1", 1), ("parent", "<i8", 1))
 
 
+_HOST_MIRROR = 1  # SPK_TREE_HOST_MIRROR
+
+
+class _HostView:
+    """__array_interface__ view of the library's host mirror of a level; the
+    NumPy array keeps it (and so the tree) alive."""
+
+    def __init__(self, owner, ptr, shape, typestr):
+        self.owner = owner
+        self.__array_interface__ = {"shape": shape, "typestr": typestr, "data": (ptr or 0, False), "version": 3}
+
+
 def _level(owner, level, d, device, to_host):
-    """One level as NumPy copies (to_host) or zero-copy CUDA tensors that keep
-    the library's tree alive."""
+    """One level as NumPy arrays over the library's host mirror (to_host) or
+    zero-copy CUDA tensors; both keep the library's tree alive."""
     n = C.c_int64()
     ptrs = [C.c_void_p() for _ in range(7)]
+    if to_host:
+        _lib.check(_lib.load().spk_tree_level_host(owner.ptr, level, C.byref(n), *[C.byref(p) for p in ptrs]))
+        n = n.value
+        out = []
+        for (name, ts, nd), p in zip(_LEVEL_SPECS, ptrs):
+            shape = (n, d) if nd == 2 else (n,)
+            out.append(np.asarray(_HostView(owner, p.value, shape, ts)) if n else np.empty(shape, np.dtype(ts)))
+        return TreeLevel(*out)
     _lib.check(_lib.load().spk_tree_level(owner.ptr, level, C.byref(n), *[C.byref(p) for p in ptrs]))
     n = n.value
-    if to_host:
-        out = [np.empty((n, d) if nd == 2 else (n,), np.dtype(ts)) for _, ts, nd in _LEVEL_SPECS]
-        _lib.call("spk_tree_level_copy", owner.ptr, level, *[a.ctypes.data for a in out])
-        return TreeLevel(*out)
     torch = dv._torch()
     out = []
     for (name, ts, nd), p in zip(_LEVEL_SPECS, ptrs):
