@@ -13,6 +13,9 @@
 #include "spk_kernels.cuh"
 #include "spk_abi_internal.h"
 
+#ifndef SPK_SMALL_TILE
+#define SPK_SMALL_TILE 1  // few-hundred-box FP32 batches on width-256 nets: the SM = 1 tile
+#endif
 #ifndef SPK_SPREAD_SMALL
 #define SPK_SPREAD_SMALL 1  // small FP32 batches on wide nets: one box group per SM sub-partition
 #endif
@@ -257,7 +260,15 @@ int run_pass(const spk_net* cnet, int mode, int S, int precision, const BoxInput
     // (spread_node); empty groups skip their K loops through the live-row masks
     const bool spread = SPK_SPREAD_SMALL && (mode == MODE_AFFINE || mode == MODE_INTERVAL) && net->mmax >= 256 &&
                         n <= (long long)sm * 8 && in.perm == nullptr;
-    if (spread) {
+    // a few hundred boxes on a width-256 net (the top tree levels): the
+    // small tile, one neuron per thread, a box pair per CTA, 2 CTAs per SM
+    const bool small = SPK_SMALL_TILE && (mode == MODE_INTERVAL || (mode == MODE_AFFINE && S >= 3)) &&
+                       net->mmax == 256 && n <= (long long)sm * 4 && in.perm == nullptr && !in.spread;
+    if (small) {
+      BoxInput in2 = in;
+      in2.small = 1;
+      e = dispatch_any<float>(net->mmax, mode, S, *nd, in2, out, n, sm, st);
+    } else if (spread) {
       BoxInput in2 = in;
       in2.spread = 1;
       in2.spread_n = n;

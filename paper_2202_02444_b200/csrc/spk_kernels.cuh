@@ -22,6 +22,7 @@ struct BoxInput {
                            // so a box group holds two sibling boxes (coherent live-row masks)
   const int* perm = nullptr;  // optional processing order: slot gb processes box perm[gb] (spk_order.cu)
   int spread = 0;             // small batch spread over every SM (see spread_node)
+  int small = 0;              // few-hundred-box batch: the SM = 1 tile (Cfg), FP32, width 256
   long long spread_n = 0;     // spread: host-side box count (capacity when n_dev is given)
 };
 
@@ -76,10 +77,10 @@ SPK_DEV double random_coord(unsigned long long seed, long long idx, int k, int d
 
 // Inputs of one tile of NB boxes -> X rows [0, d) (packed columns), zeros
 // in rows [d, MMAX).  Shared by the fixed-shape and the symbol-carrying kernels.
-template <typename T, int C, int MMAX, int MODE>
+template <typename T, int C, int MMAX, int MODE, int SM = 0>
 SPK_DEV void prep_inputs(const NetDev<T>& net, const BoxInput& in, long long n, long long g0, T* X, int tid,
                          bool pack) {
-  using CF = Cfg<T, C, MMAX>;
+  using CF = Cfg<T, C, MMAX, SM>;
   constexpr int NB = CF::NB, CP = CF::CP;
   const int d = net.d;
   // the first layer reads rows [0, d) plus the zero pad row of its
@@ -147,10 +148,10 @@ SPK_DEV void emit_bounds(const BoundOutput& out, long long gb, const State<T, C,
   if (out.cls) out.cls[gb] = (int8_t)(lo > 0.0 ? 1 : (hi < 0.0 ? -1 : 0));
 }
 
-template <typename T, int C, int MMAX, int MODE>
-__global__ void __launch_bounds__(NT, (Cfg<T, C, MMAX>::MINB))
+template <typename T, int C, int MMAX, int MODE, int SM = 0>
+__global__ void __launch_bounds__(NT, (Cfg<T, C, MMAX, SM>::MINB))
     bound_kernel(const NetDev<T> net, const BoxInput in, const BoundOutput out, const long long n_cap) {
-  using CF = Cfg<T, C, MMAX>;
+  using CF = Cfg<T, C, MMAX, SM>;
   // real box count; spread mode runs over grid x NB slots
   const long long n = in.n_dev ? *in.n_dev : (in.spread ? in.spread_n : n_cap);
   constexpr int NB = CF::NB;
@@ -173,14 +174,14 @@ __global__ void __launch_bounds__(NT, (Cfg<T, C, MMAX>::MINB))
     mbar_fence_init();
   }
   __syncthreads();
-  WRing<T, C, MMAX> ring{Wst, full, released, net.wtiles, net.tiles_per_pass, mine * net.tiles_per_pass, 0};
+  WRing<T, C, MMAX, SM> ring{Wst, full, released, net.wtiles, net.tiles_per_pass, mine * net.tiles_per_pass, 0};
   if (CF::LIVE) ring.live = reinterpret_cast<uint32_t*>(released + 16);
   ring.prologue(tid);
 
   for (long long tile = blockIdx.x; tile < nbt; tile += gridDim.x) {
     const long long g0 = tile * NB;
     if (CF::TEAMSYNC) csync();  // every team is done with the previous tile's X
-    prep_inputs<T, C, MMAX, MODE>(net, in, n, g0, X, tid, true);
+    prep_inputs<T, C, MMAX, MODE, SM>(net, in, n, g0, X, tid, true);
     auto node = [&](int b) -> long long {
       return in.spread ? spread_node<CF::TB, CF::NBG>(in, g0 + b, n, (int)gridDim.x) : node_of(in, g0 + b, n);
     };
@@ -191,16 +192,16 @@ __global__ void __launch_bounds__(NT, (Cfg<T, C, MMAX>::MINB))
       const long long nd = node(b);
       if (nd >= 0) emit_bounds<T, C, MODE>(out, nd, st);
     };
-    run_layers<T, C, MMAX, MODE>(net, X, NBUF, ring, tid, emit);
+    run_layers<T, C, MMAX, MODE, decltype(emit)&, SM>(net, X, NBUF, ring, tid, emit);
   }
 }
 
 // ------------------------------------------------------------- launchers
-template <typename T, int C, int MMAX, int MODE>
+template <typename T, int C, int MMAX, int MODE, int SM = 0>
 cudaError_t launch_bound(const NetDev<T>& net, const BoxInput& in, const BoundOutput& out, long long n,
                          int sm_count, cudaStream_t stream) {
-  using CF = Cfg<T, C, MMAX>;
-  auto kfn = bound_kernel<T, C, MMAX, MODE>;
+  using CF = Cfg<T, C, MMAX, SM>;
+  auto kfn = bound_kernel<T, C, MMAX, MODE, SM>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
@@ -230,6 +231,12 @@ struct KTOf {
   template <>                                                                                         \
   cudaError_t dispatch_bound<T, MMAX>(int mode, int S, const NetDev<T>& net, const BoxInput& in,       \
                                       const BoundOutput& out, long long n, int sm, cudaStream_t st) { \
+    if constexpr (sizeof(T) == 4 && MMAX == 256) {                                                    \
+      if (in.small && mode == MODE_INTERVAL)                                                          \
+        return launch_bound<T, 2, MMAX, MODE_INTERVAL, 1>(net, in, out, n, sm, st);                   \
+      if (in.small && mode == MODE_AFFINE && S >= 3)                                                  \
+        return launch_bound<T, 5, MMAX, MODE_AFFINE, 1>(net, in, out, n, sm, st);                     \
+    }                                                                                                 \
     if (mode == MODE_POINT) return launch_bound<T, 1, MMAX, MODE_POINT>(net, in, out, n, sm, st);      \
     if (mode == MODE_INTERVAL) return launch_bound<T, 2, MMAX, MODE_INTERVAL>(net, in, out, n, sm, st); \
     switch (S) {                                                                                      \

@@ -106,19 +106,25 @@ struct NetDev {
   LayerDev<T> L[MAX_LAYERS];
 };
 
-template <typename T, int C, int MMAX>
+// SM = 1: the small-batch tile (a box pair per CTA, one neuron per thread,
+// two CTAs per SM).  A batch of a few hundred boxes (the top tree levels) is
+// latency-bound -- one warp's K-loop chain per layer -- so the 256 output
+// neurons of a layer are spread over all 256 threads instead of 32.
+template <typename T, int C, int MMAX, int SM = 0>
 struct Cfg {
   static constexpr int VEC = 16 / (int)sizeof(T);  // elements per 16-byte vector
   // register tile: TI neurons x TB boxes x C columns per thread
-  static constexpr int TI = C <= 6 ? (sizeof(T) == 4 ? 8 : 4)
-                                   : (C <= 20 ? VEC : (VEC / 2 > 0 ? VEC / 2 : 1));
+  static constexpr int TI = SM ? 1
+                               : (C <= 6 ? (sizeof(T) == 4 ? 8 : 4)
+                                         : (C <= 20 ? VEC : (VEC / 2 > 0 ? VEC / 2 : 1)));
   // narrow nets (MMAX = 32) with affine columns: one box per thread and two
   // CTAs per SM -- their K loops are short, so latency hiding across CTAs
   // matters more than register reuse across boxes (measured: 4x32 -19%
   // time; at width 64 the 1-CTA, 2-box tile is 17% faster)
-  static constexpr int MINB = (SPK_NARROW_2CTA && MMAX <= 32 && C >= 3 && C <= 6) ? 2 : 1;
-  static constexpr int TB = C == 1 ? (sizeof(T) == 4 ? 8 : 4)
-                                   : (C == 2 ? 4 : (C <= 6 ? (MINB == 2 ? 1 : 2) : 1));
+  static constexpr int MINB = SM ? 2 : ((SPK_NARROW_2CTA && MMAX <= 32 && C >= 3 && C <= 6) ? 2 : 1);
+  static constexpr int TB = SM ? 2
+                               : (C == 1 ? (sizeof(T) == 4 ? 8 : 4)
+                                         : (C == 2 ? 4 : (C <= 6 ? (MINB == 2 ? 1 : 2) : 1)));
   static constexpr int CP = C == 1 ? 1 : (C == 2 ? 2 : (C <= 4 ? 4 : (C <= 6 ? (TB == 1 ? 8 : 6)
                                                                          : ((C + VEC - 1) / VEC) * VEC)));
   static constexpr int NG = MMAX / TI;
@@ -240,9 +246,9 @@ SPK_DEV void tma_bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t*
 // producer warp (which would cost ~25% of the register file) is needed.  When
 // the whole network fits in the ring (tiles_per_pass <= NS) every tile is
 // loaded once and stays resident for the CTA's lifetime.
-template <typename T, int C, int MMAX>
+template <typename T, int C, int MMAX, int SM = 0>
 struct WRing {
-  using CF = Cfg<T, C, MMAX>;
+  using CF = Cfg<T, C, MMAX, SM>;
   T* stages;
   uint64_t* full;
   unsigned* released;  // per-stage count of warps done with the current round
@@ -441,10 +447,10 @@ SPK_DEV State<T, C, MODE> state_from(const T* col, T be) {
 // round-to-nearest columns are summed in blocks of SUB k-steps (fresh
 // partials added to the running sums), so the rounding budget is
 // gamma_{SUB + ceil(m_in/SUB) + 1} instead of gamma_{m_in + 1}.
-template <typename T, int C, int MMAX, int BIAS2 = -1, bool TEAMS = false>
-SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, WRing<T, C, MMAX>& ring, int tid,
-                                T (&acc)[Cfg<T, C, MMAX>::TI][Cfg<T, C, MMAX>::TB][C]) {
-  using CF = Cfg<T, C, MMAX>;
+template <typename T, int C, int MMAX, int BIAS2 = -1, bool TEAMS = false, int SM = 0>
+SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, WRing<T, C, MMAX, SM>& ring, int tid,
+                                T (&acc)[Cfg<T, C, MMAX, SM>::TI][Cfg<T, C, MMAX, SM>::TB][C]) {
+  using CF = Cfg<T, C, MMAX, SM>;
   constexpr int TI = CF::TI, TB = CF::TB, CP = CF::CP, KT = CF::KT;
   const int ng = tid % CF::NG, bg = tid / CF::NG;
   // RN columns accumulate in SUB-step partial sums (blocked summation, the
@@ -646,11 +652,11 @@ SPK_DEV f32x2 f2_pack(float lo, float hi) {
 // pairs, an optional odd RN column, and the round-up error column (scalar
 // FFMA.RP with the |W| operand modifier).  Point evaluation (C == 1) pairs
 // adjacent boxes instead.  Same blocked-summation budget as the scalar loop.
-template <int C, int MMAX, int BIAS2 = -1, bool TEAMS = false>
-SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__ X, WRing<float, C, MMAX>& ring,
-                             int tid, float (&acc)[Cfg<float, C, MMAX>::TI][Cfg<float, C, MMAX>::TB][C],
+template <int C, int MMAX, int BIAS2 = -1, bool TEAMS = false, int SM = 0>
+SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__ X, WRing<float, C, MMAX, SM>& ring,
+                             int tid, float (&acc)[Cfg<float, C, MMAX, SM>::TI][Cfg<float, C, MMAX, SM>::TB][C],
                              const uint32_t* live = nullptr) {
-  using CF = Cfg<float, C, MMAX>;
+  using CF = Cfg<float, C, MMAX, SM>;
   constexpr int TI = CF::TI, TB = CF::TB, CP = CF::CP, KT = CF::KT;
   constexpr bool POINT = C == 1;
   constexpr int NRN = POINT ? 1 : C - 1;           // round-to-nearest columns per box
@@ -878,20 +884,20 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
 
 // BIAS2 >= 0: a second column that also starts from the bias (march modes:
 // the point value in column 0 and the bound's base in column 1)
-template <typename T, int C, int MMAX, int BIAS2 = -1, bool TEAMS = false>
-SPK_DEV void dense_kloop(const LayerDev<T>& L, const T* __restrict__ X, WRing<T, C, MMAX>& ring, int tid,
-                         T (&acc)[Cfg<T, C, MMAX>::TI][Cfg<T, C, MMAX>::TB][C], const uint32_t* live = nullptr) {
+template <typename T, int C, int MMAX, int BIAS2 = -1, bool TEAMS = false, int SM = 0>
+SPK_DEV void dense_kloop(const LayerDev<T>& L, const T* __restrict__ X, WRing<T, C, MMAX, SM>& ring, int tid,
+                         T (&acc)[Cfg<T, C, MMAX, SM>::TI][Cfg<T, C, MMAX, SM>::TB][C], const uint32_t* live = nullptr) {
   if constexpr (sizeof(T) == 4 && SPK_PACKED_F32) {
-    dense_kloop_f32<C, MMAX, BIAS2, TEAMS>(L, X, ring, tid, acc, live);
+    dense_kloop_f32<C, MMAX, BIAS2, TEAMS, SM>(L, X, ring, tid, acc, live);
   } else {
-    dense_kloop_scalar<T, C, MMAX, BIAS2, TEAMS>(L, X, ring, tid, acc);
+    dense_kloop_scalar<T, C, MMAX, BIAS2, TEAMS, SM>(L, X, ring, tid, acc);
   }
 }
 
-template <typename T, int C, int MMAX, int MODE>
-SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, MMAX>& ring, int tid,
+template <typename T, int C, int MMAX, int MODE, int SM = 0>
+SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, MMAX, SM>& ring, int tid,
                            bool last, T gamma_next, int lidx) {
-  using CF = Cfg<T, C, MMAX>;
+  using CF = Cfg<T, C, MMAX, SM>;
   constexpr int TI = CF::TI, TB = CF::TB, CP = CF::CP;
   const int ng = tid % CF::NG, bg = tid / CF::NG;
   // live-row masks (Cfg::LIVE; bound modes): this layer reads parity lidx&1
@@ -904,10 +910,13 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
   // one warp per box group holding 4-neuron groups at 4*lane (NG == 32, G == 4):
   // the masks are assembled with shuffles and stored whole, no clearing/atomics
   constexpr bool WMASK = LV && CF::NG == 32 && CF::G == 4;
+  // one neuron per thread over the whole CTA (SM = 1 tile): warp w holds
+  // neurons 32w..32w+31 = mask word w, one ballot
+  constexpr bool BMASK = LV && CF::TI == 1 && CF::NG == NT;
   if (LV && ring.live != nullptr) {
     m_nxt = ring.live + (size_t)(((lidx + 1) & 1) * CF::NBG + bg) * CF::LW;
     if (lidx > 0) m_cur = ring.live + (size_t)((lidx & 1) * CF::NBG + bg) * CF::LW;
-    if (!WMASK && ng < CF::LW) m_nxt[ng] = 0u;
+    if (!WMASK && !BMASK && ng < CF::LW) m_nxt[ng] = 0u;
   }
   // layer parameters the epilogue needs, read before the K loop so their
   // latency hides behind it (dynamically indexed parameter / global reads at
@@ -922,7 +931,7 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
     be_r[ti] = (MODE != MODE_POINT && i < L.m_out) ? L.berr[i] : T(0);
   }
   T acc[TI][TB][C];
-  dense_kloop<T, C, MMAX, (MODE >= MODE_MI ? 1 : -1), CF::TEAMSYNC>(L, X, ring, tid, acc, m_cur);
+  dense_kloop<T, C, MMAX, (MODE >= MODE_MI ? 1 : -1), CF::TEAMSYNC, SM>(L, X, ring, tid, acc, m_cur);
 
   // epilogue: activation rules, write next X in place (one contiguous
   // TB*CP vector per neuron: the thread's boxes are adjacent in the row)
@@ -996,7 +1005,10 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
       live_bits |= (nz ? 1u : 0u) << (ti % CF::G);
       if (ti % CF::G == CF::G - 1) {  // a group of G consecutive neurons: one word, one atomic
         const int i0 = i - (CF::G - 1);
-        if (WMASK) {
+        if (BMASK) {
+          const uint32_t v = __ballot_sync(0xffffffffu, live_bits != 0u);
+          if (m_nxt != nullptr && (tid & 31) == 0) m_nxt[i0 >> 5] = v;
+        } else if (WMASK) {
           // the warp owns every neuron of its box group: OR the nibbles of the
           // 8 lanes sharing a 32-bit word with shuffles, one plain store each
           uint32_t v = live_bits << (i0 & 31);
@@ -1028,10 +1040,10 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
 template <int MMAX>
 constexpr int narrow_lanes() { return MMAX <= 64 ? 4 : 32; }
 
-template <typename T, int C, int MMAX, int MODE, class Emit>
+template <typename T, int C, int MMAX, int MODE, class Emit, int SM = 0>
 SPK_DEV void narrow_layer(const LayerDev<T>& L, T* __restrict__ X, T* __restrict__ NBUF, int tid,
                           bool last, T gamma_next, Emit&& emit) {
-  using CF = Cfg<T, C, MMAX>;
+  using CF = Cfg<T, C, MMAX, SM>;
   constexpr int CP = CF::CP, KT = CF::KT;
   constexpr int LP = narrow_lanes<MMAX>(), IPW = 32 / LP;  // lanes per item, items per warp
   // team mode: a team reduces and finishes only its own boxes (the X columns
@@ -1126,16 +1138,16 @@ SPK_DEV void narrow_layer(const LayerDev<T>& L, T* __restrict__ X, T* __restrict
 // Runs every layer for the CTA's current tile.  X rows [0, d) must hold the
 // packed input columns and rows [d, MMAX) zeros; `emit(b, state)` receives
 // each box's final width-1 state.
-template <typename T, int C, int MMAX, int MODE, class Emit>
-SPK_DEV void run_layers(const NetDev<T>& net, T* X, T* NBUF, WRing<T, C, MMAX>& ring, int tid,
+template <typename T, int C, int MMAX, int MODE, class Emit, int SM = 0>
+SPK_DEV void run_layers(const NetDev<T>& net, T* X, T* NBUF, WRing<T, C, MMAX, SM>& ring, int tid,
                         Emit&& emit) {
   for (int l = 0; l < net.n_layers; ++l) {
     const LayerDev<T>& L = net.L[l];
     const bool last = (l == net.n_layers - 1);
     if (L.narrow) {
-      narrow_layer<T, C, MMAX, MODE>(L, X, NBUF, tid, last, L.gamma_next, emit);
+      narrow_layer<T, C, MMAX, MODE, Emit, SM>(L, X, NBUF, tid, last, L.gamma_next, emit);
     } else {
-      generic_layer<T, C, MMAX, MODE>(L, X, ring, tid, last, L.gamma_next, l);
+      generic_layer<T, C, MMAX, MODE, SM>(L, X, ring, tid, last, L.gamma_next, l);
     }
   }
 }
