@@ -190,10 +190,11 @@ def test_live_row_skipping_is_exact(policy):
     np.testing.assert_array_equal(lo.cpu().numpy(), lv.bound_lo[:m])
 
 
-def test_processing_orders_are_exact():
-    """Spread (small batches), natural, sibling-pair and Morton processing
-    orders all give bit-identical FP32 bounds: each box is bounded on its own
-    and skipped rows are exact zeros."""
+@pytest.mark.parametrize("policy", ["affine-fixed", "interval"])
+def test_processing_orders_are_exact(policy):
+    """The small tile, spread, natural and Morton processing orders all give
+    bit-identical FP32 bounds: each box is bounded on its own, skipped rows
+    are exact zeros, and every tile shape sums in the same k order."""
     import torch
 
     from paper_2202_02444_b200 import synth
@@ -204,8 +205,9 @@ def test_processing_orders_are_exact():
     c = rng.uniform(-1, 1, (n_big, 3))
     h = 10.0 ** rng.uniform(-3, -1, (n_big, 1))
     lo_t, hi_t = torch.from_numpy(c - h).cuda(), torch.from_numpy(c + h).cuda()
-    big_lo, big_hi, _ = sp.bound_aabb(net, lo_t, hi_t, "affine-fixed")
-    for a, b in ((0, 300), (1000, 1300), (5000, 12000)):  # spread, spread, natural order
-        lo, hi, _ = sp.bound_aabb(net, lo_t[a:b], hi_t[a:b], "affine-fixed")
+    big_lo, big_hi, _ = sp.bound_aabb(net, lo_t, hi_t, policy)
+    # small tile, spread, natural order (vs the Morton-ordered big batch)
+    for a, b in ((0, 300), (1000, 1900), (5000, 12000)):
+        lo, hi, _ = sp.bound_aabb(net, lo_t[a:b], hi_t[a:b], policy)
         np.testing.assert_array_equal(lo.cpu().numpy(), big_lo[a:b].cpu().numpy())
         np.testing.assert_array_equal(hi.cpu().numpy(), big_hi[a:b].cpu().numpy())
