@@ -949,6 +949,9 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
         if (act == ACT_RELU) {
 #pragma unroll
           for (int tb = 0; tb < TB; ++tb) out[tb * CP] = fmax(out[tb * CP], T(0));
+        } else if (act == ACT_ELU) {  // small inline code (elu_value): unrolled, registers only
+#pragma unroll
+          for (int tb = 0; tb < TB; ++tb) out[tb * CP] = elu_value<T>(out[tb * CP]);
         } else if (act != ACT_IDENTITY) {
 #pragma unroll 1
           for (int tb = 0; tb < TB; ++tb)

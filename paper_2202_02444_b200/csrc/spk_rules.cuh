@@ -248,11 +248,42 @@ SPK_RULE void interval_image_slow(int act, T lo, T hi, T& out_lo, T& out_hi) {
 // Pointwise value (network.py:149-160), used by point evaluation.  ReLU is
 // inline; the other activations live out of line so the unrolled epilogue
 // stays small (instruction-cache pressure).
+// FP32 ELU value (point evaluation): expm1 on [-1, 0) as its degree-10 Taylor
+// polynomial (<= 1.7e-7 relative), exp(x) - 1 below -1 (no cancellation,
+// <= 2.1e-7 relative with the MUFU exponential) -- within 3 ulp like the FP32
+// dot products around it, and ~3x cheaper than expm1f, which dominated the
+// ELU nets' point passes (C4 corner evaluation).  Bounds never use it: the
+// ELU affine and interval rules evaluate in FP64 (elu_affine, elu64).
+SPK_DEV float elu_f32(float x) {
+  float p = 2.7557319e-07f;        // 1/10!
+  p = fmaf(p, x, 2.7557319e-06f);  // 1/9!
+  p = fmaf(p, x, 2.4801587e-05f);  // 1/8!
+  p = fmaf(p, x, 1.9841270e-04f);  // 1/7!
+  p = fmaf(p, x, 1.3888889e-03f);  // 1/6!
+  p = fmaf(p, x, 8.3333333e-03f);  // 1/5!
+  p = fmaf(p, x, 4.1666667e-02f);  // 1/4!
+  p = fmaf(p, x, 1.6666667e-01f);  // 1/3!
+  p = fmaf(p, x, 0.5f);
+  p = fmaf(p, x, 1.0f);
+  p *= x;
+  const float q = __expf(x) - 1.0f;
+  return x >= 0.0f ? x : (x >= -1.0f ? p : q);
+}
+
+template <typename T>
+SPK_DEV T elu_value(T x) {
+  if constexpr (sizeof(T) == 4) {
+    return elu_f32(x);
+  } else {
+    return x >= T(0) ? x : expm1(x);
+  }
+}
+
 template <typename T>
 SPK_RULE T act_value_slow(int act, T x) {  // float / double overloads of the CUDA math library
   switch (act) {
     case ACT_RELU_BROKEN: return fmax(x, T(0));
-    case ACT_ELU: return x >= T(0) ? x : expm1(x);
+    case ACT_ELU: return elu_value<T>(x);
     case ACT_SIN: return sin(x);
     case ACT_TANH: return tanh(x);
     default: return x;
@@ -263,7 +294,7 @@ template <typename T>
 SPK_DEV T act_value_inline(int act, T x) {
   switch (act) {
     case ACT_RELU_BROKEN: return fmax(x, T(0));
-    case ACT_ELU: return x >= T(0) ? x : expm1(x);
+    case ACT_ELU: return elu_value<T>(x);
     case ACT_SIN: return sin(x);
     case ACT_TANH: return tanh(x);
     default: return x;
