@@ -54,6 +54,12 @@ constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reducti
 #ifndef SPK_LIVE_ROWS
 #define SPK_LIVE_ROWS 1  // skip all-zero X rows (ReLU-inactive neurons) in the FP32 K loop (Cfg::LIVE)
 #endif
+#ifndef SPK_LIVE_WARP
+#define SPK_LIVE_WARP 1  // narrow nets: warp-union live-row masks (Cfg::LIVE)
+#endif
+#ifndef SPK_LIVE_DENSE_NARROW
+#define SPK_LIVE_DENSE_NARROW 28  // the same for the warp-union masks of narrow nets
+#endif
 #ifndef SPK_LIVE_DENSE
 #define SPK_LIVE_DENSE 28  // tiles with more live rows than this run the unrolled chunk (18: +8%, 23: +1%)
 #endif
@@ -159,7 +165,11 @@ struct Cfg {
   // so the K loop may skip those rows with identical results.  FP32 wide nets
   // (a warp-uniform box group: NG >= 32) with 32-row W tiles (at width 512 the
   // 16-row tiles measured 10% slower masked on random cubes).
-  static constexpr bool LIVE = SPK_LIVE_ROWS && sizeof(T) == 4 && NG >= 32 && KT == 32 && C >= 2;
+  // Narrow nets (NG < 32: a warp holds 32/NG box groups) use one mask per
+  // warp -- the union over its box groups, so a skipped row is zero for every
+  // box the warp computes (needs a G-neuron group's mask word fixed by ti).
+  static constexpr bool LIVE = SPK_LIVE_ROWS && sizeof(T) == 4 && KT == 32 && C >= 2 &&
+                               (NG >= 32 || (SPK_LIVE_WARP && C >= 3 && 32 % (NG * G) == 0));
   static constexpr int LW = MMAX / 32;  // mask words per box group
   static constexpr int LLIST = 40;  // per-warp live-row list (<= 32 rows + 2 pad entries)
   static constexpr size_t LIVE_BYTES = LIVE ? (size_t)2 * NBG * LW * 4 + (size_t)(NT / 32) * LLIST * 4 : 0;
@@ -791,7 +801,7 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
       const uint32_t word = live[(t * KT) >> 5];
       m = KT == 32 ? word : ((word >> ((t * KT) & 31)) & ((1u << (KT & 31)) - 1u));
     }
-    if (CF::LIVE && live != nullptr && __popc(m) <= SPK_LIVE_DENSE) {
+    if (CF::LIVE && live != nullptr && __popc(m) <= (CF::NG < 32 ? SPK_LIVE_DENSE_NARROW : SPK_LIVE_DENSE)) {
       if (since == 0) zero_parts();
       if (m != 0u) {
         // an odd count gets one exactly-zero row (one exists: KT is even); the
@@ -913,10 +923,16 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
   // one neuron per thread over the whole CTA (SM = 1 tile): warp w holds
   // neurons 32w..32w+31 = mask word w, one ballot
   constexpr bool BMASK = LV && CF::TI == 1 && CF::NG == NT;
+  // narrow nets (NG < 32): every box group of a warp stores the warp's union
+  // (redux.sync per G-neuron group, accumulated per word, stored whole)
+  constexpr bool XMASK = LV && CF::NG < 32;
+  uint32_t xw[CF::LW];
+#pragma unroll
+  for (int w = 0; w < CF::LW; ++w) xw[w] = 0u;
   if (LV && ring.live != nullptr) {
     m_nxt = ring.live + (size_t)(((lidx + 1) & 1) * CF::NBG + bg) * CF::LW;
     if (lidx > 0) m_cur = ring.live + (size_t)((lidx & 1) * CF::NBG + bg) * CF::LW;
-    if (!WMASK && !BMASK && ng < CF::LW) m_nxt[ng] = 0u;
+    if (!WMASK && !BMASK && !XMASK && ng < CF::LW) m_nxt[ng] = 0u;
   }
   // layer parameters the epilogue needs, read before the K loop so their
   // latency hides behind it (dynamically indexed parameter / global reads at
@@ -1011,6 +1027,9 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
         if (BMASK) {
           const uint32_t v = __ballot_sync(0xffffffffu, live_bits != 0u);
           if (m_nxt != nullptr && (tid & 31) == 0) m_nxt[i0 >> 5] = v;
+        } else if (XMASK) {
+          // neurons (ti/G)*NG*G + ng*G + r: the word is fixed by ti (NG*G divides 32)
+          xw[((ti / CF::G) * CF::NG * CF::G) >> 5] |= __reduce_or_sync(0xffffffffu, live_bits << (i0 & 31));
         } else if (WMASK) {
           // the warp owns every neuron of its box group: OR the nibbles of the
           // 8 lanes sharing a 32-bit word with shuffles, one plain store each
@@ -1025,6 +1044,10 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
         live_bits = 0u;
       }
     }
+  }
+  if (XMASK && m_nxt != nullptr && ng == 0) {
+#pragma unroll
+    for (int w = 0; w < CF::LW; ++w) m_nxt[w] = xw[w];
   }
   if (CF::TEAMSYNC) {
     team_sync<CF::TEAM>(tid);

@@ -46,7 +46,7 @@ def test_affine_rule_matches_reference_rules(golden):
         # [0, 0] for ReLU: any subgradient is exact (the reference takes 0, the
         # device rule 1); both give alpha*0 + beta = 0 with gamma = 0
         zero = (lo == 0.0) & (hi == 0.0)
-        ok = np.isfinite(wa) & ~(zero if kind == "relu" else False)
+        ok = np.isfinite(wa) & ~(zero if kind == "relu" else np.zeros_like(zero))
         np.testing.assert_allclose(a[ok], wa[ok], rtol=1e-12, atol=1e-12)
         if kind == "relu":
             assert np.all((b[zero] == 0.0) & (g[zero] == 0.0))

@@ -211,3 +211,28 @@ def test_processing_orders_are_exact(policy):
         lo, hi, _ = sp.bound_aabb(net, lo_t[a:b], hi_t[a:b], policy)
         np.testing.assert_array_equal(lo.cpu().numpy(), big_lo[a:b].cpu().numpy())
         np.testing.assert_array_equal(hi.cpu().numpy(), big_hi[a:b].cpu().numpy())
+
+
+@pytest.mark.parametrize("netname", ["c1", "relu_sdf"])
+def test_narrow_warp_live_masks_are_exact(net_paths, netname):
+    """Width-32 nets skip X rows that are zero for every box a warp computes
+    (the union of its box groups' masks).  A batch sorted along z (coherent
+    warps, many rows skipped) and the same boxes in a random permutation
+    (incoherent warps, few skipped) must give bit-identical bounds."""
+    import torch
+
+    from paper_2202_02444_b200 import synth
+
+    net = synth.config_net("C1") if netname == "c1" else sp.load_network(net_paths[netname])
+    rng = np.random.default_rng(11)
+    n = 50_000
+    c = rng.uniform(-1, 1, (n, 3))
+    c = c[np.argsort(c[:, 2])]
+    h = 10.0 ** rng.uniform(-3, -1.5, (n, 1))
+    perm = rng.permutation(n)
+    for policy in ("affine-fixed", "interval"):
+        lo_a, hi_a, _ = sp.bound_aabb(net, torch.from_numpy(c - h).cuda(), torch.from_numpy(c + h).cuda(), policy)
+        lo_b, hi_b, _ = sp.bound_aabb(net, torch.from_numpy(c[perm] - h[perm]).cuda(),
+                                      torch.from_numpy(c[perm] + h[perm]).cuda(), policy)
+        np.testing.assert_array_equal(lo_b.cpu().numpy(), lo_a.cpu().numpy()[perm])
+        np.testing.assert_array_equal(hi_b.cpu().numpy(), hi_a.cpu().numpy()[perm])
