@@ -22,6 +22,9 @@
 #ifndef SPK_SPATIAL_ORDER
 #define SPK_SPATIAL_ORDER 1  // Morton order for large batches (spk_order.cu)
 #endif
+#ifndef SPK_ORDER_MIN_MMAX
+#define SPK_ORDER_MIN_MMAX 256  // narrowest net width that Morton-orders large batches
+#endif
 
 namespace spk {
 
@@ -252,8 +255,8 @@ int run_pass(const spk_net* cnet, int mode, int S, int precision, const BoxInput
     // skip more ReLU-inactive rows (identical results; spk_order.cu)
     // (tree levels keep their sibling-pair order: Morton-sorting them as well
     // measured 0.6% slower -- the sort costs more than the extra coherence)
-    const bool order = SPK_SPATIAL_ORDER && (mode == MODE_AFFINE || mode == MODE_INTERVAL) && net->mmax >= 256 &&
-                       n >= (1ll << 16) && in.n_dev == nullptr && !in.pair_order && in.perm == nullptr &&
+    const bool order = SPK_SPATIAL_ORDER && (mode == MODE_AFFINE || mode == MODE_INTERVAL) &&
+                       net->mmax >= SPK_ORDER_MIN_MMAX && n >= (1ll << 16) && in.n_dev == nullptr && !in.pair_order && in.perm == nullptr &&
                        (in.kind == IN_RANDOM || in.kind == IN_BOXES || in.kind == IN_AABB);
     // small batches (fewer boxes than 8 per SM, e.g. the top tree levels) are
     // spread over every SM, one box group per SM sub-partition first

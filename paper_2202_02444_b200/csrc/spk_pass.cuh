@@ -57,6 +57,9 @@ constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reducti
 #ifndef SPK_LIVE_WARP
 #define SPK_LIVE_WARP 1  // narrow nets: warp-union live-row masks (Cfg::LIVE)
 #endif
+#ifndef SPK_KT_F32_W64
+#define SPK_KT_F32_W64 32  // W tile rows of FP32 width-64 nets (32: live-row masks apply; C5_64 +11%)
+#endif
 #ifndef SPK_LIVE_DENSE_NARROW
 #define SPK_LIVE_DENSE_NARROW 28  // the same for the warp-union masks of narrow nets
 #endif
@@ -137,7 +140,8 @@ struct Cfg {
   static constexpr int NBG = NT / NG;
   static constexpr int NB = NBG * TB;
   static constexpr int KT_RAW = 32768 / (MMAX * (int)sizeof(T));
-  static constexpr int KT = KT_RAW > MMAX ? MMAX : (KT_RAW < 1 ? 1 : KT_RAW);
+  static constexpr int KT = (sizeof(T) == 4 && MMAX == 64) ? SPK_KT_F32_W64
+                                                            : (KT_RAW > MMAX ? MMAX : (KT_RAW < 1 ? 1 : KT_RAW));
   static constexpr int SUB = sizeof(T) == 4 ? SPK_SUB_F32 : 1 << 20;  // blocked-sum length (FP32)
   static constexpr int TILE = KT * MMAX;                 // elements per W tile
   // X row stride (elements): 16-byte aligned rows, and an odd number of
