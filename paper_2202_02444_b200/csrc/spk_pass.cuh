@@ -329,9 +329,12 @@ struct State {
 
 template <typename T, int C, int MODE>
 SPK_DEV T sum_abs_A(const State<T, C, MODE>& st) {
-  T r = T(0);
+  // starts from |A_0| (RU(0 + |A_0|) = |A_0| exactly): one dependent add less
+  constexpr int S = State<T, C, MODE>::S;
+  if constexpr (S == 0) return T(0);
+  T r = fabs(st.A[0]);
 #pragma unroll
-  for (int j = 0; j < State<T, C, MODE>::S; ++j) r = Num<T>::add_ru(r, fabs(st.A[j]));
+  for (int j = 1; j < S; ++j) r = Num<T>::add_ru(r, fabs(st.A[j]));
   return r;
 }
 
