@@ -57,6 +57,9 @@ constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reducti
 #ifndef SPK_LIVE_WARP
 #define SPK_LIVE_WARP 1  // narrow nets: warp-union live-row masks (Cfg::LIVE)
 #endif
+#ifndef SPK_2CTA_MAXW
+#define SPK_2CTA_MAXW 64  // widest FP32 net on the one-box-per-thread, 2-CTA/SM tile (64: C5_64 +3% with masks)
+#endif
 #ifndef SPK_KT_F32_W64
 #define SPK_KT_F32_W64 32  // W tile rows of FP32 width-64 nets (32: live-row masks apply; C5_64 +11%)
 #endif
@@ -129,8 +132,12 @@ struct Cfg {
   // narrow nets (MMAX = 32) with affine columns: one box per thread and two
   // CTAs per SM -- their K loops are short, so latency hiding across CTAs
   // matters more than register reuse across boxes (measured: 4x32 -19%
-  // time; at width 64 the 1-CTA, 2-box tile is 17% faster)
-  static constexpr int MINB = SM ? 2 : ((SPK_NARROW_2CTA && MMAX <= 32 && C >= 3 && C <= 6) ? 2 : 1);
+  // time; at width 64 the 1-CTA, 2-box tile was 17% faster without live-row
+  // masks, and the 2-CTA tile is 3% faster with them: FP32 only)
+  static constexpr int MINB =
+      SM ? 2
+         : ((SPK_NARROW_2CTA && (MMAX <= 32 || (sizeof(T) == 4 && MMAX <= SPK_2CTA_MAXW)) && C >= 3 && C <= 6) ? 2
+                                                                                                              : 1);
   static constexpr int TB = SM ? 2
                                : (C == 1 ? (sizeof(T) == 4 ? 8 : 4)
                                          : (C == 2 ? 4 : (C <= 6 ? (MINB == 2 ? 1 : 2) : 1)));
