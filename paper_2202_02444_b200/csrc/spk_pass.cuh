@@ -57,6 +57,9 @@ constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reducti
 #ifndef SPK_LIVE_WARP
 #define SPK_LIVE_WARP 1  // narrow nets: warp-union live-row masks (Cfg::LIVE)
 #endif
+#ifndef SPK_PACKED_ERR
+#define SPK_PACKED_ERR 0  // FP32 error column on FFMA2.RP over neuron pairs (bit-identical; measured: C2 tree +0.3%, width 64 +4% time -- off)
+#endif
 #ifndef SPK_2CTA_MAXW
 #define SPK_2CTA_MAXW 64  // widest FP32 net on the one-box-per-thread, 2-CTA/SM tile (64: C5_64 +3% with masks)
 #endif
@@ -652,6 +655,14 @@ SPK_DEV f32x2 f2_fma(float w, f32x2 x, f32x2 acc) {
   asm("{.reg .b64 wd;\n mov.b64 wd, {%1, %1};\n fma.rn.f32x2 %0, wd, %2, %0;}" : "+l"(acc) : "f"(w), "l"(x));
   return acc;
 }
+// error column of two neurons: acc(i, i+1) += RU(|w_i| * x), RU(|w_i+1| * x)
+// -- one FFMA2.RP with the |.| operand modifier and x broadcast (.F32)
+SPK_DEV f32x2 f2_fma_ru_abs(float w0, float w1, float x, f32x2 acc) {
+  asm("{.reg .b64 wd, xd;\n mov.b64 wd, {%1, %2};\n mov.b64 xd, {%3, %3};\n fma.rp.f32x2 %0, wd, xd, %0;}"
+      : "+l"(acc)
+      : "f"(fabsf(w0)), "f"(fabsf(w1)), "f"(x));
+  return acc;
+}
 SPK_DEV f32x2 f2_fma2(f32x2 w, f32x2 x, f32x2 acc) {
   asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(w), "l"(x));
   return acc;
@@ -694,6 +705,14 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
   constexpr int NPA = NP > 0 ? NP : 1;
   f32x2 accp[TI][NBOX][NPA], partp[TI][NBOX][NPA];
   float acco[TI][TB], parto[TI][TB], acce[TI][TB];
+  // error column packed over neuron pairs (SPK_PACKED_ERR; FFMA2.RP, same
+  // per-lane rounding and order as the scalar FFMA.RP, so identical sums)
+  constexpr bool PE = SPK_PACKED_ERR && !POINT && TI % 2 == 0;
+  f32x2 acce2[PE ? TI / 2 : 1][TB];
+#pragma unroll
+  for (int j = 0; j < (PE ? TI / 2 : 1); ++j)
+#pragma unroll
+    for (int tb = 0; tb < TB; ++tb) acce2[j][tb] = 0ull;
 #pragma unroll
   for (int ti = 0; ti < TI; ++ti) {
     const int i = CF::neuron(ng, ti);
@@ -774,7 +793,11 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
           float lo, hi;
           f2_split(xq[(tb * CP + C - 1) / 2], lo, hi);
           const float xe = ((C - 1) % 2 == 0) ? lo : hi;
-          acce[ti][tb] = __fmaf_ru(fabsf(w[ti]), xe, acce[ti][tb]);
+          if (!PE) {
+            acce[ti][tb] = __fmaf_ru(fabsf(w[ti]), xe, acce[ti][tb]);
+          } else if (ti % 2 == 1) {
+            acce2[ti / 2][tb] = f2_fma_ru_abs(w[ti - 1], w[ti], xe, acce2[ti / 2][tb]);
+          }
           if (ODD) {
             float ol, oh;
             f2_split(xq[(tb * CP + 2 * NP) / 2], ol, oh);
@@ -900,7 +923,13 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
 #pragma unroll
         for (int p = 0; p < NP; ++p) f2_split(accp[ti][tb][p], acc[ti][tb][2 * p], acc[ti][tb][2 * p + 1]);
         if (ODD) acc[ti][tb][2 * NP] = acco[ti][tb];
-        acc[ti][tb][C - 1] = acce[ti][tb];
+        if (PE) {
+          float e0, e1;
+          f2_split(acce2[ti / 2][tb], e0, e1);
+          acc[ti][tb][C - 1] = (ti % 2 == 0) ? e0 : e1;
+        } else {
+          acc[ti][tb][C - 1] = acce[ti][tb];
+        }
       }
     }
   }
