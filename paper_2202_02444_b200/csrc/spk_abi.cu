@@ -208,7 +208,10 @@ int build_device_net(spk_net* net, DevNet<T>& dn) {
 }
 
 template <typename T>
-int get_dev(spk_net* net, const NetDev<T>** out) {
+int get_dev(spk_net* net, NetDev<T>* out) {
+  // the kernel-parameter copy is taken under the net's lock, so a concurrent
+  // spk_net_debug_corrupt_relu (which recodes the cached program) never
+  // tears a launch's activation list
   DevNet<T>& dn = net->dev<T>();
   std::lock_guard<std::mutex> lk(net->mu);
   if (!dn.ready) {
@@ -216,11 +219,11 @@ int get_dev(spk_net* net, const NetDev<T>** out) {
     int rc = build_device_net<T>(net, dn);
     if (rc != SPK_OK) return rc;
   }
-  *out = &dn.nd;
+  *out = dn.nd;
   return SPK_OK;
 }
-template int get_dev<float>(spk_net*, const NetDev<float>**);
-template int get_dev<double>(spk_net*, const NetDev<double>**);
+template int get_dev<float>(spk_net*, NetDev<float>*);
+template int get_dev<double>(spk_net*, NetDev<double>*);
 
 template <typename T>
 cudaError_t dispatch_any(int mmax, int mode, int S, const NetDev<T>& nd, const BoxInput& in,
@@ -242,13 +245,15 @@ int run_pass(const spk_net* cnet, int mode, int S, int precision, const BoxInput
   if (sm <= 0) return fail(SPK_ERR_CUDA, "no CUDA device");
   cudaError_t e;
   if (precision == SPK_FP64) {
-    const NetDev<double>* nd;
-    int rc = get_dev<double>(net, &nd);
+    NetDev<double> nd_copy;
+    const NetDev<double>* nd = &nd_copy;
+    int rc = get_dev<double>(net, &nd_copy);
     if (rc) return rc;
     e = dispatch_any<double>(net->mmax, mode, S, *nd, in, out, n, sm, st);
   } else {
-    const NetDev<float>* nd;
-    int rc = get_dev<float>(net, &nd);
+    NetDev<float> nd_copy;
+    const NetDev<float>* nd = &nd_copy;
+    int rc = get_dev<float>(net, &nd_copy);
     if (rc) return rc;
     // large batches of independent boxes on wide nets: Morton processing
     // order, so box groups hold neighbouring boxes and the live-row masks

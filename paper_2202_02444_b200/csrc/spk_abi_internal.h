@@ -30,6 +30,18 @@ struct BoundOutput;
 
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* where);
+// RayCastParams.__post_init__ (reference rays.py:56-71) for callers that bind
+// the C-ABI directly: params6 = t_max, sigma0, eta_plus, eta_minus, delta,
+// safety.  Written as negated comparisons so NaNs are rejected too.
+inline int check_ray_params(const double* p) {
+  if (!(p[0] > 0.0)) return fail(SPK_ERR_INVALID_PARAMETER, "t_max must be positive");
+  if (!(p[1] > 0.0)) return fail(SPK_ERR_INVALID_PARAMETER, "sigma0 must be positive");
+  if (!(p[2] > 1.0)) return fail(SPK_ERR_INVALID_PARAMETER, "eta_plus must exceed 1");
+  if (!(p[3] > 0.0 && p[3] < 1.0)) return fail(SPK_ERR_INVALID_PARAMETER, "eta_minus must lie in (0, 1)");
+  if (!(p[4] > 0.0)) return fail(SPK_ERR_INVALID_PARAMETER, "delta must be positive");
+  if (!(p[5] > 0.0 && p[5] <= 1.0)) return fail(SPK_ERR_INVALID_PARAMETER, "safety must lie in (0, 1]");
+  return SPK_OK;
+}
 int sm_count_for(int device);
 
 class DeviceGuard {
@@ -86,5 +98,5 @@ template <> inline spk::DevNet<double>& spk_net::dev<double>() { return f64; }
 
 namespace spk {
 template <typename T>
-int get_dev(::spk_net* net, const NetDev<T>** out);
+int get_dev(::spk_net* net, NetDev<T>* out);  // copies the program under net->mu
 }

@@ -1,6 +1,7 @@
 // Shared device helpers: directed-rounding arithmetic per scalar type,
 // unit roundoff constants, activation codes.  sm_100a only.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cfloat>
 #include <cuda_runtime.h>
@@ -81,6 +82,22 @@ inline double gamma_n_host(int n, bool fp32) {
   const double u = fp32 ? 5.9604644775390625e-8 : 1.1102230246251565e-16;
   const double nu = n * u;
   return (nu / (1.0 - nu)) * (1.0 + 4.0 * 2.220446049250313e-16);
+}
+
+// Opt a kernel into more than 48 KB of dynamic shared memory on the CURRENT
+// device.  The attribute is per (function, device): `done` (one static per
+// launch site) records the devices already opted in, so later launches skip
+// the call; a failure is returned and NOT cached, so a transient error is
+// retried on the next launch.
+inline cudaError_t smem_optin(const void* kfn, int bytes, std::atomic<unsigned long long>& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = dev < 64 ? (1ull << dev) : 0ull;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+  e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && bit) done.fetch_or(bit, std::memory_order_release);
+  return e;
 }
 
 }  // namespace spk

@@ -326,6 +326,7 @@ int spk_frustum_cast(const spk_net* net, int policy, int n_keep, int precision, 
   if (!net || !position3 || !frame9 || !params6 || !hit || !t_out || !steps_out)
     return fail(SPK_ERR_INVALID_PARAMETER, "null argument");
   if (net->input_dim != 3) return fail(SPK_ERR_DIMENSION, "ray casting needs a 3-d network");
+  if (int rc = check_ray_params(params6)) return rc;
   if (width < 1 || height < 1 || initial_grid < 1) return fail(SPK_ERR_INVALID_PARAMETER, "bad resolution / grid");
   if ((long long)width * height > (long long)INT32_MAX)
     return fail(SPK_ERR_UNSUPPORTED_SHAPE, "image too large for one frustum cast");

@@ -268,8 +268,9 @@ template <typename T>
 static int launch_full_t(const spk_net* cnet, const BoxInput& in, const BoundOutput& out, long long n, int s0,
                          int need, cudaStream_t st) {
   spk_net* net = const_cast<spk_net*>(cnet);
-  const NetDev<T>* nd;
-  if (int rc = get_dev<T>(net, &nd)) return rc;
+  NetDev<T> nd_copy;
+  const NetDev<T>* nd = &nd_copy;
+  if (int rc = get_dev<T>(net, &nd_copy)) return rc;
   FullParams P;
   P.mmax = net->mmax;
   switch (net->mmax) {

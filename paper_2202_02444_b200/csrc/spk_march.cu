@@ -193,6 +193,9 @@ int spk_march(const spk_net* net, int policy, int n_keep, int precision, int64_t
               const double* params6, uint8_t* hit, double* t_out, double* steps, int64_t* stats, void* stream) {
   if (!net || !params6) return fail(SPK_ERR_INVALID_PARAMETER, "null argument");
   if (net->input_dim != 3) return fail(SPK_ERR_DIMENSION, "ray casting needs a 3-d network");
+  if (int rc = check_ray_params(params6)) return rc;
+  if (origin_stride != 0 && origin_stride != 3)
+    return fail(SPK_ERR_INVALID_PARAMETER, "origin_stride must be 0 (shared origin) or 3");
   if (n <= 0) return n < 0 ? fail(SPK_ERR_DIMENSION, "negative ray count") : SPK_OK;
   if (n > (int64_t)INT32_MAX) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "too many rays in one call");
   MarchParamsDev P{params6[0], params6[1], params6[2], params6[3], params6[4], params6[5]};
@@ -245,12 +248,14 @@ int spk_march(const spk_net* net, int policy, int n_keep, int precision, int64_t
       MarchState M{cur, origins, origin_stride, dirs, t, sig, steps, hit, t_out, neg0, live, cert};
       cudaError_t ke;
       if (precision == SPK_FP64) {
-        const NetDev<double>* nd;
-        if ((rc = get_dev<double>(const_cast<spk_net*>(net), &nd)) != SPK_OK) break;
+        NetDev<double> nd_copy;
+        const NetDev<double>* nd = &nd_copy;
+        if ((rc = get_dev<double>(const_cast<spk_net*>(net), &nd_copy)) != SPK_OK) break;
         ke = dispatch_march_round<double>(net->mmax, policy == SPK_POLICY_AFFINE_FIXED, *nd, M, P, na, sm, st);
       } else {
-        const NetDev<float>* nd;
-        if ((rc = get_dev<float>(const_cast<spk_net*>(net), &nd)) != SPK_OK) break;
+        NetDev<float> nd_copy;
+        const NetDev<float>* nd = &nd_copy;
+        if ((rc = get_dev<float>(const_cast<spk_net*>(net), &nd_copy)) != SPK_OK) break;
         ke = dispatch_march_round<float>(net->mmax, policy == SPK_POLICY_AFFINE_FIXED, *nd, M, P, na, sm, st);
       }
       if (ke != cudaSuccess) { rc = cuda_fail(ke, "march round"); break; }

@@ -125,12 +125,8 @@ cudaError_t launch_march_round(const NetDev<T>& net, const MarchState& M, const 
                                int sm_count, cudaStream_t stream) {
   using CF = Cfg<T, C, MMAX>;
   auto kfn = march_round_kernel<T, C, MMAX, MODE>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
-  });
-  if (attr_err != cudaSuccess) return attr_err;
+  static std::atomic<unsigned long long> optin{0};
+  if (cudaError_t e = smem_optin((const void*)kfn, (int)CF::SMEM, optin)) return e;
   if (n <= 0) return cudaSuccess;
   const long long nbt = (n + CF::NB - 1) / CF::NB;
   const long long slots = (long long)sm_count * CF::MINB;

@@ -236,6 +236,9 @@ int spk_render_shade(const spk_net* net, int precision, int64_t n, const double*
   if (!net || !light3 || !background3 || (n > 0 && (!origins || !dirs || !hit || !t || !pixels)))
     return fail(SPK_ERR_INVALID_PARAMETER, "null argument");
   if (net->input_dim != 3) return fail(SPK_ERR_DIMENSION, "rendering needs a 3-d network");
+  if (origin_stride != 0 && origin_stride != 3)
+    return fail(SPK_ERR_INVALID_PARAMETER, "origin_stride must be 0 (shared origin) or 3");
+  if (!(delta > 0.0)) return fail(SPK_ERR_INVALID_PARAMETER, "delta must be positive");
   if (n < 0 || iters < 0) return fail(SPK_ERR_DIMENSION, "negative size");
   if (n > (int64_t)INT32_MAX / 6) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "too many pixels in one call");
   if (n == 0) {
@@ -293,6 +296,9 @@ int spk_fixed_step_march(const spk_net* net, int precision, int64_t n, const dou
   if (!net || (n > 0 && (!origins || !dirs || !hit || !t_out)))
     return fail(SPK_ERR_INVALID_PARAMETER, "null argument");
   if (!(step > 0.0)) return fail(SPK_ERR_INVALID_PARAMETER, "fixed_step mode needs a positive step");
+  if (!(t_max > 0.0)) return fail(SPK_ERR_INVALID_PARAMETER, "t_max must be positive");
+  if (origin_stride != 0 && origin_stride != 3)
+    return fail(SPK_ERR_INVALID_PARAMETER, "origin_stride must be 0 (shared origin) or 3");
   if (net->input_dim != 3) return fail(SPK_ERR_DIMENSION, "ray casting needs a 3-d network");
   if (n < 0) return fail(SPK_ERR_DIMENSION, "negative ray count");
   if (n > (int64_t)INT32_MAX) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "too many rays in one call");

@@ -61,12 +61,14 @@ static int run_sym(const spk_net* cnet, int policy, int n_keep, int precision, c
   if (sm <= 0) return fail(SPK_ERR_CUDA, "no CUDA device");
   cudaError_t e;
   if (precision == SPK_FP64) {
-    const NetDev<double>* nd;
-    if (int rc = get_dev<double>(net, &nd)) return rc;
+    NetDev<double> nd_copy;
+    const NetDev<double>* nd = &nd_copy;
+    if (int rc = get_dev<double>(net, &nd_copy)) return rc;
     e = sym_any<double>(net->mmax, kc, *nd, in, out, n, P, sm, st);
   } else {
-    const NetDev<float>* nd;
-    if (int rc = get_dev<float>(net, &nd)) return rc;
+    NetDev<float> nd_copy;
+    const NetDev<float>* nd = &nd_copy;
+    if (int rc = get_dev<float>(net, &nd_copy)) return rc;
     e = sym_any<float>(net->mmax, kc, *nd, in, out, n, P, sm, st);
   }
   if (e != cudaSuccess) return cuda_fail(e, "symbolic kernel launch");

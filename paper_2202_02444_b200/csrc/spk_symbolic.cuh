@@ -335,12 +335,8 @@ cudaError_t launch_sym(const NetDev<T>& net, const BoxInput& in, const BoundOutp
                        const SymParams& P, int sm_count, cudaStream_t stream) {
   using SC = SymCfg<T, KC, MMAX>;
   auto kfn = sym_bound_kernel<T, KC, MMAX>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SC::SMEM);
-  });
-  if (attr_err != cudaSuccess) return attr_err;
+  static std::atomic<unsigned long long> optin{0};
+  if (cudaError_t e = smem_optin((const void*)kfn, (int)SC::SMEM, optin)) return e;
   if (n <= 0) return cudaSuccess;
   const long long nbt = (n + SC::NB - 1) / SC::NB;
   const int grid = (int)(nbt < sm_count ? nbt : sm_count);

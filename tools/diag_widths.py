@@ -1,4 +1,8 @@
-"""Diagnostics printed on the GPU box (always passes when kernels run)."""
+"""Diagnostic (not a test): FP32 vs FP64 vs oracle bound statistics on
+3-layer width-256/512 nets, printed on the GPU box:
+
+    python -m pytest tools/diag_widths.py -s
+"""
 
 import numpy as np
 import pytest
@@ -7,7 +11,6 @@ import paper_2202_02444_b200 as sp
 from oracle import spelunk_oracle as orc
 from paper_2202_02444_b200 import synth
 
-pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("width", [256, 512])
