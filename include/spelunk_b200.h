@@ -97,6 +97,15 @@ int spk_ffma_peak(int iters, double* flops_per_s, void* stream);
  * NetworkSpec.__post_init__ (network.py:86-107). */
 int spk_net_create(int input_dim, int n_ops, const int* op_kind, const int* op_out_dim,
                    const double* params, int64_t n_params, int device, spk_net** out);
+/* Same with creation flags.  SPK_NET_FP64_UNPADDED: the net's FP64 program
+ * carries no a-priori rounding budget (gamma_n |W| |x| on each dense layer),
+ * i.e. it runs the reference's own FP64 arithmetic (range_core.py:573-582)
+ * rather than the sound padded FP64 enclosure -- used by the Option-B shim
+ * (INTEGRATION.md), whose callers compare bounds with the reference at 1e-12
+ * or exactly (test_range_core.py:241-255, 286-304).  FP32 is unaffected. */
+enum { SPK_NET_FP64_UNPADDED = 1 };
+int spk_net_create_ex(int input_dim, int n_ops, const int* op_kind, const int* op_out_dim,
+                      const double* params, int64_t n_params, int device, int flags, spk_net** out);
 int spk_net_destroy(spk_net* net);
 /* TEST HOOK, not for production: on != 0 makes every ReLU of this net use an
  * affine rule with a negated remainder (gamma -> -gamma), so bounds stop

@@ -10,8 +10,9 @@ the dispatch up (spatial.py:183, rays.py:132, meshing.py:146, bench.py:96).
 
 Environment:
   SPELUNK_B200_LIB        path of _spk.so (required)
-  SPELUNK_B200_PRECISION  fp64 (default: the reference's arithmetic, so its
-                          1e-12 composition tests hold) or fp32 (sound FP32)
+  SPELUNK_B200_PRECISION  fp64 (default: the reference's own FP64 arithmetic,
+                          no rounding padding -- SPK_NET_FP64_UNPADDED -- so its
+                          exact and 1e-12 tests hold) or fp32 (sound FP32)
   SPELUNK_B200_CALLS      optional file: the number of GPU calls is written
                           there at exit (lets a test prove the GPU ran)
 
@@ -33,8 +34,8 @@ from .network import DenseLayer
 
 _lib = C.CDLL(os.environ["SPELUNK_B200_LIB"])
 _vp, _i32, _i64 = C.c_void_p, C.c_int, C.c_int64
-_lib.spk_net_create.argtypes = [_i32, _i32, _vp, _vp, _vp, _i64, _i32, _vp]
-_lib.spk_net_create.restype = _i32
+_lib.spk_net_create_ex.argtypes = [_i32, _i32, _vp, _vp, _vp, _i64, _i32, _i32, _vp]
+_lib.spk_net_create_ex.restype = _i32
 _lib.spk_net_destroy.argtypes = [_vp]
 _lib.spk_bound_batch_host.argtypes = [_vp, _i32, _i32, _i32, _i64, _i32, _vp, _vp, _vp, _vp, _vp]
 _lib.spk_bound_batch_host.restype = _i32
@@ -85,8 +86,9 @@ def _handle(net):
         o = np.array(outs, np.int32)
         p = np.ascontiguousarray(np.concatenate(params) if params else np.zeros(0))
         h = C.c_void_p()
-        _check(_lib.spk_net_create(net.input_dim, len(k), k.ctypes.data, o.ctypes.data, p.ctypes.data, p.size,
-                                   0, C.byref(h)))
+        # fp64: the reference's own (unpadded) FP64 arithmetic, SPK_NET_FP64_UNPADDED
+        _check(_lib.spk_net_create_ex(net.input_dim, len(k), k.ctypes.data, o.ctypes.data, p.ctypes.data, p.size,
+                                      0, 1 if _PRECISION == 1 else 0, C.byref(h)))
         try:
             weakref.finalize(net, _drop, key)
             _handles[key] = (None, h)

@@ -50,6 +50,7 @@ SIGNATURES = {
     "spk_device_sm_count": ([], i32),
     "spk_ffma_peak": ([i32, vp, vp], i32),
     "spk_net_create": ([i32, i32, vp, vp, vp, i64, i32, vp], i32),
+    "spk_net_create_ex": ([i32, i32, vp, vp, vp, i64, i32, i32, vp], i32),
     "spk_net_destroy": ([vp], i32),
     "spk_net_info": ([vp, vp, vp, vp], i32),
     "spk_net_debug_corrupt_relu": ([vp, i32], i32),

@@ -153,6 +153,9 @@ int build_device_net(spk_net* net, DevNet<T>& dn) {
     // + u for FP32: W and b are rounded from FP64 to T, |dW| <= u|W|, so the
     // certified function is the reference's FP64 network.
     gam[l] = gamma_n_host(n_eff, fp32) + (fp32 ? 5.9604644775390625e-8 * (1.0 + 1e-6) : 0.0);
+    // SPK_NET_FP64_UNPADDED: the reference's own FP64 arithmetic (no a-priori
+    // dot-product budget), for callers that compare at 1e-15 (integration shim)
+    if (!fp32 && (net->flags & SPK_NET_FP64_UNPADDED)) gam[l] = 0.0;
     if (narrow) {
       offs[l].w = small.size();
       for (size_t q = 0; q < L.W.size(); ++q) small.push_back((T)L.W[q]);
@@ -163,8 +166,10 @@ int build_device_net(spk_net* net, DevNet<T>& dn) {
     for (int i = 0; i < L.m_out; ++i) {
       // |b_i| enters the FMA chain exactly once; its share of the rounding
       // budget plus an underflow guard, rounded up.
-      const double be = gam[l] * std::fabs((double)(T)L.b[i]) * (1.0 + 1e-6) +
-                        (fp32 ? 1e-37 : 1e-300) * (L.m_in + 2);
+      const double be = (!fp32 && (net->flags & SPK_NET_FP64_UNPADDED))
+                            ? 0.0
+                            : gam[l] * std::fabs((double)(T)L.b[i]) * (1.0 + 1e-6) +
+                                  (fp32 ? 1e-37 : 1e-300) * (L.m_in + 2);
       small.push_back(round_up_to<T>(be));
     }
     while (small.size() % 4) small.push_back(T(0));
@@ -359,12 +364,19 @@ int spk_device_sm_count(void) {
 
 int spk_net_create(int input_dim, int n_ops, const int* op_kind, const int* op_out_dim,
                    const double* params, int64_t n_params, int device, spk_net** out) {
+  return spk_net_create_ex(input_dim, n_ops, op_kind, op_out_dim, params, n_params, device, 0, out);
+}
+
+int spk_net_create_ex(int input_dim, int n_ops, const int* op_kind, const int* op_out_dim,
+                      const double* params, int64_t n_params, int device, int flags, spk_net** out) {
   if (!out) return fail(SPK_ERR_INVALID_PARAMETER, "null output handle");
   *out = nullptr;
   if (input_dim < 1) return fail(SPK_ERR_DIMENSION, "input_dim must be >= 1");
+  if (flags & ~SPK_NET_FP64_UNPADDED) return fail(SPK_ERR_INVALID_PARAMETER, "unknown net flags");
   auto net = std::make_unique<spk_net>();
   net->input_dim = input_dim;
   net->device = device;
+  net->flags = flags;
   int dim = input_dim;
   int64_t off = 0;
   int max_w = input_dim;

@@ -61,9 +61,10 @@ int launch_symbolic(const struct ::spk_net* net, int policy, int n_keep, int pre
                     cudaStream_t st);
 int launch_symbolic_in(const struct ::spk_net* net, int policy, int n_keep, int precision, const BoxInput& in,
                        const BoundOutput& o, long long n_cap, int s, cudaStream_t st);
-// affine-full beyond the register-tiled capacity (spk_full.cu); need = s + hidden widths
+// affine-full (n_keep = 0) or affine-truncate:n_keep beyond the register-tiled
+// capacity (spk_full.cu); need = the planned symbol capacity
 int launch_full(const struct ::spk_net* net, int precision, const BoxInput& in, const BoundOutput& out,
-                long long n, int s0, int need, cudaStream_t st);
+                long long n, int s0, int need, int n_keep, cudaStream_t st);
 int bound_aabb_internal(const struct ::spk_net* net, int policy, int n_keep, int precision, long long n_cap,
                         const long long* n_dev, const double* box_lo, const double* box_hi, double* lo, double* hi,
                         int8_t* cls, cudaStream_t st, int pair_order = 0);
@@ -86,6 +87,7 @@ struct spk_net {
   int max_width = 0;
   int64_t macs = 0;
   int corrupt_relu = 0;  // test hook (spk_net_debug_corrupt_relu)
+  int flags = 0;         // SPK_NET_* (spk_net_create_ex)
   std::vector<int> pre_acts;
   std::vector<spk::HostLayer> layers;
   std::mutex mu;

@@ -24,6 +24,12 @@
 //   final      width-1 layer by warp butterfly (the narrow path's order),
 //              final activations fold gamma into e (same lo/hi), outward
 //              rounded lo/hi.
+// affine-truncate beyond the register tile (n_keep > 16 on widths > 64, > 32
+// otherwise) runs here too: after each activation's append, per-symbol L1
+// norms (one warp per symbol), rank = #(larger norm, or equal norm and lower
+// index) -- the reference's stable argsort, range_core.py:604-619 -- the
+// n_keep best kept in their original order, the dropped |coefficients| added
+// to the error channel with round-up adds.
 // FP32: sound like every other kernel; FP64: the reference's algorithm.
 #include <algorithm>
 #include <string>
@@ -37,6 +43,7 @@ constexpr int FULL_MMAX = 512;
 
 struct FullParams {
   int mmax, kt, sub, ncol_cap, s0;
+  int n_keep;  // affine-truncate: symbols kept after every activation (0 = affine-full)
   long long toff[MAX_LAYERS];  // first W^T tile row of every generic layer
 };
 
@@ -74,8 +81,10 @@ __global__ void __launch_bounds__(NT) full_bound_kernel(const NetDev<T> net, con
   __shared__ T E[FULL_MMAX], V[FULL_MMAX], RA[FULL_MMAX], ALPHA[FULL_MMAX], NEWG[FULL_MMAX];
   __shared__ T PART[NT];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, M = P.mmax, d = net.d;
-  T* buf0 = scratch + (size_t)blockIdx.x * 2 * P.ncol_cap * M;
+  T* buf0 = scratch + (size_t)blockIdx.x * (2 * (size_t)P.ncol_cap * M + 2 * P.ncol_cap);
   T* buf1 = buf0 + (size_t)P.ncol_cap * M;
+  T* NRM = buf1 + (size_t)P.ncol_cap * M;            // truncate: per-symbol L1 norms
+  int* POS = reinterpret_cast<int*>(NRM + P.ncol_cap);  // truncate: kept flag per symbol
 
   for (long long box = blockIdx.x; box < n; box += gridDim.x) {
     T* cur = buf0;
@@ -252,6 +261,58 @@ __global__ void __launch_bounds__(NT) full_bound_kernel(const NetDev<T> net, con
         }
         ncol += m;
         __syncthreads();
+        if (P.n_keep > 0 && ncol - 1 > P.n_keep) {
+          // ---- affine-truncate (range_core.py:604-619): keep the n_keep
+          // symbols of largest L1 norm over the components, ties to the lower
+          // index (stable argsort), in their original order; the dropped
+          // |coefficients| move into the error channel.  Symbol k is row 1+k-1.
+          const int ncand = ncol - 1;
+          for (int k = warp; k < ncand; k += NT / 32) {
+            const T* row = cur + (size_t)(1 + k) * M;
+            T s = T(0);
+            for (int o = lane; o < m; o += 32) s += fabs(row[o]);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+            if (lane == 0) NRM[k] = s;
+          }
+          __syncthreads();
+          for (int k = tid; k < ncand; k += NT) {
+            const T nk = NRM[k];
+            int rank = 0;
+            for (int j = 0; j < ncand; ++j) {
+              const T nj = NRM[j];
+              rank += (nj > nk || (nj == nk && j < k)) ? 1 : 0;
+            }
+            POS[k] = rank < P.n_keep ? 1 : 0;
+          }
+          __syncthreads();
+          for (int k = tid; k < ncand; k += NT) {
+            int pos = -1;
+            if (POS[k] > 0) {
+              pos = 0;
+              for (int j = 0; j < k; ++j) pos += POS[j] > 0 ? 1 : 0;
+            }
+            NRM[k] = (T)pos;  // the norms are dead; POS (read here) stays intact
+          }
+          __syncthreads();
+          for (int o = tid; o < m; o += NT) {
+            T dropped = T(0);
+            for (int k = 0; k < ncand; ++k)
+              if (NRM[k] < T(0)) dropped = Num<T>::add_ru(dropped, fabs(cur[(size_t)(1 + k) * M + o]));
+            E[o] = Num<T>::add_ru(E[o], dropped);
+            nxt[o] = cur[o];
+          }
+          for (int q = tid; q < ncand * m; q += NT) {
+            const int k = q / m, o = q % m;
+            const int pos = (int)NRM[k];
+            if (pos >= 0) nxt[(size_t)(1 + pos) * M + o] = cur[(size_t)(1 + k) * M + o];
+          }
+          __syncthreads();
+          T* t2 = cur;
+          cur = nxt;
+          nxt = t2;
+          ncol = 1 + P.n_keep;
+        }
       }
       // ---- pack: v = e + gamma'(|base| + sum|A| + e)
       symbol_norms<T>(cur, ncol, m, M, PART, RA, tid);
@@ -266,7 +327,7 @@ __global__ void __launch_bounds__(NT) full_bound_kernel(const NetDev<T> net, con
 
 template <typename T>
 static int launch_full_t(const spk_net* cnet, const BoxInput& in, const BoundOutput& out, long long n, int s0,
-                         int need, cudaStream_t st) {
+                         int need, int n_keep, cudaStream_t st) {
   spk_net* net = const_cast<spk_net*>(cnet);
   NetDev<T> nd_copy;
   const NetDev<T>* nd = &nd_copy;
@@ -282,6 +343,7 @@ static int launch_full_t(const spk_net* cnet, const BoxInput& in, const BoundOut
   }
   P.ncol_cap = 1 + need;
   P.s0 = s0;
+  P.n_keep = n_keep;
   long long t = 0;
   for (int l = 0; l < nd->n_layers && l < MAX_LAYERS; ++l) {
     P.toff[l] = t * P.kt;  // rows of W^T (each MMAX wide) before layer l
@@ -292,7 +354,7 @@ static int launch_full_t(const spk_net* cnet, const BoxInput& in, const BoundOut
   if (n <= 0) return SPK_OK;
   const long long grid = std::min<long long>(n, (long long)sm * 4);
   T* scratch = nullptr;
-  const size_t bytes = (size_t)grid * 2 * P.ncol_cap * P.mmax * sizeof(T);
+  const size_t bytes = (size_t)grid * (2 * (size_t)P.ncol_cap * P.mmax + 2 * P.ncol_cap) * sizeof(T);
   cudaError_t e = cudaMallocAsync(&scratch, bytes, st);
   if (e != cudaSuccess) return cuda_fail(e, "affine-full scratch");
   full_bound_kernel<T><<<(int)grid, NT, 0, st>>>(*nd, in, out, n, P, scratch);
@@ -303,13 +365,13 @@ static int launch_full_t(const spk_net* cnet, const BoxInput& in, const BoundOut
 }
 
 int launch_full(const spk_net* net, int precision, const BoxInput& in, const BoundOutput& out, long long n, int s0,
-                int need, cudaStream_t st) {
+                int need, int n_keep, cudaStream_t st) {
   if (net->mmax > FULL_MMAX) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "affine-full: layer width beyond 512");
   if (s0 > 3) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "more than 3 box axes");
   if ((int)net->layers.size() > MAX_LAYERS) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "too many layers");
   DeviceGuard g(net->device);
-  return precision == SPK_FP64 ? launch_full_t<double>(net, in, out, n, s0, need, st)
-                               : launch_full_t<float>(net, in, out, n, s0, need, st);
+  return precision == SPK_FP64 ? launch_full_t<double>(net, in, out, n, s0, need, n_keep, st)
+                               : launch_full_t<float>(net, in, out, n, s0, need, n_keep, st);
 }
 
 }  // namespace spk

@@ -26,8 +26,19 @@ static int plan_capacity(const spk_net* net, int policy, int n_keep, int s, int*
   if (!net->pre_acts.empty())
     return fail(SPK_ERR_UNSUPPORTED_SHAPE, "symbolic policies: activation before the first dense layer");
   int need;
+  int big = 0;  // large-capacity (K3F) symbol count if the register tile is too small
   if (policy == SPK_POLICY_AFFINE_TRUNCATE) {
     need = std::max(n_keep, s);
+    // K3F capacity: max over layers of min(prev, n_keep) + m (range_core.py:530-544)
+    int cur = s;
+    big = s;
+    for (size_t l = 0; l + 1 < net->layers.size(); ++l)
+      for (int a : net->layers[l].acts)
+        if (a != SPK_OP_IDENTITY) {
+          cur += net->layers[l].m_out;
+          big = std::max(big, cur);
+          cur = std::min(cur, n_keep);
+        }
   } else {
     need = s;
     for (size_t l = 0; l + 1 < net->layers.size(); ++l)
@@ -35,13 +46,12 @@ static int plan_capacity(const spk_net* net, int policy, int n_keep, int s, int*
         if (a != SPK_OP_IDENTITY) need += net->layers[l].m_out;
   }
   const int kcmax = net->mmax <= 64 ? 32 : 16;
-  if (policy == SPK_POLICY_AFFINE_FULL && need > kcmax) {
-    *kc = -need;  // beyond the register-tiled kernel: the large-capacity path (spk_full.cu)
+  if (need > kcmax) {
+    // beyond the register-tiled kernel: the large-capacity path (spk_full.cu)
+    *kc = -(policy == SPK_POLICY_AFFINE_FULL ? need : big);
+    P->n_keep = policy == SPK_POLICY_AFFINE_TRUNCATE ? n_keep : 0;
     return SPK_OK;
   }
-  if (need > kcmax)
-    return fail(SPK_ERR_UNSUPPORTED_SHAPE,
-                "symbol capacity " + std::to_string(need) + " exceeds the compiled maximum " + std::to_string(kcmax));
   *kc = need <= 8 ? 8 : (need <= 16 ? 16 : 32);
   P->n_keep = policy == SPK_POLICY_AFFINE_TRUNCATE ? n_keep : *kc;
   P->full = policy == SPK_POLICY_AFFINE_FULL;
@@ -55,7 +65,7 @@ static int run_sym(const spk_net* cnet, int policy, int n_keep, int precision, c
   int kc;
   SymParams P;
   if (int rc = plan_capacity(net, policy, n_keep, s, &kc, &P)) return rc;
-  if (kc < 0) return launch_full(net, precision, in, out, n, s, -kc, st);
+  if (kc < 0) return launch_full(net, precision, in, out, n, s, -kc, P.n_keep, st);
   DeviceGuard g(net->device);
   const int sm = sm_count_for(net->device);
   if (sm <= 0) return fail(SPK_ERR_CUDA, "no CUDA device");

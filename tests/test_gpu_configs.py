@@ -17,7 +17,8 @@ C4  ELU 3->8x512->1, extract_mesh (meshing.py:111-169), dense_levels=3,
     signs agree between FP32 and FP64 evaluation are identical.
 C5  4096 cubes of half-extent 1/64, 8-layer width-64 and width-512 ReLU nets,
     centres from the on-device C5 stream: range_bound_batch
-    (range_core.py:547-642).  FP64 within 1e-10 * S of the reference; FP32
+    (range_core.py:547-642).  FP64 contains the reference and is within
+    1e-8 * S of it (the sound FP64 padding; see the test); FP32
     contains the reference's FP64 enclosure and stays within the band stated
     in C5_BAND; labels equal wherever both sides are definite.
 """
@@ -191,7 +192,12 @@ def test_c5_bounds_match_reference(gold, tag, policy):
     wl, wh = gold[f"{tag}/{policy}/lo"], gold[f"{tag}/{policy}/hi"]
     s = np.maximum(1.0, np.maximum(np.abs(wl), np.abs(wh)))
     lo64, hi64 = sp.range_bound_batch(net, c, _c5_axes(len(c)), policy, precision="fp64")
-    assert np.max(np.abs(lo64 - wl) / s) <= 1e-10 and np.max(np.abs(hi64 - wh) / s) <= 1e-10
+    # the FP64 kernels are padded by the FP64 dot-product budget gamma_n |W| |x|
+    # (sound, unlike the reference's FP64); on 8 non-cancelling affine-fixed
+    # layers that padding grows to 2.4e-9 * S (measured, C5_512), so: contain
+    # the reference up to its own rounding, and stay within 1e-8 * S of it
+    assert np.all(lo64 <= wl + 1e-12 * s) and np.all(hi64 >= wh - 1e-12 * s)
+    assert np.max(np.abs(lo64 - wl) / s) <= 1e-8 and np.max(np.abs(hi64 - wh) / s) <= 1e-8
     # FP32 through the on-device C5 stream (the bench path), same seed
     lo, hi, cls = sp.bound_random_cubes(net, len(c), seed=5, half=1.0 / 64, policy=policy)
     lo, hi, cls = lo.cpu().numpy(), hi.cpu().numpy(), cls.cpu().numpy()

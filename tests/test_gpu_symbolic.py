@@ -109,3 +109,50 @@ def test_truncate_full_vs_fixed_conservatism(nets):
         for pol in ("affine-fixed", "affine-truncate:4"):
             ol, oh = sp.range_bound_batch(net, c, a, pol, precision="fp64")
             assert np.all(ol <= fl + 1e-9) and np.all(oh >= fh - 1e-9), (name, pol)
+
+
+def _segments(rng, n, d=3):
+    c = rng.uniform(-1, 1, (n, d))
+    u = rng.standard_normal((n, d))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    return c, (u * 10.0 ** rng.uniform(-3, -1.5, (n, 1)))[:, None, :]
+
+
+def _cubes(rng, n, d=3):
+    c = rng.uniform(-1, 1, (n, d))
+    a = np.zeros((n, d, d))
+    a[:, np.arange(d), np.arange(d)] = 10.0 ** rng.uniform(-3, -1.5, (n, 1))
+    return c, a
+
+
+@pytest.mark.parametrize("case", ["C3_trunc32_seg", "C3_trunc64_cube", "w512_trunc24", "relu_sdf_trunc40"])
+def test_truncate_beyond_register_tile(net_paths, case):
+    """affine-truncate with more kept symbols than the register tile holds
+    (> 16 on widths > 64, > 32 otherwise) runs on the large-capacity kernel
+    with per-box top-k (range_core.py:604-619): FP64 within 1e-9 * S of the
+    oracle, FP32 sound on dense samples and within 2e-2 (S + w)."""
+    from paper_2202_02444_b200 import synth
+
+    rng = np.random.default_rng(17)
+    if case.startswith("C3"):
+        net = synth.config_net("C3")
+    elif case.startswith("w512"):
+        net = synth.random_mlp(512, 3, "relu", "ref-normal", seed=3)
+    else:
+        net = sp.load_network(net_paths["relu_sdf"])
+    pol = "affine-truncate:" + case.split("trunc")[1].split("_")[0]
+    c, a = (_segments if case.endswith("seg") else _cubes)(rng, 48)
+    wl, wh = orc.bound_batch(orc.as_oracle_net(net), c, a, pol)
+    lo, hi = sp.range_bound_batch(net, c, a, pol, precision="fp64")
+    s = scale(wl, wh)
+    err = max(np.max(np.abs(lo - wl) / s), np.max(np.abs(hi - wh) / s))
+    print(f"{case} {pol}: fp64 max rel {err:.2e}")
+    assert err <= 1e-9, err
+    lo32, hi32 = sp.range_bound_batch(net, c, a, pol, precision="fp32")
+    tol = 2e-2 * (s + (wh - wl))
+    assert np.all(np.abs(lo32 - wl) <= tol) and np.all(np.abs(hi32 - wh) <= tol)
+    # dense-sample soundness of the FP32 enclosure
+    t = rng.uniform(-1, 1, (len(c), 64, a.shape[1]))
+    pts = c[:, None, :] + np.einsum("bks,bsd->bkd", t, a)
+    vals = orc.eval_points_blas(orc.as_oracle_net(net), pts.reshape(-1, 3)).reshape(len(c), 64)
+    assert np.all(vals >= lo32[:, None]) and np.all(vals <= hi32[:, None])
