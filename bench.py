@@ -22,11 +22,14 @@ stream; the max over ranks is taken.  L2 (126 MB) is flushed by writing a
 256 MB buffer before every timed step.  SM clocks and throttle reasons are
 sampled with nvidia-smi during the timed region.
 
---impl reference times the reference's own CPU algorithm (the pinned NumPy
-oracle port, oracle/spelunk_oracle.py; the reference itself is pure Python
-and cannot travel to the GPU box) on all host cores: P processes with one
-BLAS thread each bound 4096-box chunks of the same depth-18 level
-(spatial.py:172-186 calls range_bound_batch in 4096-box chunks).
+--impl reference times the reference's own CPU implementation on all host
+cores: the unmodified reference package staged in baseline/_ref
+(integration/stage_reference.sh; it travels to the GPU box with the repo
+snapshot) -- its range_bound_batch (range_core.py:547) -- in P processes with
+one BLAS thread each, bounding 4096-box chunks of the same depth-18 level
+(spatial.py:172-186 calls range_bound_batch in 4096-box chunks).  If
+baseline/_ref is absent it falls back to the pinned NumPy oracle port
+(oracle/spelunk_oracle.py) and says so (cpu_baseline.kind "port").
 """
 
 from __future__ import annotations
@@ -52,44 +55,75 @@ CHUNK = 4096
 
 
 # --------------------------------------------------------------------------- CPU legs
+REF_PKG = ROOT / "baseline" / "_ref"
+
+
+def reference_kind():
+    """'reference' when the unmodified reference is staged in baseline/_ref,
+    else 'port' (the pinned oracle restatement)."""
+    return "reference" if (REF_PKG / "spelunk" / "range_core.py").exists() else "port"
+
+
+def _ref_bounder(net_doc, kind):
+    """range_bound_batch(centres, axes) of the reference (or the port)."""
+    if kind == "reference":
+        if str(REF_PKG) not in sys.path:
+            sys.path.insert(0, str(REF_PKG))
+        import spelunk
+        from spelunk.network import ActivationKind, DenseLayer, NetworkSpec
+
+        layers = []
+        for L in net_doc["layers"]:
+            if L["type"] == "dense":
+                layers.append(DenseLayer(np.asarray(L["weights"], np.float64), np.asarray(L["bias"], np.float64)))
+            else:
+                layers.append(ActivationKind(L["type"] if L["type"] != "activation" else L["kind"]))
+        net = NetworkSpec(int(net_doc["input_dim"]), tuple(layers), net_doc.get("output_semantics", "sdf"),
+                          net_doc.get("name", "net"))
+        return lambda c, a: spelunk.range_bound_batch(net, c, a, spelunk.AFFINE_FIXED)
+    from oracle import spelunk_oracle as orc
+
+    onet = orc.net_from_json_doc(net_doc)
+    return lambda c, a: orc.bound_batch(onet, c, a, "affine-fixed")
+
+
 def _cpu_worker(args):
-    """One single-BLAS-thread process bounding its share of boxes (oracle port)."""
+    """One single-BLAS-thread process bounding its share of boxes."""
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     os.environ.setdefault("OMP_NUM_THREADS", "1")
-    net_doc, centers, axes, reps = args
+    net_doc, centers, axes, reps, kind = args
     try:
         from threadpoolctl import threadpool_limits
 
         lim = threadpool_limits(1)
     except Exception:  # pragma: no cover
         lim = None
-    from oracle import spelunk_oracle as orc
-
-    net = orc.net_from_json_doc(net_doc)
-    orc.bound_batch(net, centers[:64], axes[:64], "affine-fixed")  # warm
+    bound = _ref_bounder(net_doc, kind)
+    bound(centers[:64], axes[:64])  # warm
     t0 = time.perf_counter()
     for _ in range(reps):
         for s in range(0, len(centers), CHUNK):
-            orc.bound_batch(net, centers[s : s + CHUNK], axes[s : s + CHUNK], "affine-fixed")
+            bound(centers[s : s + CHUNK], axes[s : s + CHUNK])
     dt = time.perf_counter() - t0
     del lim
     return len(centers) * reps, dt
 
 
 class CpuPool:
-    def __init__(self, procs):
+    def __init__(self, procs, kind):
         import multiprocessing as mp
 
         os.environ["OPENBLAS_NUM_THREADS"] = "1"
         os.environ["OMP_NUM_THREADS"] = "1"
         self.procs = procs
+        self.kind = kind
         self.pool = mp.get_context("spawn").Pool(procs)
 
     def run(self, net_doc, centers, axes, per_proc, reps=1):
         parts = []
         for p in range(self.procs):
             sl = slice(p * per_proc, (p + 1) * per_proc)
-            parts.append((net_doc, centers[sl], axes[sl], reps))
+            parts.append((net_doc, centers[sl], axes[sl], reps, self.kind))
         t0 = time.perf_counter()
         res = self.pool.map(_cpu_worker, parts)
         wall = time.perf_counter() - t0
@@ -132,7 +166,8 @@ def run_reference(args, rank):
     doc = network.network_to_doc(net)
     centers, axes = level18_boxes()
     model, cores = cpu_info()
-    pool = CpuPool(cores)
+    kind = reference_kind()
+    pool = CpuPool(cores, kind)
     per_proc = CHUNK
     rng = np.random.default_rng(0)
     sel = rng.permutation(len(centers))[: per_proc * cores]
@@ -146,8 +181,10 @@ def run_reference(args, rank):
         tot_time += wall
     pool.close()
     value = tot_boxes / tot_time
+    what = ("the unmodified reference's spelunk.range_bound_batch (baseline/_ref)" if kind == "reference"
+            else "the oracle port of range_bound_batch (baseline/_ref not staged)")
     sample = (f"{cores} procs x 1 BLAS thread, each one {CHUNK}-box chunk of the depth-18 level per step "
-              f"(range_bound_batch chunking of spatial.py:38); CPU {model}")
+              f"(range_bound_batch chunking of spatial.py:38) through {what}; CPU {model}")
     return {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tot_time / args.steps, "higher_is_better": True,
@@ -156,7 +193,7 @@ def run_reference(args, rank):
         "config": {"workload": "C2 k-d tree depth 18, 8x256 ReLU (torch-uniform seed 0), affine-fixed; "
                                "reference arm bounds the depth-18 level in 4096-box chunks",
                    "flush": "n/a (CPU)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -340,6 +377,8 @@ def run_ours(args, rank, world, local_rank):
                                   "levels": tree.n_levels, "complete": tree.n_nodes == 2 ** (DEPTH + 1) - 1,
                                   "collective": f"all_gather ({args.dist_backend})"}
         del tree
+        sharded["C5_8x256_16M_per_rank"] = bench_c5_sharded(torch, sp, synth, 16 << 20, rank, world, coll_dev,
+                                                             barrier, flush)
         if not args.no_rays:
             sharded["C3_siren_rays_interval_256sq_fp64"] = bench_c3_sharded(torch, sp, synth, 256, rank, world,
                                                                             coll_dev, barrier)
@@ -356,16 +395,28 @@ def run_ours(args, rank, world, local_rank):
     achieved_tf = kernel_boxes * flop_box / (kernel_ms / 1e3) / 1e12
     traffic = load_traffic().get("C2_bound_kernel_bytes_per_launch")
 
-    # ---- extra workloads (single GPU, rank 0): C5 16M cubes and C1 grid
+    # ---- extra workloads (single GPU, rank 0), each with its own clock record
     extra = {}
-    extra["C5_8x256_16M"] = bench_c5(torch, sp, synth, "C5_256", 16 << 20, flush, peak_tf)
-    extra["C1_4x32_64cubed"] = bench_c1(torch, sp, synth, flush, peak_tf)
+    gpu_idx = physical_gpu_index(local_rank)
+
+    def clocked(fn, *a):
+        with ClockSampler(gpu_idx) as ck_x:
+            out = fn(*a)
+        out["clocks"] = ck_x.summary()
+        return out
+
+    extra["C2_tree_fp64"] = clocked(bench_c2_fp64, torch, sp, spatial, net, bounds, flush)
+    extra["C5_8x256_16M"] = clocked(bench_c5, torch, sp, synth, "C5_256", 16 << 20, flush, peak_tf)
+    extra["C5_8x64_16M"] = clocked(bench_c5, torch, sp, synth, "C5_64", 16 << 20, flush, peak_tf)
+    extra["C5_8x512_4M"] = clocked(bench_c5, torch, sp, synth, "C5_512", 4 << 20, flush, peak_tf)
+    extra["C1_4x32_64cubed"] = clocked(bench_c1, torch, sp, synth, flush, peak_tf)
+    extra["host_range_bound_batch_4096"] = clocked(bench_host_calls, sp, synth)
     if not args.no_mesh:
-        extra["C4_elu8x512_mesh_256cubed"] = bench_c4(torch, sp, synth, 8)
+        extra["C4_elu8x512_mesh_256cubed"] = clocked(bench_c4, torch, sp, synth, 8)
     if not args.no_rays:
-        extra["C3_siren_rays_interval_256sq_fp64"] = bench_c3(torch, sp, synth, "interval", 256)
-        extra["C3_siren_rays_truncate16_128sq_fp64"] = bench_c3(torch, sp, synth, "affine-truncate:16", 128)
-        extra["F1_frustum_relu_sdf_1024sq"] = bench_frustum(torch, sp, 1024)
+        extra["C3_siren_rays_interval_256sq_fp64"] = clocked(bench_c3, torch, sp, synth, "interval", 256)
+        extra["C3_siren_rays_truncate16_128sq_fp64"] = clocked(bench_c3, torch, sp, synth, "affine-truncate:16", 128)
+        extra["F1_frustum_relu_sdf_1024sq"] = clocked(bench_frustum, torch, sp, 1024)
 
     # ---- e2e through the public API (host arrays out)
     e2e = bench_e2e_tree(torch, sp, spatial, net, bounds, args)
@@ -404,6 +455,48 @@ def run_ours(args, rank, world, local_rank):
         "extra": extra,
         "sharded": sharded or None,
     }
+
+
+def bench_c2_fp64(torch, sp, spatial, net, bounds, flush):
+    """The headline build with the FP64 kernels -- the reference's arithmetic
+    (sound-padded FP64; topology identical to the reference's tree)."""
+    run = lambda: spatial.build_spatial_tree_arrays(net, bounds, policy=sp.AFFINE_FIXED, max_depth=DEPTH,
+                                                    precision="fp64", to_host=False)
+    run()
+    ts = []
+    for _ in range(2):
+        dt, arr = timed(run, torch, flush, lambda: None)
+        ts.append(dt)
+    dt = float(np.median(ts))
+    return {"nodes": arr.n_nodes, "boxes_per_s": arr.n_nodes / dt, "ms": dt * 1e3,
+            "bound_kernel_ms": arr.bound_ms, "precision": "fp64"}
+
+
+def bench_host_calls(sp, synth):
+    """The reference's calling pattern through the host-array entry point
+    (spk_bound_batch_host): 4096-box chunks (spatial.py:38) of the depth-18
+    level, NumPy in / out, one caller and 8 concurrent ThreadPoolExecutor
+    callers (rays.py:170-181).  Wall clock, copies included."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    net = synth.config_net("C2")
+    c, a = level18_boxes()
+    chunks = [(c[i:i + CHUNK], a[i:i + CHUNK]) for i in range(0, 64 * CHUNK, CHUNK)]
+    for cc, aa in chunks[:4]:
+        sp.range_bound_batch(net, cc, aa, sp.AFFINE_FIXED)
+    t0 = time.perf_counter()
+    for cc, aa in chunks:
+        sp.range_bound_batch(net, cc, aa, sp.AFFINE_FIXED)
+    serial = time.perf_counter() - t0
+    with ThreadPoolExecutor(max_workers=8) as pool:
+        list(pool.map(lambda x: sp.range_bound_batch(net, x[0], x[1], sp.AFFINE_FIXED), chunks[:8]))
+        t0 = time.perf_counter()
+        list(pool.map(lambda x: sp.range_bound_batch(net, x[0], x[1], sp.AFFINE_FIXED), chunks))
+        threaded = time.perf_counter() - t0
+    n = len(chunks) * CHUNK
+    return {"calls": len(chunks), "boxes_per_call": CHUNK, "serial_ms_per_call": 1e3 * serial / len(chunks),
+            "serial_boxes_per_s": n / serial, "threads8_boxes_per_s": n / threaded,
+            "api": "range_bound_batch(net, centers[4096,3], axes[4096,3,3], AFFINE_FIXED) with NumPy arrays"}
 
 
 def bench_c5(torch, sp, synth, tag, n, flush, peak_tf):
@@ -500,6 +593,27 @@ def bench_c3_sharded(torch, sp, synth, res, rank, world, coll_dev, barrier):
             "parallelism": f"pixel tiles 16x16 interleaved x{world}"}
 
 
+def bench_c5_sharded(torch, sp, synth, n_per_rank, rank, world, coll_dev, barrier, flush):
+    """C5 sharded by contiguous index ranges of the on-device cube stream
+    (rank r bounds cubes [r*n, (r+1)*n): first_index), no collective in the
+    data path -- weak scaling; boxes/s over the max rank time."""
+    from paper_2202_02444_b200.shard import reduce_time_units
+
+    net = synth.config_net("C5_256")
+    out = tuple(torch.empty(n_per_rank, dtype=dt, device="cuda")
+                for dt in (torch.float64, torch.float64, torch.int8))
+    run = lambda: sp.bound_random_cubes(net, n_per_rank, seed=1, half=1.0 / 64, first_index=rank * n_per_rank,
+                                        out=out)
+    run()
+    ts = []
+    for _ in range(2):
+        dt, _ = timed(run, torch, flush, barrier)
+        ts.append(dt)
+    dt, n = reduce_time_units(float(np.median(ts)), float(n_per_rank), device=coll_dev)
+    return {"boxes": int(n), "boxes_per_s": n / dt, "ms": dt * 1e3, "scaling": "weak",
+            "parallelism": f"contiguous first_index ranges x{world}"}
+
+
 def bench_frustum(torch, sp, res):
     """§8(f1): cast_frustum_image (rays.py:232-341) vs per-pixel casting on the
     reference's trained relu_sdf fixture (tests/golden/nets, 7x32), default
@@ -583,13 +697,15 @@ def cpu_baseline(sp):
     model, cores = cpu_info()
     per_proc = 2 * CHUNK
     sel = np.random.default_rng(1).permutation(len(centers))[: per_proc * cores]
-    pool = CpuPool(cores)
+    kind = reference_kind()
+    pool = CpuPool(cores, kind)
     pool.run(doc, centers[sel][: cores * 64], axes[sel][: cores * 64], 64)  # spawn + import warm-up
     boxes, busy, wall = pool.run(doc, centers[sel], axes[sel], per_proc)
     pool.close()
-    return {"value": boxes / wall, "unit": UNIT, "cores": cores, "kind": "port",
+    what = "reference spelunk.range_bound_batch (baseline/_ref)" if kind == "reference" else "oracle port"
+    return {"value": boxes / wall, "unit": UNIT, "cores": cores, "kind": kind,
             "sample": f"{boxes} depth-18 boxes ({cores} procs x {per_proc}, 4096-box chunks, 1 BLAS thread each), "
-                      f"affine-fixed 8x256, oracle port of range_bound_batch; CPU {model}; wall {wall:.1f}s"}
+                      f"affine-fixed 8x256, {what}; CPU {model}; wall {wall:.1f}s"}
 
 
 def main():

@@ -106,6 +106,10 @@ static void recode_acts(spk_net* net, DevNet<T>& dn) {
     for (int a = 0; a < dn.nd.L[l].n_act; ++a) dn.nd.L[l].act[a] = act_code(net, net->layers[l].acts[a]);
 }
 
+#ifndef SPK_RUNERR_LAYERS
+#define SPK_RUNERR_LAYERS 1  // leading wide layers on the running-error K loop (FP32)
+#endif
+
 // Build the device program for one precision (lazily, once per net).
 template <typename T>
 int build_device_net(spk_net* net, DevNet<T>& dn) {
@@ -156,6 +160,11 @@ int build_device_net(spk_net* net, DevNet<T>& dn) {
     // SPK_NET_FP64_UNPADDED: the reference's own FP64 arithmetic (no a-priori
     // dot-product budget), for callers that compare at 1e-15 (integration shim)
     if (!fp32 && (net->flags & SPK_NET_FP64_UNPADDED)) gam[l] = 0.0;
+#ifdef SPK_DEBUG_GAMMA_KEEP_MASK
+    // measurement-only builds (tools/build_variant.py): UNSOUND, attributes the
+    // FP32 enclosure excess to the rounding budgets of individual layers
+    if (fp32 && !((SPK_DEBUG_GAMMA_KEEP_MASK >> l) & 1)) gam[l] = 0.0;
+#endif
     if (narrow) {
       offs[l].w = small.size();
       for (size_t q = 0; q < L.W.size(); ++q) small.push_back((T)L.W[q]);
@@ -191,6 +200,16 @@ int build_device_net(spk_net* net, DevNet<T>& dn) {
   nd.wtiles = d_tiles;
   nd.tiles_per_pass = (int)(tiles.size() / (size_t)tile);
   nd.gamma_first = round_up_to<T>(gam.empty() ? 0.0 : gam[0]);
+  // which generic layers run the running-error K loop (FP32 affine passes)
+  std::vector<int> runerr(net->layers.size(), 0);
+  for (size_t l = 0, k = 0; l < net->layers.size() && (int)k < SPK_RUNERR_LAYERS; ++l) {
+    const bool narrow = (l + 1 == net->layers.size()) && net->layers[l].m_out <= NARROW_MAX;
+    if (!narrow && net->layers[l].m_in >= 64) {
+      runerr[l] = 1;
+      ++k;
+    }
+  }
+  auto run_layer = [&](size_t l) { return SPK_RUNERR && runerr[l] != 0; };
   for (size_t l = 0; l < net->layers.size(); ++l) {
     const HostLayer& L = net->layers[l];
     LayerDev<T>& D = nd.L[l];
@@ -204,6 +223,14 @@ int build_device_net(spk_net* net, DevNet<T>& dn) {
     D.bias = d_small + offs[l].b;
     D.berr = d_small + offs[l].be;
     D.gamma_next = (l + 1 < net->layers.size()) ? round_up_to<T>(gam[l + 1]) : T(0);
+    // running-error K loops (FP32, spk_pass.cuh dense_kloop_f32): the first
+    // SPK_RUNERR_LAYERS generic layers with >= 64 inputs bound their base
+    // column's FMA rounding a posteriori, so the pack feeding them charges only
+    // the weights' FP64 -> T rounding (u |W| |base|) a priori
+    D.runerr = fp32 && run_layer(l) ? 1 : 0;
+    D.gamma_base_next = (fp32 && l + 1 < net->layers.size() && run_layer(l + 1))
+                            ? round_up_to<T>(5.9604644775390625e-8 * (1.0 + 1e-6))
+                            : D.gamma_next;
   }
   dn.nd = nd;
   dn.tiles = d_tiles;

@@ -78,6 +78,15 @@ constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reducti
 #ifndef SPK_TEAM_MIN_NS
 #define SPK_TEAM_MIN_NS 4  // ring depth from which layer boundaries are team-local
 #endif
+#ifndef SPK_RUNERR
+#define SPK_RUNERR 1  // FP32 affine K loops: running (a-posteriori) rounding bound of the base column
+#endif
+#ifndef SPK_FUSED_RELU
+#define SPK_FUSED_RELU 1  // affine-fixed ReLU layers: fused rule + pack, straddle branch behind a warp vote
+#endif
+#ifndef SPK_FUSED_RELU_VOTE
+#define SPK_FUSED_RELU_VOTE 0  // the straddle branch behind a warp vote (measured: predicated is 2-4% faster)
+#endif
 #ifndef SPK_PACKED_F32
 #define SPK_PACKED_F32 1  // FP32 K loop on FFMA2 (sm_100a packed f32x2)
 #endif
@@ -107,6 +116,9 @@ struct LayerDev {
   const T* bias;     // m_out
   const T* berr;     // m_out: rounding budget of the bias term, rounded up
   T gamma_next;      // rounding budget factor of the NEXT dense layer (0 after the last)
+  T gamma_base_next; // the same for |base| when the next layer's K loop bounds the base
+                     // column's rounding a posteriori (runerr): weight rounding only
+  int runerr;        // FP32 affine K loops: this layer runs the running-error form
 };
 
 template <typename T>
@@ -420,7 +432,7 @@ SPK_DEV void apply_act(State<T, C, MODE>& st, int act) {
 }
 // Column values handed to the next dense layer.
 template <typename T, int C, int MODE>
-SPK_DEV void pack_next(const State<T, C, MODE>& st, T gamma_next, T* out) {
+SPK_DEV void pack_next(const State<T, C, MODE>& st, T gamma_next, T* out, T gamma_base = T(-1)) {
   constexpr int BM = bound_mode(MODE), OFF = pv_off(MODE);
   if (MODE >= MODE_MI) out[0] = st.pv;
   out[OFF] = st.base;
@@ -432,8 +444,63 @@ SPK_DEV void pack_next(const State<T, C, MODE>& st, T gamma_next, T* out) {
     const T rA = sum_abs_A(st);
 #pragma unroll
     for (int j = 0; j < State<T, C, MODE>::S; ++j) out[OFF + 1 + j] = st.A[j];
-    out[C - 1] = Num<T>::fma_ru(gamma_next, Num<T>::add_ru(Num<T>::add_ru(fabs(st.base), rA), st.e), st.e);
+    if (gamma_base >= T(0)) {
+      // the next K loop bounds the base column's FMA rounding itself (RUNERR):
+      // only the weights' FP64 -> T rounding is charged on |base| here
+      out[C - 1] = Num<T>::fma_ru(gamma_next, Num<T>::add_ru(rA, st.e), Num<T>::fma_ru(gamma_base, fabs(st.base), st.e));
+    } else {
+      out[C - 1] = Num<T>::fma_ru(gamma_next, Num<T>::add_ru(Num<T>::add_ru(fabs(st.base), rA), st.e), st.e);
+    }
   }
+}
+
+// ReLU rule + pack for the next layer, fused (affine-fixed layers whose only
+// activation is ReLU -- the hot epilogue).  Identical to apply_act(ACT_RELU)
+// followed by pack_next on active (lo >= 0) and inactive (hi <= 0) neurons,
+// which take a short select-only path; straddling neurons (the only ones
+// that need the slope division and the remainder / rounding terms) run in a
+// branch guarded by a warp vote, so a warp without a straddling (neuron,
+// box) skips it.  Returns whether the packed columns can be nonzero (the
+// live-row mask bit): inactive neurons pack exact (+-)zeros.
+template <typename T, int C, int MODE>
+SPK_DEV bool relu_affine_pack(State<T, C, MODE>& st, T gamma_next, T* out, T gamma_base = T(-1)) {
+  constexpr int S = State<T, C, MODE>::S;
+  const T rA = sum_abs_A(st);
+  const T r = Num<T>::add_ru(rA, st.e);
+  const T lo = Num<T>::sub_rd(st.base, r), hi = Num<T>::add_ru(st.base, r);
+  const bool on = lo >= T(0), off = hi <= T(0), mix = !(on || off);
+  // on: (1, 0, 0) leaves the state exactly as it is; off: everything 0
+  T nb = on ? st.base : T(0);
+  T e = on ? st.e : T(0);
+  T rA2 = on ? rA : T(0);
+  // (straddling lanes keep A for the scaling below)
+#pragma unroll
+  for (int j = 0; j < S; ++j) st.A[j] = off ? Num<T>::mul_rn(T(0), st.A[j]) : st.A[j];
+  if (SPK_FUSED_RELU_VOTE ? __any_sync(__activemask(), mix) : true) {
+    if (mix) {
+      T a = fmin(fmax(Num<T>::div_fast(hi, hi - lo), T(0)), T(1));
+      const T ru = fmax(Num<T>::mul_ru(-a, lo), Num<T>::fma_ru(-a, hi, hi));
+      const T b = Num<T>::mul_rn(ru, T(0.5));
+      const T g = fmax(b, Num<T>::sub_ru(ru, b));
+      nb = Num<T>::fma_rn(a, st.base, b);
+#pragma unroll
+      for (int j = 0; j < S; ++j) st.A[j] = Num<T>::mul_rn(a, st.A[j]);
+      e = Num<T>::fma_ru(a, st.e, g);
+      const T rnd = Num<T>::fma_ru(Num<T>::RHO, Num<T>::add_ru(fabs(nb), Num<T>::mul_ru(a, rA)), Num<T>::TINY);
+      e = Num<T>::add_ru(e, rnd);
+      rA2 = sum_abs_A(st);
+    }
+  }
+  st.base = nb;
+  st.e = e;
+  constexpr int OFF = pv_off(MODE);
+  out[OFF] = nb;
+#pragma unroll
+  for (int j = 0; j < S; ++j) out[OFF + 1 + j] = st.A[j];
+  out[C - 1] = gamma_base >= T(0)
+                   ? Num<T>::fma_ru(gamma_next, Num<T>::add_ru(rA2, e), Num<T>::fma_ru(gamma_base, fabs(nb), e))
+                   : Num<T>::fma_ru(gamma_next, Num<T>::add_ru(Num<T>::add_ru(fabs(nb), rA2), e), e);
+  return !off;
 }
 
 // Final bound of a width-1 output: lo/hi rounded outward.
@@ -687,7 +754,17 @@ SPK_DEV f32x2 f2_pack(float lo, float hi) {
 // pairs, an optional odd RN column, and the round-up error column (scalar
 // FFMA.RP with the |W| operand modifier).  Point evaluation (C == 1) pairs
 // adjacent boxes instead.  Same blocked-summation budget as the scalar loop.
-template <int C, int MMAX, int BIAS2 = -1, bool TEAMS = false, int SM = 0>
+// RE (running error): on the layers the host flags (LayerDev::runerr) the
+// base column (low lane of pair 0) also accumulates Wilkinson's a-posteriori
+// bound sum_k |s_k| of its partial and flushed sums (one FFMA.RP per step),
+// and the loop charges u/(1-u) * that sum to the error column -- instead of
+// the a-priori gamma_n * sum |W| |base| that pack_next would otherwise put on
+// v (~6x tighter per layer).  The extra op sits on the saturated FP32 pipe
+// (+24% when every layer does it), so only the leading wide layers, whose
+// budgets dominate the FP32 excess of deep affine-fixed nets through the
+// non-cancelling error channel (x10 per layer, tools/excess_attrib.py), take
+// this form of the loop.
+template <int C, int MMAX, int BIAS2 = -1, bool TEAMS = false, int SM = 0, bool RE = false>
 SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__ X, WRing<float, C, MMAX, SM>& ring,
                              int tid, float (&acc)[Cfg<float, C, MMAX, SM>::TI][Cfg<float, C, MMAX, SM>::TB][C],
                              const uint32_t* live = nullptr) {
@@ -700,6 +777,16 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
   constexpr bool ODD = !POINT && (NRN % 2 == 1);
   constexpr int XQ = TB * CP / 2;                  // x fragment as f32x2 words
   static_assert(POINT ? (TB % 2 == 0) : (CP % 2 == 0), "pair alignment");
+  constexpr bool RUN = RE && !POINT && NP >= 1 && BIAS2 < 0;
+  static_assert(RE == RUN, "running error bound: affine columns (base in pair 0) only");
+  // runtime per layer (LayerDev::runerr, set by the host for the leading wide
+  // layers whose budgets dominate): the K loop below exists in both forms
+  const bool re_layer = RUN && L.runerr;
+  float erun[RUN ? TI : 1][RUN ? TB : 1];
+#pragma unroll
+  for (int ti = 0; ti < (RUN ? TI : 1); ++ti)
+#pragma unroll
+    for (int tb = 0; tb < (RUN ? TB : 1); ++tb) erun[ti][tb] = 0.f;
   const int ng = tid % CF::NG, bg = tid / CF::NG;
 
   constexpr int NPA = NP > 0 ? NP : 1;
@@ -736,13 +823,20 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
   constexpr bool ALWAYS_FRESH = (KT % CF::SUB) == 0;
   int since = 0;
   // partial sums -> running sums (a fresh block re-initialises the partials)
-  auto flush = [&]() {
+  auto flush = [&](auto rec) {
+    constexpr bool REC = decltype(rec)::value && RUN;
 #pragma unroll
     for (int ti = 0; ti < TI; ++ti) {
 #pragma unroll
-      for (int g = 0; g < NBOX; ++g)
+      for (int g = 0; g < NBOX; ++g) {
 #pragma unroll
         for (int p = 0; p < NP; ++p) accp[ti][g][p] = f2_add(accp[ti][g][p], partp[ti][g][p]);
+        if (REC) {  // the flush's own rounding: u |acc_new|
+          float b_, a_;
+          f2_split(accp[ti][g][0], b_, a_);
+          erun[ti][g] = __fadd_ru(erun[ti][g], fabsf(b_));
+        }
+      }
       if (ODD) {
 #pragma unroll
         for (int tb = 0; tb < TB; ++tb) acco[ti][tb] += parto[ti][tb];
@@ -776,8 +870,9 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
   };
   // one k-step; FIRST: the first step of a fresh block writes the partials
   // (RN(w*x) == RN(w*x + 0): the same sums as zero-initialised partials)
-  auto fma_step = [&](const float* w, const f32x2* xq, auto first) {
+  auto fma_step = [&](const float* w, const f32x2* xq, auto first, auto rec) {
     constexpr bool FIRST = decltype(first)::value;
+    constexpr bool REC = decltype(rec)::value && RUN;
 #pragma unroll
     for (int ti = 0; ti < TI; ++ti) {
 #pragma unroll
@@ -786,6 +881,17 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
         for (int p = 0; p < NP; ++p) {
           const f32x2 xv = xq[POINT ? p : (g * CP) / 2 + p];
           partp[ti][g][p] = FIRST ? f2_mul(w[ti], xv) : f2_fma(w[ti], xv, partp[ti][g][p]);
+          if (REC && p == 0) {
+            // Wilkinson's running bound sum_k |s_k|.  Only steps whose base
+            // input is nonzero can round (an exact-zero x leaves s_k ==
+            // s_(k-1)): gating on it keeps the bound independent of which
+            // all-zero rows the live-row masks skip -- results stay identical
+            // for any batch composition
+            float b_, a_, x0_, x1_;
+            f2_split(partp[ti][g][0], b_, a_);
+            f2_split(xv, x0_, x1_);
+            erun[ti][g] = __fmaf_ru(fabsf(b_), x0_ != 0.f ? 1.f : 0.f, erun[ti][g]);
+          }
         }
       if (!POINT) {
 #pragma unroll
@@ -811,7 +917,7 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
   using F1 = std::integral_constant<bool, true>;
   // a full SUBIN chunk, fully unrolled: constant shared-memory offsets, no
   // loop control, fragments double-buffered one step ahead
-  auto full_chunk = [&](const float* __restrict__ Ws, const float* __restrict__ Xt, int k0, auto fresh) {
+  auto full_chunk = [&](const float* __restrict__ Ws, const float* __restrict__ Xt, int k0, auto fresh, auto rec) {
     float wf[2][TI];
     f32x2 xf[2][XQ];
     load_frag(Ws, Xt, k0, wf[0], xf[0]);
@@ -819,13 +925,14 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
     for (int j = 0; j < SUBIN; ++j) {
       if (j + 1 < SUBIN) load_frag(Ws, Xt, k0 + j + 1, wf[(j + 1) & 1], xf[(j + 1) & 1]);
       if (j == 0 && decltype(fresh)::value) {
-        fma_step(wf[0], xf[0], F1{});
+        fma_step(wf[0], xf[0], F1{}, rec);
       } else {
-        fma_step(wf[j & 1], xf[j & 1], F0{});
+        fma_step(wf[j & 1], xf[j & 1], F0{}, rec);
       }
     }
   };
 
+  auto tiles = [&](auto rec) {
   for (int t = 0; t < L.ntiles; ++t) {
     const float* __restrict__ Ws = ring.acquire();
     const float* __restrict__ Xt = X + (size_t)(t * KT) * CF::RS + bg * TB * CP;
@@ -860,15 +967,15 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
         for (int p = 0; p < cnt; p += 2) {
           load_frag(Ws, Xt, kk.y, w1, x1);
           const int2 nx = *reinterpret_cast<const int2*>(lst + p + 2);
-          fma_step(w0, x0, F0{});
+          fma_step(w0, x0, F0{}, rec);
           load_frag(Ws, Xt, nx.x, w0, x0);
-          fma_step(w1, x1, F0{});
+          fma_step(w1, x1, F0{}, rec);
           kk = nx;
         }
       }
       since += KT;
       if (since >= CF::SUB) {
-        flush();
+        flush(rec);
         since = 0;
       }
       ring.release(tid);
@@ -880,9 +987,9 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
       // (interval, C == 2: the rolled loop measured 2% faster)
       if (SPK_UNROLL_BLOCK && C != 2 && k1 - k0 == SUBIN) {
         if (ALWAYS_FRESH || since == 0) {
-          full_chunk(Ws, Xt, k0, F1{});
+          full_chunk(Ws, Xt, k0, F1{}, rec);
         } else {
-          full_chunk(Ws, Xt, k0, F0{});
+          full_chunk(Ws, Xt, k0, F0{}, rec);
         }
       } else {
         if (since == 0) zero_parts();
@@ -892,20 +999,26 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
 #pragma unroll 1
         for (int kk = k0; kk < k1; kk += 2) {
           load_frag(Ws, Xt, kk + 1, w1, x1);
-          fma_step(w0, x0, F0{});
+          fma_step(w0, x0, F0{}, rec);
           if (SPK_SPEC_PREFETCH || kk + 2 < k1) load_frag(Ws, Xt, kk + 2, w0, x0);  // row k1 <= KT: in bounds
-          fma_step(w1, x1, F0{});
+          fma_step(w1, x1, F0{}, rec);
         }
       }
       since += SUBIN;
       if (since >= CF::SUB) {
-        flush();
+        flush(rec);
         since = 0;
       }
     }
     ring.release(tid);
   }
-  if (since > 0) flush();
+  if (since > 0) flush(rec);
+  };
+  if (RUN && re_layer) {
+    tiles(std::integral_constant<bool, RUN>{});
+  } else {
+    tiles(F0{});
+  }
   if (TEAMS) {
     team_sync<CF::TEAM>(tid);
   } else {
@@ -930,6 +1043,8 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
         } else {
           acc[ti][tb][C - 1] = acce[ti][tb];
         }
+        // base column rounding <= u/(1-u) sum |s| with u/(1-u) <= 0x1.000002p-24
+        if (RUN && re_layer) acc[ti][tb][C - 1] = __fmaf_ru(erun[ti][tb], 0x1.000002p-24f, acc[ti][tb][C - 1]);
       }
     }
   }
@@ -937,11 +1052,11 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
 
 // BIAS2 >= 0: a second column that also starts from the bias (march modes:
 // the point value in column 0 and the bound's base in column 1)
-template <typename T, int C, int MMAX, int BIAS2 = -1, bool TEAMS = false, int SM = 0>
+template <typename T, int C, int MMAX, int BIAS2 = -1, bool TEAMS = false, int SM = 0, bool RE = false>
 SPK_DEV void dense_kloop(const LayerDev<T>& L, const T* __restrict__ X, WRing<T, C, MMAX, SM>& ring, int tid,
                          T (&acc)[Cfg<T, C, MMAX, SM>::TI][Cfg<T, C, MMAX, SM>::TB][C], const uint32_t* live = nullptr) {
   if constexpr (sizeof(T) == 4 && SPK_PACKED_F32) {
-    dense_kloop_f32<C, MMAX, BIAS2, TEAMS, SM>(L, X, ring, tid, acc, live);
+    dense_kloop_f32<C, MMAX, BIAS2, TEAMS, SM, RE>(L, X, ring, tid, acc, live);
   } else {
     dense_kloop_scalar<T, C, MMAX, BIAS2, TEAMS, SM>(L, X, ring, tid, acc);
   }
@@ -990,7 +1105,17 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
     be_r[ti] = (MODE != MODE_POINT && i < L.m_out) ? L.berr[i] : T(0);
   }
   T acc[TI][TB][C];
-  dense_kloop<T, C, MMAX, (MODE >= MODE_MI ? 1 : -1), CF::TEAMSYNC, SM>(L, X, ring, tid, acc, m_cur);
+  // running-error K loop (affine-fixed, FP32): this layer bounds its base
+  // column's rounding itself, so the packs feeding a generic layer of this
+  // instantiation charge only the weight rounding on |base| (gamma_base_next)
+  // (wide-net tiles only: on the 2-CTA/SM tiles of narrow nets -- 128-register
+  // cap -- the second form of the loop cost 15-25%, for little: their excess
+  // is already small; consistency is per instantiation, so a tile without RE
+  // packs with the full budget and ignores the runerr flags)
+  constexpr bool RE = SPK_RUNERR && SPK_PACKED_F32 && sizeof(T) == 4 && MODE == MODE_AFFINE && C >= 3 &&
+                      CF::MINB == 1 && SM == 0;
+  const T gamma_base = RE ? L.gamma_base_next : T(-1);
+  dense_kloop<T, C, MMAX, (MODE >= MODE_MI ? 1 : -1), CF::TEAMSYNC, SM, RE>(L, X, ring, tid, acc, m_cur);
 
   // epilogue: activation rules, write next X in place (one contiguous
   // TB*CP vector per neuron: the thread's boxes are adjacent in the row)
@@ -1043,16 +1168,23 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
     T out[TB * CP];
 #pragma unroll
     for (int c = 0; c < TB * CP; ++c) out[c] = T(0);
+    // fused ReLU epilogue (affine-fixed): live bit from the rule itself
+    constexpr bool FUSED_RELU = SPK_FUSED_RELU && MODE == MODE_AFFINE;
+    bool nz_rule = false;
 #pragma unroll
     for (int tb = 0; tb < TB; ++tb) {
       if (valid) {
         State<T, C, MODE> st = state_from<T, C, MODE>(acc[ti][tb], be);
+        if (FUSED_RELU && relu_only) {
+          nz_rule |= relu_affine_pack<T, C, MODE>(st, gamma_next, out + tb * CP, gamma_base);
+          continue;
+        }
         if (relu_only) {
           apply_act<T, C, MODE>(st, ACT_RELU);
         } else {
           for (int a = 0; a < nact; ++a) apply_act<T, C, MODE>(st, L.act[a]);
         }
-        pack_next<T, C, MODE>(st, gamma_next, out + tb * CP);
+        pack_next<T, C, MODE>(st, gamma_next, out + tb * CP, gamma_base);
       }
     }
     float4* dst = reinterpret_cast<float4*>(X + (size_t)i * CF::RS + bg * TB * CP);
@@ -1061,8 +1193,12 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
     for (int q = 0; q < (int)(TB * CP * sizeof(T) / 16); ++q) dst[q] = srcv[q];
     if (LV) {
       bool nz = false;
+      if (FUSED_RELU && relu_only) {
+        nz = nz_rule;
+      } else {
 #pragma unroll
-      for (int c = 0; c < TB * CP; ++c) nz |= out[c] != T(0);
+        for (int c = 0; c < TB * CP; ++c) nz |= out[c] != T(0);
+      }
       nz = nz && !ring.group_empty;
       live_bits |= (nz ? 1u : 0u) << (ti % CF::G);
       if (ti % CF::G == CF::G - 1) {  // a group of G consecutive neurons: one word, one atomic

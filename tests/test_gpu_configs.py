@@ -173,8 +173,10 @@ def test_c4_mesh_fp32_identical_on_sign_agreeing_cells(gold):
 
 # ---------------------------------------------------------------- C5
 # FP32 band vs the reference, in units of S + w (S = max(1, |lo|, |hi|),
-# w = hi - lo of the reference): measured maxima in DESIGN.md §2.
-C5_BAND = {"affine-fixed": 0.12, "interval": 1e-4}
+# w = hi - lo of the reference): measured maxima 4.2e-2 (C5_512) / 8.4e-4
+# (C5_64) affine-fixed, 9.2e-5 interval (tests/test_gpu_fullsize.py
+# explains the deep-net amplification of the FP32 rounding budget).
+C5_BAND = {"affine-fixed": 0.06, "interval": 2e-4}
 
 
 def _c5_axes(n):
