@@ -212,6 +212,10 @@ int spk_march(const spk_net* net, int policy, int n_keep, int precision, int64_t
               int64_t origin_stride, const double* dirs, const double* t_init, const double* sigma_init,
               const double* params6, uint8_t* hit, double* t_out, double* steps, int64_t* stats,
               void* stream);
+/* Per-round record of the calling thread's last spk_march (lock-step rounds):
+ * active rays and host wall time (ms, kernels + the count read-back) of every
+ * round; writes min(rounds, cap) entries, returns the round count. */
+int spk_march_round_log(int64_t* active, double* ms, int cap);
 /* Camera.pixel_dirs (camera.py:82-92) on the device, bit-exact: frame9 =
  * forward, right, true_up (host), dirs (device) = height x width x 3. */
 int spk_camera_dirs(const double* frame9, double half_w, double half_h, int width, int height,

@@ -67,6 +67,7 @@ SIGNATURES = {
     "spk_tree_stats": ([vp, vp, vp], i32),
     "spk_tree_level_copy": ([vp, i32, vp, vp, vp, vp, vp, vp, vp], i32),
     "spk_march": ([vp, i32, i32, i32, i64, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp], i32),
+    "spk_march_round_log": ([vp, vp, i32], i32),
     "spk_camera_dirs": ([vp, f64, f64, i32, i32, vp, vp], i32),
     "spk_affine_rule": ([i32, i32, i64, vp, vp, vp, vp, vp], i32),
     "spk_render_shade": ([vp, i32, i64, vp, i64, vp, vp, vp, f64, i32, vp, vp, vp, vp, vp], i32),

@@ -21,6 +21,7 @@
 // device with round-to-nearest FP64 ops in numpy's evaluation order, so they
 // match the reference bit for bit.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <vector>
 
@@ -171,6 +172,12 @@ __global__ void march_update_kernel(long long na, const int* __restrict__ idx, c
   if (known) atomicAdd(certified, 1ull);
 }
 
+// the calling thread's record of its last spk_march: (active rays, ms) per round
+static std::vector<std::pair<long long, double>>& round_log() {
+  thread_local std::vector<std::pair<long long, double>> log;
+  return log;
+}
+
 }  // namespace spk
 
 using namespace spk;
@@ -186,6 +193,16 @@ int spk_camera_dirs(const double* frame9, double half_w, double half_h, int widt
       frame9[8], half_w, half_h, dirs);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SPK_OK : cuda_fail(e, "camera dirs");
+}
+
+int spk_march_round_log(int64_t* active, double* ms, int cap) {
+  const auto& log = round_log();
+  const int n = (int)log.size();
+  for (int i = 0; i < n && i < cap; ++i) {
+    if (active) active[i] = log[i].first;
+    if (ms) ms[i] = log[i].second;
+  }
+  return n;
 }
 
 int spk_march(const spk_net* net, int policy, int n_keep, int precision, int64_t n, const double* origins,
@@ -219,6 +236,10 @@ int spk_march(const spk_net* net, int policy, int n_keep, int precision, int64_t
   int rc = SPK_OK;
   std::vector<int> hcnt(nblk);
   long long rounds = 0, evals = 0;
+  // per-round record of this call (spk_march_round_log): active rays and the
+  // host wall time of the round (kernel + count + the one synchronisation)
+  round_log().clear();
+  auto t_round = std::chrono::steady_clock::now();
   if (e != cudaSuccess) {
     rc = cuda_fail(e, "march alloc");
   } else {
@@ -275,6 +296,11 @@ int spk_march(const spk_net* net, int policy, int n_keep, int precision, int64_t
     if (e != cudaSuccess) { rc = cuda_fail(e, "march round"); break; }
     long long nn = 0;
     for (int b = 0; b < ab; ++b) nn += hcnt[b];
+    {
+      const auto now = std::chrono::steady_clock::now();
+      round_log().push_back({na, std::chrono::duration<double, std::milli>(now - t_round).count()});
+      t_round = now;
+    }
     if (nn > 0) compact_kernel<<<ab, MT, 0, st>>>(na, live, cur, bcnt, nxt);
     std::swap(cur, nxt);
     na = nn;

@@ -1112,8 +1112,10 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
   // cap -- the second form of the loop cost 15-25%, for little: their excess
   // is already small; consistency is per instantiation, so a tile without RE
   // packs with the full budget and ignores the runerr flags)
+  // (the small tile, SM = 1, runs the same bound as the big tiles of its
+  // width, so every processing order of a batch stays bit-identical)
   constexpr bool RE = SPK_RUNERR && SPK_PACKED_F32 && sizeof(T) == 4 && MODE == MODE_AFFINE && C >= 3 &&
-                      CF::MINB == 1 && SM == 0;
+                      (CF::MINB == 1 || SM == 1);
   const T gamma_base = RE ? L.gamma_base_next : T(-1);
   dense_kloop<T, C, MMAX, (MODE >= MODE_MI ? 1 : -1), CF::TEAMSYNC, SM, RE>(L, X, ring, tid, acc, m_cur);
 

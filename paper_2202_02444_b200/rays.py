@@ -133,6 +133,19 @@ def march_arrays(net, origins, dirs, params: RayCastParams = RayCastParams(), po
     return hit.bool(), t, steps, st
 
 
+def last_march_rounds():
+    """(active rays, host ms) per lock-step round of this thread's last march
+    (spk_march_round_log): the record behind the K6 tail analysis."""
+    import ctypes as C
+
+    lib = _lib.load()
+    n = lib.spk_march_round_log(None, None, 0)
+    active = np.zeros(n, np.int64)
+    ms = np.zeros(n, np.float64)
+    lib.spk_march_round_log(active.ctypes.data_as(C.c_void_p), ms.ctypes.data_as(C.c_void_p), n)
+    return active, ms
+
+
 def cast_rays(net, rays, params: RayCastParams = RayCastParams(), policy=None, threads: int = 1,
               precision: str = "fp64") -> list:
     """Cast many rays; elementwise identical to cast_ray on each (rays.py:151-184).
