@@ -379,6 +379,9 @@ def run_ours(args, rank, world, local_rank):
         del tree
         sharded["C5_8x256_16M_per_rank"] = bench_c5_sharded(torch, sp, synth, 16 << 20, rank, world, coll_dev,
                                                              barrier, flush)
+        if not args.no_mesh:
+            sharded["C4_elu8x512_mesh_256cubed"] = bench_c4_sharded(torch, sp, synth, 8, rank, world, coll_dev,
+                                                                    barrier)
         if not args.no_rays:
             sharded["C3_siren_rays_interval_256sq_fp64"] = bench_c3_sharded(torch, sp, synth, 256, rank, world,
                                                                             coll_dev, barrier)
@@ -612,6 +615,33 @@ def bench_c5_sharded(torch, sp, synth, n_per_rank, rank, world, coll_dev, barrie
     dt, n = reduce_time_units(float(np.median(ts)), float(n_per_rank), device=coll_dev)
     return {"boxes": int(n), "boxes_per_s": n / dt, "ms": dt * 1e3, "scaling": "weak",
             "parallelism": f"contiguous first_index ranges x{world}"}
+
+
+def bench_c4_sharded(torch, sp, synth, m, rank, world, coll_dev, barrier):
+    """C4 sharded: every rank prunes redundantly and extracts its contiguous
+    slice of the surviving blocks (spk_mesh_extract_shard), no collective
+    inside; then the one gather (edge-key triangles + vertex rows, global
+    sort-unique dedup on the device).  Wall time, max over ranks."""
+    from paper_2202_02444_b200 import meshing
+    from paper_2202_02444_b200.shard import reduce_time_units
+    from paper_2202_02444_b200.spatial import AABB
+
+    net = synth.config_net("C4")
+    bounds = AABB(-np.ones(3), np.ones(3))
+    meshing.extract_mesh_sharded(net, bounds, 5, rank, world, 3, sp.AFFINE_FIXED, precision="fp32")  # warm
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    part = meshing.extract_mesh_sharded(net, bounds, m, rank, world, 3, sp.AFFINE_FIXED, precision="fp32")
+    torch.cuda.synchronize()
+    dt, evals = reduce_time_units(time.perf_counter() - t0, float(part.point_evals), device=coll_dev)
+    barrier()
+    g0 = time.perf_counter()
+    mesh = meshing.gather_mesh(part, device=coll_dev)
+    barrier()
+    return {"m": m, "seconds": dt, "point_evals": int(evals), "point_evals_per_s": evals / dt,
+            "gather_ms": 1e3 * (time.perf_counter() - g0), "triangles": int(len(mesh.triangles)),
+            "parallelism": f"surviving-block slices x{world}"}
 
 
 def bench_frustum(torch, sp, res):

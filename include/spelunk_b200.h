@@ -307,8 +307,20 @@ int spk_bisect(const spk_net* net, int precision, int64_t n, double* a, double* 
 int spk_mesh_extract(const spk_net* net, int policy, int n_keep, int precision, const double* lo3,
                      const double* hi3, int m, int dense_levels, int prune, const int8_t* tri_table,
                      const uint8_t* tri_count, void* stream, spk_mesh** out);
+/* The same for shard `shard` of n_shards (one per GPU): the
+ * prune runs in full on every shard, then only the shard's contiguous slice
+ * of the surviving blocks (visiting order; even split) is extracted, with
+ * vertices deduplicated within the shard.  The shards' triangles as edge-key
+ * triples, concatenated in shard order, are the unsharded triangle stream;
+ * a global dedup by edge key (first occurrence) gives extract_mesh's arrays
+ * (paper_2202_02444_b200.meshing.gather_mesh).  Shard 0 of 1 = spk_mesh_extract. */
+int spk_mesh_extract_shard(const spk_net* net, int policy, int n_keep, int precision, const double* lo3,
+                           const double* hi3, int m, int dense_levels, int prune, const int8_t* tri_table,
+                           const uint8_t* tri_count, int shard, int n_shards, void* stream, spk_mesh** out);
 int spk_mesh_info(const spk_mesh* mesh, int64_t* n_vertices, int64_t* n_triangles, int64_t* n_blocks,
                   int64_t* point_evals, int64_t* bound_evals);
+/* the shard's first surviving block (visiting order) and the surviving total */
+int spk_mesh_shard_info(const spk_mesh* mesh, int64_t* block_first, int64_t* blocks_total);
 /* copy out (host or device pointers, any may be NULL): vertices n_v x 3,
  * triangles n_t x 3 (vertex ids), vertex edge keys n_v
  * ((i*(2^m+1) + j)*(2^m+1) + k) * 3 + axis of the edge's lower corner */

@@ -76,7 +76,8 @@ from .spatial import (
     iter_leaves,
 )
 
-from .meshing import extract_mesh, extract_mesh_arrays, extract_mesh_dense
+from .meshing import (extract_mesh, extract_mesh_arrays, extract_mesh_dense, extract_mesh_sharded, gather_mesh,
+                      merge_sharded_meshes)
 from .render import Image, read_ppm, render_image, write_image
 from .bench import BenchRow, FuzzReport, FuzzViolation, bench_variants, fuzz_soundness
 from .queries import (

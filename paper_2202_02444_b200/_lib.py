@@ -77,7 +77,9 @@ SIGNATURES = {
     "spk_bisect": ([vp, i32, i64, vp, vp, i32, vp, vp], i32),
     "spk_frustum_cast": ([vp, i32, i32, i32, vp, vp, f64, f64, i32, i32, i32, vp, vp, vp, vp, vp, vp], i32),
     "spk_mesh_extract": ([vp, i32, i32, i32, vp, vp, i32, i32, i32, vp, vp, vp, vp], i32),
+    "spk_mesh_extract_shard": ([vp, i32, i32, i32, vp, vp, i32, i32, i32, vp, vp, i32, i32, vp, vp], i32),
     "spk_mesh_info": ([vp, vp, vp, vp, vp, vp], i32),
+    "spk_mesh_shard_info": ([vp, vp, vp], i32),
     "spk_mesh_copy": ([vp, vp, vp, vp], i32),
     "spk_mesh_destroy": ([vp], i32),
     "spk_tree_destroy": ([vp], i32),

@@ -240,6 +240,7 @@ struct spk_mesh {
   int device = 0;
   cudaStream_t stream = nullptr;
   long long n_vertices = 0, n_triangles = 0, n_blocks = 0, evals = 0, bound_evals = 0;
+  long long block_first = 0, blocks_total = 0;  // this shard's slice of the surviving blocks
   double* verts = nullptr;                // n_vertices x 3
   unsigned long long* vkeys = nullptr;    // n_vertices (edge keys)
   long long* tris = nullptr;              // n_triangles x 3
@@ -293,7 +294,15 @@ extern "C" {
 int spk_mesh_extract(const spk_net* net, int policy, int n_keep, int precision, const double* lo3, const double* hi3,
                      int m, int dense_levels, int prune, const int8_t* tri_table, const uint8_t* tri_count,
                      void* stream, spk_mesh** out) {
+  return spk_mesh_extract_shard(net, policy, n_keep, precision, lo3, hi3, m, dense_levels, prune, tri_table,
+                                tri_count, 0, 1, stream, out);
+}
+
+int spk_mesh_extract_shard(const spk_net* net, int policy, int n_keep, int precision, const double* lo3,
+                           const double* hi3, int m, int dense_levels, int prune, const int8_t* tri_table,
+                           const uint8_t* tri_count, int shard, int n_shards, void* stream, spk_mesh** out) {
   if (!net || !out || !tri_table || !tri_count) return fail(SPK_ERR_INVALID_PARAMETER, "null argument");
+  if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(SPK_ERR_INVALID_PARAMETER, "bad shard index");
   *out = nullptr;
   if (net->input_dim != 3) return fail(SPK_ERR_DIMENSION, "meshing needs a 3-d network");
   if (m <= dense_levels || dense_levels < 0) return fail(SPK_ERR_INVALID_PARAMETER, "ResolutionTooSmall");
@@ -378,6 +387,19 @@ int spk_mesh_extract(const spk_net* net, int policy, int n_keep, int precision, 
     org = nxt;
     nb = nn;
     if (!last) sz[ax] = half;  // blocks at a level share their sizes
+  }
+  // sharding (C4 across GPUs): every shard runs the (cheap)
+  // prune redundantly and extracts a contiguous slice of the surviving blocks
+  // in visiting order; the slices' triangles, concatenated in shard order, are
+  // the unsharded visiting order (meshing.gather_mesh dedups the vertices)
+  {
+    const long long base = nb / n_shards, extra = nb % n_shards;
+    const long long first = shard * base + std::min<long long>(shard, extra);
+    const long long count = base + (shard < extra ? 1 : 0);
+    mesh->blocks_total = nb;
+    mesh->block_first = first;
+    org = org + first * 3;
+    nb = count;
   }
   mesh->n_blocks = nb;
 
@@ -524,6 +546,13 @@ int spk_mesh_info(const spk_mesh* mesh, int64_t* n_vertices, int64_t* n_triangle
   if (n_blocks) *n_blocks = mesh->n_blocks;
   if (point_evals) *point_evals = mesh->evals;
   if (bound_evals) *bound_evals = mesh->bound_evals;
+  return SPK_OK;
+}
+
+int spk_mesh_shard_info(const spk_mesh* mesh, int64_t* block_first, int64_t* blocks_total) {
+  if (!mesh) return fail(SPK_ERR_INVALID_PARAMETER, "null mesh");
+  if (block_first) *block_first = mesh->block_first;
+  if (blocks_total) *blocks_total = mesh->blocks_total;
   return SPK_OK;
 }
 

@@ -76,6 +76,83 @@ def extract_mesh_arrays(net, bounds: AABB, m: int, dense_levels: int = 3, policy
     return MeshResult(verts, tris, keys.astype(np.int64), nb.value, pe.value, be.value)
 
 
+def extract_mesh_sharded(net, bounds: AABB, m: int, rank: int, world: int, dense_levels: int = 3,
+                         policy=AFFINE_FULL, precision: str = "fp64") -> MeshResult:
+    """This rank's share of a hierarchical extraction (one process per GPU,
+    SURVEY.md §8(e)): the prune runs redundantly, then the rank extracts its
+    contiguous slice of the surviving blocks (visiting order) with no
+    collective.  `gather_mesh` reassembles the reference's arrays."""
+    _check_domain(net, bounds)
+    if m <= dense_levels:
+        raise ResolutionTooSmall(f"resolution exponent {m} must exceed dense_levels {dense_levels}")
+    pcode, n_keep = policy_code(policy)
+    dn = device_net(net)
+    table, count = _tables()
+    lo = np.ascontiguousarray(bounds.lo, dtype=np.float64)
+    hi = np.ascontiguousarray(bounds.hi, dtype=np.float64)
+    h = C.c_void_p()
+    _lib.call("spk_mesh_extract_shard", dn.ptr, pcode, n_keep, _precision_code(precision), lo.ctypes.data,
+              hi.ctypes.data, int(m), int(dense_levels), 1, table.ctypes.data, count.ctypes.data, int(rank),
+              int(world), dv.stream_ptr(dn.device), C.byref(h))
+    lib = _lib.load()
+    try:
+        nv, nt, nb, pe, be, bf, btot = (C.c_int64() for _ in range(7))
+        _lib.check(lib.spk_mesh_info(h, C.byref(nv), C.byref(nt), C.byref(nb), C.byref(pe), C.byref(be)))
+        _lib.check(lib.spk_mesh_shard_info(h, C.byref(bf), C.byref(btot)))
+        verts = np.empty((nv.value, 3))
+        tris = np.empty((nt.value, 3), np.int64)
+        keys = np.empty(nv.value, np.uint64)
+        _lib.call("spk_mesh_copy", h, verts.ctypes.data, tris.ctypes.data, keys.ctypes.data)
+    finally:
+        lib.spk_mesh_destroy(h)
+    return MeshResult(verts, tris, keys.astype(np.int64), nb.value, pe.value, be.value,
+                      meta={"rank": rank, "world": world, "block_first": bf.value, "blocks_total": btot.value})
+
+
+def _mesh_part_t(res: MeshResult, device):
+    torch = dv._torch()
+    keys = torch.from_numpy(np.ascontiguousarray(res.vertex_keys, np.int64)).to(device)
+    tris = torch.from_numpy(np.ascontiguousarray(res.triangles, np.int64)).to(device)
+    verts = torch.from_numpy(np.ascontiguousarray(res.vertices, np.float64)).to(device)
+    return keys[tris] if tris.numel() else tris.reshape(0, 3), keys, verts
+
+
+def _mesh_result(vertices, triangles, vertex_keys, meta) -> MeshResult:
+    return MeshResult(vertices.cpu().numpy(), triangles.cpu().numpy(), vertex_keys.cpu().numpy(), meta=meta)
+
+
+def merge_sharded_meshes(parts) -> MeshResult:
+    """The unsharded mesh from every rank's extract_mesh_sharded result (held
+    in one process, rank order)."""
+    from .shard import merge_mesh_parts_t
+
+    parts = list(parts)
+    v, t, k = merge_mesh_parts_t([_mesh_part_t(p, "cpu") for p in parts])
+    return _mesh_result(v, t, k, {"merged_from": len(parts)})
+
+
+def gather_mesh(res: MeshResult, device=None) -> MeshResult:
+    """Final gather of a sharded extraction -- the one collective step: every
+    rank all_gathers the others' triangles (as edge-key triples) and vertex
+    rows (NCCL over NVLink on GPUs, gloo on CPU), then the global sort-unique
+    dedup on edge keys (first occurrence) runs on `device` and every rank
+    holds extract_mesh's arrays (vertices numbered in first-visit order)."""
+    import torch.distributed as dist
+
+    from .shard import allgather_tensor, merge_mesh_parts_t
+
+    if device is None:
+        torch = dv._torch()
+        device = f"cuda:{torch.cuda.current_device()}" if torch.cuda.is_available() else "cpu"
+    tk, vk, vp = _mesh_part_t(res, device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        parts = list(zip(allgather_tensor(tk, device), allgather_tensor(vk, device), allgather_tensor(vp, device)))
+    else:
+        parts = [(tk, vk, vp)]
+    v, t, k = merge_mesh_parts_t(parts)
+    return _mesh_result(v, t, k, {"gathered_from": len(parts)})
+
+
 def extract_mesh(net, bounds: AABB, m: int, dense_levels: int = 3, policy=AFFINE_FULL,
                  precision: str = "fp64") -> TriangleMesh:
     """Hierarchical extraction at resolution 2**m (meshing.py:111-169)."""

@@ -206,25 +206,31 @@ def gather_camera_image(pix, hit, t, steps, n_pixels: int, device=None):
     at row-major index i, on every rank.  Single process: a scatter."""
     import torch.distributed as dist
 
-    from .shard import allgather_rows
+    torch = dv._torch()
+    from .shard import allgather_tensor
 
-    def host(x):
-        return x.cpu().numpy() if dv.is_tensor(x) else np.asarray(x)
+    if device is None:
+        device = pix.device if dv.is_tensor(pix) else "cpu"
 
-    ints = np.stack([host(pix).astype(np.int64), host(hit).astype(np.int64), host(steps).astype(np.int64)], axis=1)
-    flts = host(t).astype(np.float64).reshape(-1, 1)
+    def t_(x, dtype):
+        x = x if dv.is_tensor(x) else torch.from_numpy(np.ascontiguousarray(x))
+        return x.to(device=device, dtype=dtype).reshape(-1)
+
+    # the image is assembled where the collective runs (the GPU with NCCL)
+    ints = torch.stack([t_(pix, torch.int64), t_(hit, torch.int64), t_(steps, torch.int64)], dim=1)
+    flts = t_(t, torch.float64).reshape(-1, 1)
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
-        ints = np.concatenate(allgather_rows(ints, device), axis=0)
-        flts = np.concatenate(allgather_rows(flts, device), axis=0)
-    out_hit = np.zeros(n_pixels, dtype=bool)
-    out_t = np.full(n_pixels, np.inf)
-    out_steps = np.zeros(n_pixels, dtype=np.int64)
-    if np.unique(ints[:, 0]).size != ints.shape[0]:
+        ints = torch.cat(allgather_tensor(ints, device), dim=0)
+        flts = torch.cat(allgather_tensor(flts, device), dim=0)
+    if torch.unique(ints[:, 0]).numel() != ints.shape[0]:
         raise InvalidParameter("pixel shards overlap")
+    out_hit = torch.zeros(n_pixels, dtype=torch.bool, device=device)
+    out_t = torch.full((n_pixels,), float("inf"), dtype=torch.float64, device=device)
+    out_steps = torch.zeros(n_pixels, dtype=torch.int64, device=device)
     out_hit[ints[:, 0]] = ints[:, 1] != 0
     out_t[ints[:, 0]] = flts[:, 0]
     out_steps[ints[:, 0]] = ints[:, 2]
-    return out_hit, out_t, out_steps
+    return out_hit.cpu().numpy(), out_t.cpu().numpy(), out_steps.cpu().numpy()
 
 
 @dataclass

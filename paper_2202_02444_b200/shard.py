@@ -136,3 +136,113 @@ def allgather_rows(rows: np.ndarray, device=None):
     bufs = [torch.empty_like(t) for _ in range(world)]
     dist.all_gather(bufs, t)
     return [b[:s].cpu().numpy() for b, s in zip(bufs, sizes)]
+
+
+# --------------------------------------------------------------------------
+# Device-resident gathers (torch tensors end to end: NCCL over NVLink on GPUs
+# -- the level arrays never leave HBM -- and the same code on CPU tensors with
+# gloo).  Results equal the NumPy merge above.
+
+def allgather_tensor(t, device=None):
+    """all_gather of a per-rank (n_r, ...) tensor with n_r varying by rank:
+    sizes first, then one padded all_gather on `device` (the collective's
+    device: the rank's GPU for NCCL, "cpu" for gloo).  Returns the list over
+    ranks, on `device`."""
+    import torch
+    import torch.distributed as dist
+
+    dev = torch.device(device) if device is not None else t.device
+    t = t.to(dev)
+    world = dist.get_world_size()
+    n = torch.tensor([t.shape[0]], dtype=torch.int64, device=dev)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n)
+    sizes = [int(s.item()) for s in sizes]
+    cap = max(sizes) if sizes else 0
+    buf = torch.zeros((cap,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
+    if t.shape[0]:
+        buf[: t.shape[0]] = t
+    bufs = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(bufs, buf)
+    return [b[:s] for b, s in zip(bufs, sizes)]
+
+
+def subtree_keys_t(parents, root_ids, n_roots: int):
+    """subtree_keys on torch tensors (int64, on the levels' device)."""
+    import torch
+
+    keys = [root_ids.to(torch.int64)]
+    for j in range(1, len(parents)):
+        par = parents[j].to(torch.int64)
+        k = par.numel() // 2
+        bit = torch.zeros_like(par)
+        bit[k:] = 1
+        keys.append(bit * ((1 << (j - 1)) * int(n_roots)) + keys[j - 1][par])
+    return keys
+
+
+def merge_shard_levels_t(parts, open_idx):
+    """merge_shard_levels on torch tensors: per rank a list over levels j of
+    (f64 rows (n, F), i64 rows (n, 3) = [key, label, face]); open_idx an int64
+    tensor.  Stable key sort and searchsorted on the device."""
+    import torch
+
+    depth = max((len(p) for p in parts), default=0)
+    out = []
+    prev_keys = None
+    n_roots = int(open_idx.numel())
+    for j in range(1, depth + 1):
+        fs = [p[j - 1][0] for p in parts if len(p) >= j]
+        ks = [p[j - 1][1] for p in parts if len(p) >= j]
+        f = torch.cat(fs, dim=0)
+        k = torch.cat(ks, dim=0)
+        order = torch.sort(k[:, 0], stable=True).indices
+        f, k = f[order], k[order]
+        span = (1 << (j - 1)) * n_roots
+        pkey = k[:, 0] % span
+        parent = open_idx[pkey] if j == 1 else torch.searchsorted(prev_keys, pkey)
+        out.append((f, k[:, 1].to(torch.int8), k[:, 2].to(torch.int8), parent.to(torch.int64)))
+        prev_keys = k[:, 0].contiguous()
+    return out
+
+
+# --------------------------------------------------------------------------
+# Mesh shards (C4): contiguous slices of the surviving blocks in visiting
+# order (spk_mesh_extract_shard).  Concatenated in rank order, the shards'
+# triangles -- as edge-key triples -- are the unsharded triangle stream; the
+# reference's _MeshBuilder numbers vertices by first visit and fixes a
+# vertex's position at the first cell that visits its edge, so a global
+# sort-unique on the edge keys with first occurrence (lowest rank, then the
+# shard's own first visit) reproduces extract_mesh's arrays exactly.
+
+def merge_mesh_parts_t(parts):
+    """parts: per rank, in rank order, (tri_keys (T_r, 3) int64, vertex_keys
+    (V_r,) int64, vertices (V_r, 3) f64) torch tensors on one device.
+    Returns (vertices, triangles, vertex_keys) of the unsharded mesh."""
+    import torch
+
+    dev = parts[0][0].device if parts else torch.device("cpu")
+    tk = torch.cat([p[0].reshape(-1, 3) for p in parts], dim=0) if parts else torch.zeros((0, 3), dtype=torch.int64)
+    if tk.numel() == 0:
+        return (torch.zeros((0, 3), dtype=torch.float64, device=dev), torch.zeros((0, 3), dtype=torch.int64, device=dev),
+                torch.zeros(0, dtype=torch.int64, device=dev))
+
+    def first_occurrence(x):
+        uk, inv = torch.unique(x, return_inverse=True)
+        pos = torch.arange(x.numel(), device=x.device)
+        first = torch.full((uk.numel(),), x.numel(), dtype=torch.int64, device=x.device)
+        first.scatter_reduce_(0, inv, pos, reduce="amin")
+        return uk, inv, first
+
+    flat = tk.reshape(-1)
+    uk, inv, first = first_occurrence(flat)
+    order = torch.argsort(first)                     # unique keys in first-visit order
+    new_id = torch.empty_like(order)
+    new_id[order] = torch.arange(order.numel(), device=dev)
+    triangles = new_id[inv].reshape(-1, 3)
+    vertex_keys = uk[order]
+    vk = torch.cat([p[1].reshape(-1) for p in parts], dim=0)
+    vp = torch.cat([p[2].reshape(-1, 3) for p in parts], dim=0)
+    uk2, _, first2 = first_occurrence(vk)
+    vertices = vp[first2][torch.searchsorted(uk2, vertex_keys)]
+    return vertices, triangles, vertex_keys

@@ -441,22 +441,87 @@ def merge_sharded_trees(parts) -> TreeArrays:
     return _assemble(parts[0].meta, [_pack_subtree(p) for p in parts])
 
 
-def gather_spatial_tree(arr: TreeArrays, device=None) -> TreeArrays:
+def _pack_subtree_t(arr: TreeArrays, device):
+    """_pack_subtree on torch tensors on `device` (the build's levels stay on
+    the GPU: keys, row packing and the collective never touch the host)."""
+    torch = dv._torch()
+    from .shard import subtree_keys_t
+
+    meta = arr.meta
+    if "open_idx" not in meta:
+        raise InvalidParameter("not a build_spatial_tree_sharded result")
+
+    def t(x, dtype=None):
+        x = x if dv.is_tensor(x) else torch.from_numpy(np.ascontiguousarray(x))
+        return x.to(device=device, dtype=dtype) if dtype is not None else x.to(device)
+
+    d = _np(meta["top"][0].lo).shape[1]
+    f_rows, i_rows, sizes = [], [], []
+    if meta.get("own_sub"):
+        lv = arr.levels
+        keys = subtree_keys_t([t(l.parent, torch.int64) for l in lv],
+                              t(np.asarray(meta["root_ids"], np.int64)), len(meta["open_idx"]))
+        for j in range(1, len(lv)):
+            l = lv[j]
+            f_rows.append(torch.cat([t(l.lo, torch.float64), t(l.hi, torch.float64),
+                                     t(l.bound_lo, torch.float64)[:, None], t(l.bound_hi, torch.float64)[:, None]],
+                                    dim=1))
+            i_rows.append(torch.stack([keys[j], t(l.label, torch.int64), t(l.face, torch.int64)], dim=1))
+            sizes.append(len(l))
+    f_all = torch.cat(f_rows, dim=0) if f_rows else torch.zeros((0, 2 * d + 2), dtype=torch.float64, device=device)
+    i_all = torch.cat(i_rows, dim=0) if i_rows else torch.zeros((0, 3), dtype=torch.int64, device=device)
+    return torch.tensor(sizes, dtype=torch.int64, device=device).reshape(-1, 1), f_all, i_all
+
+
+def gather_spatial_tree(arr: TreeArrays, device=None, to_host: bool = True) -> TreeArrays:
     """Final gather of a frontier-sharded build -- the one collective step,
     after the build (torch.distributed all_gather: NCCL over NVLink on GPUs,
-    gloo on CPU).  Every rank receives the whole tree as host level arrays in
-    the unsharded (reference) order: the redundant top levels, then each
-    deeper level merged by order key (shard.subtree_keys)."""
+    gloo on CPU).  Every rank receives the whole tree in the unsharded
+    (reference) order: the redundant top levels, then each deeper level merged
+    by order key (shard.subtree_keys).  The packing, the all_gather and the
+    key merge (stable sort + searchsorted) run on `device` -- the rank's GPU
+    with NCCL, so the sub-tree levels never leave HBM; "cpu" with gloo.
+    to_host=False keeps the merged levels there as tensors."""
     import torch.distributed as dist
 
-    from .shard import allgather_rows
+    torch = dv._torch()
+    from .shard import allgather_tensor, merge_shard_levels_t
 
-    mine = _pack_subtree(arr)
+    if device is None:
+        lv0 = arr.levels[0].label
+        device = lv0.device if dv.is_tensor(lv0) else "cpu"
+    mine = _pack_subtree_t(arr, device)
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
-        packed = list(zip(*[allgather_rows(x, device) for x in mine]))
+        packed = list(zip(*[allgather_tensor(x, device) for x in mine]))
     else:
         packed = [mine]
-    return _assemble(arr.meta, packed)
+    meta = arr.meta
+    top = meta["top"]
+    d = _np(top[0].lo).shape[1]
+    parts = []
+    for sz, fr, ir in packed:
+        edges = [0]
+        for v in sz[:, 0].tolist():
+            edges.append(edges[-1] + int(v))
+        parts.append([(fr[edges[j]:edges[j + 1]], ir[edges[j]:edges[j + 1]]) for j in range(len(edges) - 1)])
+    open_idx = torch.from_numpy(np.asarray(meta["open_idx"], np.int64)).to(device)
+    merged = merge_shard_levels_t(parts, open_idx)
+
+    def out(x):
+        return x.cpu().numpy() if to_host else x
+
+    def top_field(x):
+        if to_host:
+            return _np(x)
+        return (x if dv.is_tensor(x) else torch.from_numpy(np.ascontiguousarray(x))).to(device)
+
+    levels = [TreeLevel(*[top_field(getattr(l, f)) for f in ("lo", "hi", "bound_lo", "bound_hi", "label", "face",
+                                                              "parent")]) for l in top]
+    for f, lab, face, parent in merged:
+        levels.append(TreeLevel(out(f[:, :d].contiguous()), out(f[:, d:2 * d].contiguous()),
+                                out(f[:, 2 * d].contiguous()), out(f[:, 2 * d + 1].contiguous()), out(lab),
+                                out(face), out(parent)))
+    return TreeArrays(levels, 0, meta={"cut": meta["cut"], "gathered_from": len(packed), "device": str(device)})
 
 
 # The volumetric queries live in queries.py; re-exported here because the

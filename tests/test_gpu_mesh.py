@@ -82,3 +82,22 @@ def test_watertight_and_volume(net_paths):
     assert all(directed[(b, a)] == n for (a, b), n in directed.items())
     v0, v1, v2 = v[t[:, 0]], v[t[:, 1]], v[t[:, 2]]
     assert abs(np.einsum("ij,ij->", v0, np.cross(v1, v2)) / 6.0 - 1.0) <= 0.01
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_mesh_shards_merge_to_unsharded(net_paths, world):
+    """C4 sharding (spk_mesh_extract_shard): block slices per rank, merged by
+    the global edge-key dedup, reproduce the unsharded arrays exactly."""
+    net = sp.load_network(net_paths["relu_sdf"])
+    full = meshing.extract_mesh_arrays(net, BOUNDS, 6, 3, "affine-fixed", precision="fp64")
+    parts = [meshing.extract_mesh_sharded(net, BOUNDS, 6, r, world, 3, "affine-fixed", precision="fp64")
+             for r in range(world)]
+    assert sum(p.n_blocks for p in parts) == full.n_blocks
+    assert [p.meta["block_first"] for p in parts] == sorted(p.meta["block_first"] for p in parts)
+    got = meshing.merge_sharded_meshes(parts)
+    np.testing.assert_array_equal(got.triangles, full.triangles)
+    np.testing.assert_array_equal(got.vertex_keys, full.vertex_keys)
+    np.testing.assert_array_equal(got.vertices, full.vertices)
+    # single process: gather_mesh of the whole mesh is the identity
+    one = meshing.gather_mesh(meshing.extract_mesh_sharded(net, BOUNDS, 6, 0, 1, 3, "affine-fixed"))
+    np.testing.assert_array_equal(one.triangles, full.triangles)

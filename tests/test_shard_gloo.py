@@ -177,3 +177,70 @@ def test_subtree_keys_order():
     assert list(k[1]) == [1, 3]
     k0 = shard.subtree_keys([None, par1], [0], 2)
     assert sorted(list(k0[1]) + list(k[1])) == [0, 1, 2, 3]
+
+
+# ---------------------------------------------------------------- C4 meshes
+MESH_NET = os.path.join(os.path.dirname(__file__), "golden", "nets", "relu_sdf.json")
+
+
+def _oracle_mesh_shard(net, m, rank, world):
+    """A rank's extract_mesh_sharded result with the oracle standing in for
+    the device kernels: its contiguous slice of the surviving blocks."""
+    from paper_2202_02444_b200.meshing import MeshResult
+
+    blocks, coords = orc.mesh_blocks(net, -np.ones(3), np.ones(3), m, 3, "affine-fixed")
+    first, count = shard.shard_range(len(blocks), rank, world)
+    builder = orc._Builder(coords)
+    for blk in blocks[first:first + count]:
+        orc._polygonize(builder, orc._grid_values(net, coords, blk), (blk[0][0], blk[1][0], blk[2][0]))
+    v, t, k = builder.result()
+    return MeshResult(v, t, k, count, meta={"block_first": first, "blocks_total": len(blocks)})
+
+
+def test_merge_mesh_shards_single_process():
+    """Shards merged in one process equal the unsharded extraction (arrays,
+    first-visit vertex numbering)."""
+    from paper_2202_02444_b200.meshing import merge_sharded_meshes
+
+    net = orc.load_net(MESH_NET)
+    want_v, want_t, want_k = orc.mesh_extract(net, -np.ones(3), np.ones(3), 5, 3, "affine-fixed")
+    for world in (1, 3):
+        got = merge_sharded_meshes([_oracle_mesh_shard(net, 5, r, world) for r in range(world)])
+        np.testing.assert_array_equal(got.triangles, want_t)
+        np.testing.assert_array_equal(got.vertex_keys, want_k)
+        np.testing.assert_array_equal(got.vertices, want_v)
+
+
+def _mesh_worker(rank, world, port, m, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2202_02444_b200.meshing import gather_mesh
+
+        net = orc.load_net(MESH_NET)
+        res = gather_mesh(_oracle_mesh_shard(net, m, rank, world), device="cpu")
+        if rank == 0:
+            out_q.put((res.vertices, res.triangles, res.vertex_keys))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gather_mesh_gloo():
+    """C4 mesh sharding: block slices per rank, one all_gather of edge-key
+    triangles and vertex rows, global sort-unique dedup -> extract_mesh's arrays."""
+    m, world = 5, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mesh_worker, args=(r, world, port, m, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    v, t, k = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want_v, want_t, want_k = orc.mesh_extract(orc.load_net(MESH_NET), -np.ones(3), np.ones(3), m, 3, "affine-fixed")
+    np.testing.assert_array_equal(t, want_t)
+    np.testing.assert_array_equal(k, want_k)
+    np.testing.assert_array_equal(v, want_v)
