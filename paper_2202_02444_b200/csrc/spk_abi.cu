@@ -98,9 +98,21 @@ static int act_code(const spk_net* net, int act) {
   return (net->corrupt_relu && act == ACT_RELU) ? (int)ACT_RELU_BROKEN : act;
 }
 
+// ReLU-specialised kernels apply (every dense layer's activations are exactly
+// [] or [ReLU], none before the first layer, the test hook off)
+static int relu_net_of(const spk_net* net) {
+  if (net->corrupt_relu || !net->pre_acts.empty()) return 0;
+  for (const auto& L : net->layers) {
+    if (L.acts.size() > 1) return 0;
+    if (L.acts.size() == 1 && L.acts[0] != SPK_OP_RELU) return 0;
+  }
+  return 1;
+}
+
 template <typename T>
 static void recode_acts(spk_net* net, DevNet<T>& dn) {
   if (!dn.ready) return;
+  dn.nd.relu_net = relu_net_of(net);
   for (int i = 0; i < dn.nd.n_pre; ++i) dn.nd.pre_act[i] = act_code(net, net->pre_acts[i]);
   for (size_t l = 0; l < net->layers.size(); ++l)
     for (int a = 0; a < dn.nd.L[l].n_act; ++a) dn.nd.L[l].act[a] = act_code(net, net->layers[l].acts[a]);
@@ -169,8 +181,13 @@ int build_device_net(spk_net* net, DevNet<T>& dn) {
       offs[l].w = small.size();
       for (size_t q = 0; q < L.W.size(); ++q) small.push_back((T)L.W[q]);
     }
+    // bias and bias-budget arrays start 16-byte aligned and are zero-padded to
+    // a multiple of 4 entries: the K loops read them as one vector per group
+    // of G consecutive neurons (spk_pass.cuh load_group)
+    while (small.size() % 4) small.push_back(T(0));
     offs[l].b = small.size();
     for (int i = 0; i < L.m_out; ++i) small.push_back((T)L.b[i]);
+    while (small.size() % 4) small.push_back(T(0));
     offs[l].be = small.size();
     for (int i = 0; i < L.m_out; ++i) {
       // |b_i| enters the FMA chain exactly once; its share of the rounding
@@ -200,6 +217,7 @@ int build_device_net(spk_net* net, DevNet<T>& dn) {
   nd.wtiles = d_tiles;
   nd.tiles_per_pass = (int)(tiles.size() / (size_t)tile);
   nd.gamma_first = round_up_to<T>(gam.empty() ? 0.0 : gam[0]);
+  nd.relu_net = relu_net_of(net);
   // which generic layers run the running-error K loop (FP32 affine passes)
   std::vector<int> runerr(net->layers.size(), 0);
   for (size_t l = 0, k = 0; l < net->layers.size() && (int)k < SPK_RUNERR_LAYERS; ++l) {

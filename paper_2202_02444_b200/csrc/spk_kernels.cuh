@@ -64,6 +64,13 @@ struct BoundOutput {
   int8_t* cls;  // may be null
 };
 
+#ifndef SPK_RELU_SPECIAL
+#define SPK_RELU_SPECIAL 1  // FP32 affine passes of ReLU-only nets run a ReLU-specialised kernel
+#endif
+#ifndef SPK_PREFETCH_INPUTS
+#define SPK_PREFETCH_INPUTS 0  // L2 prefetch of the next tile's inputs (prefetch_tile; measured: C1 +-0, C2 tree +2% -- off)
+#endif
+
 // splitmix64 finaliser; the C5 box stream.
 SPK_DEV unsigned long long mix64(unsigned long long z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -139,6 +146,34 @@ SPK_DEV void prep_inputs(const NetDev<T>& net, const BoxInput& in, long long n, 
   }
 }
 
+// L2 prefetch of a future tile's FP64 inputs (box corners / centres + axes):
+// the first layer of a tile otherwise waits on DRAM latency with every warp
+// idle (C1: ~6% long-scoreboard stalls).  Contiguous slot ranges only (natural
+// order, or the two sibling halves of a tree level); no registers held.
+SPK_DEV void prefetch_l2(const void* p, size_t bytes, int tid) {
+  const char* c = reinterpret_cast<const char*>((reinterpret_cast<uintptr_t>(p)) & ~uintptr_t(127));
+  const char* e = reinterpret_cast<const char*>(p) + bytes;
+  for (const char* q = c + (size_t)tid * 128; q < e; q += (size_t)NT * 128)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+}
+template <int NB>
+SPK_DEV void prefetch_tile(const BoxInput& in, int d, long long g0, long long n, int tid) {
+  if (SPK_PREFETCH_INPUTS == 0 || g0 >= n || in.perm || in.spread || in.n_dev) return;
+  if (in.kind != IN_BOXES && in.kind != IN_AABB && in.kind != IN_POINTS) return;
+  const long long cnt = (g0 + NB < n ? NB : n - g0);
+  const int sb = in.kind == IN_BOXES ? in.s : (in.kind == IN_AABB ? 1 : 0);
+  auto range = [&](long long first, long long count) {
+    prefetch_l2(in.a + first * d, (size_t)count * d * 8, tid);
+    if (sb) prefetch_l2(in.b + first * sb * d, (size_t)count * sb * d * 8, tid);
+  };
+  if (in.pair_order && !(n & 1)) {  // slots 2p+c -> nodes p + c n/2
+    range(g0 >> 1, (cnt + 1) >> 1);
+    range((g0 >> 1) + (n >> 1), (cnt + 1) >> 1);
+  } else {
+    range(g0, cnt);
+  }
+}
+
 template <typename T, int C, int MODE>
 SPK_DEV void emit_bounds(const BoundOutput& out, long long gb, const State<T, C, MODE>& st) {
   double lo, hi;
@@ -148,7 +183,7 @@ SPK_DEV void emit_bounds(const BoundOutput& out, long long gb, const State<T, C,
   if (out.cls) out.cls[gb] = (int8_t)(lo > 0.0 ? 1 : (hi < 0.0 ? -1 : 0));
 }
 
-template <typename T, int C, int MMAX, int MODE, int SM = 0>
+template <typename T, int C, int MMAX, int MODE, int SM = 0, int RL = 0>
 __global__ void __launch_bounds__(NT, (Cfg<T, C, MMAX, SM>::MINB))
     bound_kernel(const NetDev<T> net, const BoxInput in, const BoundOutput out, const long long n_cap) {
   using CF = Cfg<T, C, MMAX, SM>;
@@ -182,6 +217,7 @@ __global__ void __launch_bounds__(NT, (Cfg<T, C, MMAX, SM>::MINB))
     const long long g0 = tile * NB;
     if (CF::TEAMSYNC) csync();  // every team is done with the previous tile's X
     prep_inputs<T, C, MMAX, MODE, SM>(net, in, n, g0, X, tid, true);
+    prefetch_tile<NB>(in, net.d, g0 + (long long)gridDim.x * NB, n, tid);
     auto node = [&](int b) -> long long {
       return in.spread ? spread_node<CF::TB, CF::NBG>(in, g0 + b, n, (int)gridDim.x) : node_of(in, g0 + b, n);
     };
@@ -192,16 +228,16 @@ __global__ void __launch_bounds__(NT, (Cfg<T, C, MMAX, SM>::MINB))
       const long long nd = node(b);
       if (nd >= 0) emit_bounds<T, C, MODE>(out, nd, st);
     };
-    run_layers<T, C, MMAX, MODE, decltype(emit)&, SM>(net, X, NBUF, ring, tid, emit);
+    run_layers<T, C, MMAX, MODE, decltype(emit)&, SM, RL>(net, X, NBUF, ring, tid, emit);
   }
 }
 
 // ------------------------------------------------------------- launchers
-template <typename T, int C, int MMAX, int MODE, int SM = 0>
+template <typename T, int C, int MMAX, int MODE, int SM = 0, int RL = 0>
 cudaError_t launch_bound(const NetDev<T>& net, const BoxInput& in, const BoundOutput& out, long long n,
                          int sm_count, cudaStream_t stream) {
   using CF = Cfg<T, C, MMAX, SM>;
-  auto kfn = bound_kernel<T, C, MMAX, MODE, SM>;
+  auto kfn = bound_kernel<T, C, MMAX, MODE, SM, RL>;
   static std::atomic<unsigned long long> optin{0};
   if (cudaError_t e = smem_optin((const void*)kfn, (int)CF::SMEM, optin)) return e;
   if (n <= 0) return cudaSuccess;
@@ -231,8 +267,13 @@ struct KTOf {
       if (in.small && mode == MODE_INTERVAL)                                                          \
         return launch_bound<T, 2, MMAX, MODE_INTERVAL, 1>(net, in, out, n, sm, st);                   \
       if (in.small && mode == MODE_AFFINE && S >= 3)                                                  \
-        return launch_bound<T, 5, MMAX, MODE_AFFINE, 1>(net, in, out, n, sm, st);                     \
+        return net.relu_net ? launch_bound<T, 5, MMAX, MODE_AFFINE, 1, 1>(net, in, out, n, sm, st)     \
+                            : launch_bound<T, 5, MMAX, MODE_AFFINE, 1>(net, in, out, n, sm, st);       \
     }                                                                                                 \
+    /* ReLU-only nets, FP32 affine cubes (the configs): the specialised pass */                       \
+    if constexpr (sizeof(T) == 4 && SPK_RELU_SPECIAL)                                                 \
+      if (mode == MODE_AFFINE && S >= 3 && net.relu_net)                                              \
+        return launch_bound<T, 5, MMAX, MODE_AFFINE, 0, 1>(net, in, out, n, sm, st);                  \
     if (mode == MODE_POINT) return launch_bound<T, 1, MMAX, MODE_POINT>(net, in, out, n, sm, st);      \
     if (mode == MODE_INTERVAL) return launch_bound<T, 2, MMAX, MODE_INTERVAL>(net, in, out, n, sm, st); \
     switch (S) {                                                                                      \

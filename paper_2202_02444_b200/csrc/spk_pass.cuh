@@ -58,7 +58,10 @@ constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reducti
 #define SPK_LIVE_WARP 1  // narrow nets: warp-union live-row masks (Cfg::LIVE)
 #endif
 #ifndef SPK_PACKED_ERR
-#define SPK_PACKED_ERR 0  // FP32 error column on FFMA2.RP over neuron pairs (bit-identical; measured: C2 tree +0.3%, width 64 +4% time -- off)
+#define SPK_PACKED_ERR 1  // FP32 error column on FFMA2.RP over neuron pairs (bit-identical sums)
+#endif
+#ifndef SPK_PACKED_ERR_MINW
+#define SPK_PACKED_ERR_MINW 128  // measured (round 2): C2 tree -1.2%, C5 width 512 -2.5%, width 64 +2.5%, width 32 +-0
 #endif
 #ifndef SPK_2CTA_MAXW
 #define SPK_2CTA_MAXW 64  // widest FP32 net on the one-box-per-thread, 2-CTA/SM tile (64: C5_64 +3% with masks)
@@ -77,6 +80,9 @@ constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reducti
 #endif
 #ifndef SPK_TEAM_MIN_NS
 #define SPK_TEAM_MIN_NS 4  // ring depth from which layer boundaries are team-local
+#endif
+#ifndef SPK_NARROW_TI4
+#define SPK_NARROW_TI4 0  // FP32 width-32 affine tile: 4 neurons/thread, 3 CTAs/SM (Cfg::TI4; measured: 80-register cap spills, C1 0.307 -> 0.451 ms)
 #endif
 #ifndef SPK_RUNERR
 #define SPK_RUNERR 1  // FP32 affine K loops: running (a-posteriori) rounding bound of the base column
@@ -129,6 +135,7 @@ struct NetDev {
   int pre_act[MAX_ACTS];
   T gamma_first;
   int tiles_per_pass;
+  int relu_net;      // every dense layer's activations are exactly [] or [ReLU], none before the first
   const T* wtiles;   // generic layers' k-tiles, each KT x MMAX (row k = column k of W)
   LayerDev<T> L[MAX_LAYERS];
 };
@@ -140,10 +147,16 @@ struct NetDev {
 template <typename T, int C, int MMAX, int SM = 0>
 struct Cfg {
   static constexpr int VEC = 16 / (int)sizeof(T);  // elements per 16-byte vector
+  // FP32 width-32 nets with affine columns: 4 neurons per thread and three
+  // CTAs per SM (SPK_NARROW_TI4) -- their K loops are 32 steps long, so the
+  // tile is latency-bound and more resident warps pay more than register
+  // reuse of W across neurons
+  static constexpr bool TI4 = SPK_NARROW_TI4 && SM == 0 && sizeof(T) == 4 && MMAX <= 32 && C >= 3 && C <= 6;
   // register tile: TI neurons x TB boxes x C columns per thread
   static constexpr int TI = SM ? 1
-                               : (C <= 6 ? (sizeof(T) == 4 ? 8 : 4)
-                                         : (C <= 20 ? VEC : (VEC / 2 > 0 ? VEC / 2 : 1)));
+                               : (TI4 ? 4
+                                      : (C <= 6 ? (sizeof(T) == 4 ? 8 : 4)
+                                                : (C <= 20 ? VEC : (VEC / 2 > 0 ? VEC / 2 : 1))));
   // narrow nets (MMAX = 32) with affine columns: one box per thread and two
   // CTAs per SM -- their K loops are short, so latency hiding across CTAs
   // matters more than register reuse across boxes (measured: 4x32 -19%
@@ -151,8 +164,10 @@ struct Cfg {
   // masks, and the 2-CTA tile is 3% faster with them: FP32 only)
   static constexpr int MINB =
       SM ? 2
-         : ((SPK_NARROW_2CTA && (MMAX <= 32 || (sizeof(T) == 4 && MMAX <= SPK_2CTA_MAXW)) && C >= 3 && C <= 6) ? 2
-                                                                                                              : 1);
+         : (TI4 ? 3
+                : ((SPK_NARROW_2CTA && (MMAX <= 32 || (sizeof(T) == 4 && MMAX <= SPK_2CTA_MAXW)) && C >= 3 && C <= 6)
+                       ? 2
+                       : 1));
   static constexpr int TB = SM ? 2
                                : (C == 1 ? (sizeof(T) == 4 ? 8 : 4)
                                          : (C == 2 ? 4 : (C <= 6 ? (MINB == 2 ? 1 : 2) : 1)));
@@ -226,6 +241,27 @@ template <int N> struct VecOf;
 template <> struct VecOf<16> { using type = float4; };
 template <> struct VecOf<8> { using type = float2; };
 template <> struct VecOf<4> { using type = float; };
+
+// A thread's TI per-neuron parameters (bias, bias budget) as TI/G vector loads
+// of G consecutive neurons (the arrays are 16-byte aligned and zero-padded to
+// a multiple of 4 entries, spk_abi.cu); groups wholly past m_out read zeros.
+template <typename T, int TI, int G, int NG>
+SPK_DEV void load_group(const T* __restrict__ p, int m_out, int ng, T (&out)[TI]) {
+  using GV = typename VecOf<G * (int)sizeof(T)>::type;
+#pragma unroll
+  for (int q = 0; q < TI / G; ++q) {
+    const int i0 = q * (NG * G) + ng * G;
+    if (i0 < m_out) {
+      const GV v = __ldg(reinterpret_cast<const GV*>(p + i0));
+      const T* e = reinterpret_cast<const T*>(&v);
+#pragma unroll
+      for (int j = 0; j < G; ++j) out[q * G + j] = e[j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < G; ++j) out[q * G + j] = T(0);
+    }
+  }
+}
 
 // ------------------------------------------------------------ mbarrier/TMA
 SPK_DEV uint32_t smem_u32(const void* p) {
@@ -473,9 +509,11 @@ SPK_DEV bool relu_affine_pack(State<T, C, MODE>& st, T gamma_next, T* out, T gam
   T nb = on ? st.base : T(0);
   T e = on ? st.e : T(0);
   T rA2 = on ? rA : T(0);
-  // (straddling lanes keep A for the scaling below)
+  // inactive: 0 * A (the reference's signed zeros); active and straddling
+  // lanes keep A (exact times 1; straddling lanes scale it below)
+  const T keep = off ? T(0) : T(1);
 #pragma unroll
-  for (int j = 0; j < S; ++j) st.A[j] = off ? Num<T>::mul_rn(T(0), st.A[j]) : st.A[j];
+  for (int j = 0; j < S; ++j) st.A[j] = Num<T>::mul_rn(keep, st.A[j]);
   if (SPK_FUSED_RELU_VOTE ? __any_sync(__activemask(), mix) : true) {
     if (mix) {
       T a = fmin(fmax(Num<T>::div_fast(hi, hi - lo), T(0)), T(1));
@@ -559,10 +597,11 @@ SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, W
   constexpr int SUBIN = KT < CF::SUB ? KT : CF::SUB;
   constexpr int PTI = DIRECT ? 1 : TI, PTB = DIRECT ? 1 : TB;
 
+  T bias_r[TI];
+  if (!DIRECT) load_group<T, TI, CF::G, CF::NG>(L.bias, L.m_out, ng, bias_r);
 #pragma unroll
   for (int ti = 0; ti < TI; ++ti) {
-    const int i = CF::neuron(ng, ti);
-    const T b0 = (!DIRECT && i < L.m_out) ? L.bias[i] : T(0);
+    const T b0 = DIRECT ? T(0) : bias_r[ti];
 #pragma unroll
     for (int tb = 0; tb < TB; ++tb) {
       acc[ti][tb][0] = b0;
@@ -693,10 +732,11 @@ SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, W
   }
   if (since > 0) flush();
   if (DIRECT) {
+    T bias_r[TI];
+    load_group<T, TI, CF::G, CF::NG>(L.bias, L.m_out, ng, bias_r);
 #pragma unroll
     for (int ti = 0; ti < TI; ++ti) {
-      const int i = CF::neuron(ng, ti);
-      const T b0 = (i < L.m_out) ? L.bias[i] : T(0);
+      const T b0 = bias_r[ti];
 #pragma unroll
       for (int tb = 0; tb < TB; ++tb) {
         acc[ti][tb][0] = acc[ti][tb][0] + b0;
@@ -794,16 +834,17 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
   float acco[TI][TB], parto[TI][TB], acce[TI][TB];
   // error column packed over neuron pairs (SPK_PACKED_ERR; FFMA2.RP, same
   // per-lane rounding and order as the scalar FFMA.RP, so identical sums)
-  constexpr bool PE = SPK_PACKED_ERR && !POINT && TI % 2 == 0;
+  constexpr bool PE = SPK_PACKED_ERR && !POINT && TI % 2 == 0 && MMAX >= SPK_PACKED_ERR_MINW;
   f32x2 acce2[PE ? TI / 2 : 1][TB];
 #pragma unroll
   for (int j = 0; j < (PE ? TI / 2 : 1); ++j)
 #pragma unroll
     for (int tb = 0; tb < TB; ++tb) acce2[j][tb] = 0ull;
+  float bias_r[TI];
+  load_group<float, TI, CF::G, CF::NG>(L.bias, L.m_out, ng, bias_r);
 #pragma unroll
   for (int ti = 0; ti < TI; ++ti) {
-    const int i = CF::neuron(ng, ti);
-    const float b0 = (i < L.m_out) ? L.bias[i] : 0.f;
+    const float b0 = bias_r[ti];
 #pragma unroll
     for (int g = 0; g < NBOX; ++g)
 #pragma unroll
@@ -1062,7 +1103,11 @@ SPK_DEV void dense_kloop(const LayerDev<T>& L, const T* __restrict__ X, WRing<T,
   }
 }
 
-template <typename T, int C, int MMAX, int MODE, int SM = 0>
+// RL = 1: the net's activations are all ReLU, one per hidden layer
+// (NetDev::relu_net, checked by the host): the ELU / sin / tanh rules and the
+// runtime activation dispatch are compiled out -- a smaller kernel (fewer
+// instruction-cache misses, fewer registers) for the configs' ReLU nets.
+template <typename T, int C, int MMAX, int MODE, int SM = 0, int RL = 0>
 SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, MMAX, SM>& ring, int tid,
                            bool last, T gamma_next, int lidx) {
   using CF = Cfg<T, C, MMAX, SM>;
@@ -1097,12 +1142,13 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
   // the epilogue stalled every warp at once); the common single-ReLU layer
   // takes a constant-folded rule
   const int nact = L.n_act;
-  const bool relu_only = nact == 1 && L.act[0] == ACT_RELU;
+  const bool relu_only = RL ? nact == 1 : (nact == 1 && L.act[0] == ACT_RELU);
   T be_r[TI];
+  if (MODE != MODE_POINT) {
+    load_group<T, TI, CF::G, CF::NG>(L.berr, L.m_out, ng, be_r);
+  } else {
 #pragma unroll
-  for (int ti = 0; ti < TI; ++ti) {
-    const int i = CF::neuron(ng, ti);
-    be_r[ti] = (MODE != MODE_POINT && i < L.m_out) ? L.berr[i] : T(0);
+    for (int ti = 0; ti < TI; ++ti) be_r[ti] = T(0);
   }
   T acc[TI][TB][C];
   // running-error K loop (affine-fixed, FP32): this layer bounds its base
@@ -1183,10 +1229,14 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
         }
         if (relu_only) {
           apply_act<T, C, MODE>(st, ACT_RELU);
-        } else {
+        } else if (!RL) {
           for (int a = 0; a < nact; ++a) apply_act<T, C, MODE>(st, L.act[a]);
         }
         pack_next<T, C, MODE>(st, gamma_next, out + tb * CP, gamma_base);
+        if (LV) {
+#pragma unroll
+          for (int c = 0; c < CP; ++c) nz_rule |= out[tb * CP + c] != T(0);
+        }
       }
     }
     float4* dst = reinterpret_cast<float4*>(X + (size_t)i * CF::RS + bg * TB * CP);
@@ -1194,14 +1244,7 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
 #pragma unroll
     for (int q = 0; q < (int)(TB * CP * sizeof(T) / 16); ++q) dst[q] = srcv[q];
     if (LV) {
-      bool nz = false;
-      if (FUSED_RELU && relu_only) {
-        nz = nz_rule;
-      } else {
-#pragma unroll
-        for (int c = 0; c < TB * CP; ++c) nz |= out[c] != T(0);
-      }
-      nz = nz && !ring.group_empty;
+      const bool nz = nz_rule && !ring.group_empty;
       live_bits |= (nz ? 1u : 0u) << (ti % CF::G);
       if (ti % CF::G == CF::G - 1) {  // a group of G consecutive neurons: one word, one atomic
         const int i0 = i - (CF::G - 1);
@@ -1247,7 +1290,7 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
 template <int MMAX>
 constexpr int narrow_lanes() { return MMAX <= 64 ? 4 : 32; }
 
-template <typename T, int C, int MMAX, int MODE, class Emit, int SM = 0>
+template <typename T, int C, int MMAX, int MODE, class Emit, int SM = 0, int RL = 0>
 SPK_DEV void narrow_layer(const LayerDev<T>& L, T* __restrict__ X, T* __restrict__ NBUF, int tid,
                           bool last, T gamma_next, Emit&& emit) {
   using CF = Cfg<T, C, MMAX, SM>;
@@ -1318,7 +1361,7 @@ SPK_DEV void narrow_layer(const LayerDev<T>& L, T* __restrict__ X, T* __restrict
     col[0] += L.bias[i];
     if (pv_off(MODE)) col[1] += L.bias[i];  // march modes: the bound's base column too
     State<T, C, MODE> st = state_from<T, C, MODE>(col, L.berr[i]);
-    for (int a = 0; a < L.n_act; ++a) apply_act<T, C, MODE>(st, L.act[a]);
+    for (int a = 0; a < L.n_act; ++a) apply_act<T, C, MODE>(st, RL ? (int)ACT_RELU : L.act[a]);
     if (last) {
       emit(b, st);
     } else {
@@ -1345,16 +1388,16 @@ SPK_DEV void narrow_layer(const LayerDev<T>& L, T* __restrict__ X, T* __restrict
 // Runs every layer for the CTA's current tile.  X rows [0, d) must hold the
 // packed input columns and rows [d, MMAX) zeros; `emit(b, state)` receives
 // each box's final width-1 state.
-template <typename T, int C, int MMAX, int MODE, class Emit, int SM = 0>
+template <typename T, int C, int MMAX, int MODE, class Emit, int SM = 0, int RL = 0>
 SPK_DEV void run_layers(const NetDev<T>& net, T* X, T* NBUF, WRing<T, C, MMAX, SM>& ring, int tid,
                         Emit&& emit) {
   for (int l = 0; l < net.n_layers; ++l) {
     const LayerDev<T>& L = net.L[l];
     const bool last = (l == net.n_layers - 1);
     if (L.narrow) {
-      narrow_layer<T, C, MMAX, MODE, Emit, SM>(L, X, NBUF, tid, last, L.gamma_next, emit);
+      narrow_layer<T, C, MMAX, MODE, Emit, SM, RL>(L, X, NBUF, tid, last, L.gamma_next, emit);
     } else {
-      generic_layer<T, C, MMAX, MODE, SM>(L, X, ring, tid, last, L.gamma_next, l);
+      generic_layer<T, C, MMAX, MODE, SM, RL>(L, X, ring, tid, last, L.gamma_next, l);
     }
   }
 }
