@@ -81,6 +81,9 @@ constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reducti
 #ifndef SPK_TEAM_MIN_NS
 #define SPK_TEAM_MIN_NS 4  // ring depth from which layer boundaries are team-local
 #endif
+#ifndef SPK_ONE_BLOCK
+#define SPK_ONE_BLOCK 1  // FP32 nets of width <= SPK_SUB_F32: accumulate onto the bias, no partials
+#endif
 #ifndef SPK_NARROW_TI4
 #define SPK_NARROW_TI4 0  // FP32 width-32 affine tile: 4 neurons/thread, 3 CTAs/SM (Cfg::TI4; measured: 80-register cap spills, C1 0.307 -> 0.451 ms)
 #endif
@@ -862,9 +865,15 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
   constexpr int SUBIN = KT < CF::SUB ? KT : CF::SUB;
   // every SUBIN chunk starts a fresh blocked-summation block (KT a multiple of SUB)
   constexpr bool ALWAYS_FRESH = (KT % CF::SUB) == 0;
+  // nets no wider than one summation block (width <= SUB, e.g. C1's 4x32):
+  // every layer is a single block, so the products accumulate straight onto
+  // the bias -- an (m_in + 1)-term chain inside the same gamma_{m_in + 2}
+  // budget -- with no partial registers, zeroing or flushes
+  constexpr bool ONEBLK = SPK_ONE_BLOCK && MMAX <= CF::SUB && !RUN;
   int since = 0;
   // partial sums -> running sums (a fresh block re-initialises the partials)
   auto flush = [&](auto rec) {
+    if (ONEBLK) return;
     constexpr bool REC = decltype(rec)::value && RUN;
 #pragma unroll
     for (int ti = 0; ti < TI; ++ti) {
@@ -885,6 +894,7 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
     }
   };
   auto zero_parts = [&]() {
+    if (ONEBLK) return;
 #pragma unroll
     for (int ti = 0; ti < TI; ++ti) {
 #pragma unroll
@@ -921,7 +931,8 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
           const f32x2 xv = xq[POINT ? p : (g * CP) / 2 + p];
-          partp[ti][g][p] = FIRST ? f2_mul(w[ti], xv) : f2_fma(w[ti], xv, partp[ti][g][p]);
+          f32x2& dst = ONEBLK ? accp[ti][g][p] : partp[ti][g][p];
+          dst = (FIRST && !ONEBLK) ? f2_mul(w[ti], xv) : f2_fma(w[ti], xv, dst);
           if (REC && p == 0) {
             // Wilkinson's running bound sum_k |s_k|.  Only steps whose base
             // input is nonzero can round (an exact-zero x leaves s_k ==
@@ -948,7 +959,8 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
           if (ODD) {
             float ol, oh;
             f2_split(xq[(tb * CP + 2 * NP) / 2], ol, oh);
-            parto[ti][tb] = FIRST ? __fmul_rn(w[ti], ol) : __fmaf_rn(w[ti], ol, parto[ti][tb]);
+            float& dso = ONEBLK ? acco[ti][tb] : parto[ti][tb];
+            dso = (FIRST && !ONEBLK) ? __fmul_rn(w[ti], ol) : __fmaf_rn(w[ti], ol, dso);
           }
         }
       }
