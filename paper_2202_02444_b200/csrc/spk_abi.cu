@@ -151,6 +151,15 @@ int build_device_net(spk_net* net, DevNet<T>& dn) {
       // warp butterfly (32 lanes; K3F) or 4-lane groups (nets of width <= 64)
       const int lp = mmax <= 64 ? 4 : 32;
       n_eff = std::max((L.m_in + 31) / 32 + 6, (L.m_in + lp - 1) / lp + 3);
+      // the fused output layer of the ReLU-specialised passes (spk_pass.cuh
+      // generic_layer FF, nets of width <= 64): a TI-term chain per thread,
+      // log2(NG) butterfly levels, the bias -- TI = 8 neurons per thread,
+      // NG = mmax / 8
+      if (mmax <= 64) {
+        int lg = 0;
+        while ((8 << lg) < mmax) ++lg;
+        n_eff = std::max(n_eff, 8 + lg + 1);
+      }
     } else {
       const int nt = (L.m_in + KT - 1) / KT;
       const int sub = sub_for<T>(mmax);

@@ -70,10 +70,18 @@ template <> struct Num<double> {
   SPK_DEV static double from_d_rd(double x) { return x; }
 };
 
-// Upper bound of |x - fl(x)| when converting an exact double to T.
+// Upper bound of |x - fl(x)| when converting an exact double to T.  FP32:
+// |x - RN(x)| <= u |x| <= u/(1-u) |RN(x)| for normal results, plus 2^-150
+// below the normal range -- one FFMA.RP instead of the exact residual's two
+// FP64 conversions and a DADD (slow-pipe ops on every input coordinate).
 template <typename T>
 SPK_DEV T conv_err(double x, T xt) {
-  return Num<T>::from_d_ru(fabs(x - (double)xt));
+  if constexpr (sizeof(T) == 4) {
+    (void)x;
+    return __fmaf_ru(fabsf(xt), 0x1.000002p-24f, 0x1p-149f);
+  } else {
+    return Num<T>::from_d_ru(fabs(x - (double)xt));
+  }
 }
 
 // gamma_n = n u / (1 - n u), rounded up: the classic bound on the rounding

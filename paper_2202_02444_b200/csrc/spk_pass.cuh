@@ -81,6 +81,9 @@ constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reducti
 #ifndef SPK_TEAM_MIN_NS
 #define SPK_TEAM_MIN_NS 4  // ring depth from which layer boundaries are team-local
 #endif
+#ifndef SPK_FUSE_FINAL
+#define SPK_FUSE_FINAL 1  // ReLU-specialised passes: width-1 output layer folded into the last epilogue
+#endif
 #ifndef SPK_ONE_BLOCK
 #define SPK_ONE_BLOCK 1  // FP32 nets of width <= SPK_SUB_F32: accumulate onto the bias, no partials
 #endif
@@ -1119,12 +1122,34 @@ SPK_DEV void dense_kloop(const LayerDev<T>& L, const T* __restrict__ X, WRing<T,
 // (NetDev::relu_net, checked by the host): the ELU / sin / tanh rules and the
 // runtime activation dispatch are compiled out -- a smaller kernel (fewer
 // instruction-cache misses, fewer registers) for the configs' ReLU nets.
-template <typename T, int C, int MMAX, int MODE, int SM = 0, int RL = 0>
+struct NoEmit {
+  template <class S> SPK_DEV void operator()(int, const S&) const {}
+};
+
+// FF (fused final): this is the last hidden layer and the next one is the
+// width-1 output layer without activations (Lf).  Instead of writing X and
+// running narrow_layer, each thread folds its packed neurons straight into the
+// output's columns (RN FMA chain over its TI neurons, RU error column), the NG
+// threads of a box group combine them with a butterfly, and the group's first
+// lane emits the bound: chain length TI + log2(NG) + 1, inside the output
+// layer's rounding budget (spk_abi.cu).  No X stores, no staging, no syncs.
+template <typename T, int C, int MMAX, int MODE, int SM = 0, int RL = 0, bool FF = false, class Emit = NoEmit>
 SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, MMAX, SM>& ring, int tid,
-                           bool last, T gamma_next, int lidx) {
+                           bool last, T gamma_next, int lidx, const LayerDev<T>* Lf = nullptr,
+                           Emit* emit = nullptr) {
   using CF = Cfg<T, C, MMAX, SM>;
   constexpr int TI = CF::TI, TB = CF::TB, CP = CF::CP;
   const int ng = tid % CF::NG, bg = tid / CF::NG;
+  static_assert(!FF || (CF::NG <= 32 && MODE == MODE_AFFINE), "fused final layer: box group within a warp");
+  T wf[FF ? TI : 1];
+  T fin[FF ? TB : 1][FF ? C : 1];
+  if constexpr (FF) {
+    load_group<T, TI, CF::G, CF::NG>(Lf->w, Lf->m_in, ng, wf);
+#pragma unroll
+    for (int tb = 0; tb < TB; ++tb)
+#pragma unroll
+      for (int c = 0; c < C; ++c) fin[tb][c] = T(0);
+  }
   // live-row masks (Cfg::LIVE; bound modes): this layer reads parity lidx&1
   // (written by the previous epilogue; the first layer reads every row) and
   // its epilogue fills the other parity, cleared here -- its last reader
@@ -1237,6 +1262,11 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
         State<T, C, MODE> st = state_from<T, C, MODE>(acc[ti][tb], be);
         if (FUSED_RELU && relu_only) {
           nz_rule |= relu_affine_pack<T, C, MODE>(st, gamma_next, out + tb * CP, gamma_base);
+          if constexpr (FF) {
+#pragma unroll
+            for (int c = 0; c < C - 1; ++c) fin[tb][c] = Num<T>::fma_rn(wf[ti], out[tb * CP + c], fin[tb][c]);
+            fin[tb][C - 1] = Num<T>::fma_ru(fabs(wf[ti]), out[tb * CP + C - 1], fin[tb][C - 1]);
+          }
           continue;
         }
         if (relu_only) {
@@ -1245,12 +1275,18 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
           for (int a = 0; a < nact; ++a) apply_act<T, C, MODE>(st, L.act[a]);
         }
         pack_next<T, C, MODE>(st, gamma_next, out + tb * CP, gamma_base);
+        if constexpr (FF) {
+#pragma unroll
+          for (int c = 0; c < C - 1; ++c) fin[tb][c] = Num<T>::fma_rn(wf[ti], out[tb * CP + c], fin[tb][c]);
+          fin[tb][C - 1] = Num<T>::fma_ru(fabs(wf[ti]), out[tb * CP + C - 1], fin[tb][C - 1]);
+        }
         if (LV) {
 #pragma unroll
           for (int c = 0; c < CP; ++c) nz_rule |= out[tb * CP + c] != T(0);
         }
       }
     }
+    if constexpr (FF) continue;  // nothing goes back to X
     float4* dst = reinterpret_cast<float4*>(X + (size_t)i * CF::RS + bg * TB * CP);
     const float4* srcv = reinterpret_cast<const float4*>(out);
 #pragma unroll
@@ -1281,7 +1317,27 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
       }
     }
   }
-  if (XMASK && m_nxt != nullptr && ng == 0) {
+  if constexpr (FF) {
+    // the box group's NG lanes (consecutive, NG | 32) combine their partials
+#pragma unroll
+    for (int off = 1; off < CF::NG; off <<= 1) {
+#pragma unroll
+      for (int tb = 0; tb < TB; ++tb)
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const T o = __shfl_xor_sync(0xffffffffu, fin[tb][c], off);
+          fin[tb][c] = c == C - 1 ? Num<T>::add_ru(fin[tb][c], o) : fin[tb][c] + o;
+        }
+    }
+    if (ng == 0) {
+#pragma unroll
+      for (int tb = 0; tb < TB; ++tb) {
+        fin[tb][0] += Lf->bias[0];
+        State<T, C, MODE> st = state_from<T, C, MODE>(fin[tb], Lf->berr[0]);
+        (*emit)(bg * TB + tb, st);
+      }
+    }
+  } else if (XMASK && m_nxt != nullptr && ng == 0) {
 #pragma unroll
     for (int w = 0; w < CF::LW; ++w) m_nxt[w] = xw[w];
   }
@@ -1403,11 +1459,24 @@ SPK_DEV void narrow_layer(const LayerDev<T>& L, T* __restrict__ X, T* __restrict
 template <typename T, int C, int MMAX, int MODE, class Emit, int SM = 0, int RL = 0>
 SPK_DEV void run_layers(const NetDev<T>& net, T* X, T* NBUF, WRing<T, C, MMAX, SM>& ring, int tid,
                         Emit&& emit) {
+  using CF = Cfg<T, C, MMAX, SM>;
+  // ReLU-specialised affine passes fold the width-1 output layer into the
+  // last hidden layer's epilogue (generic_layer FF)
+  // (narrow nets only: at width 256 the 5-level butterfly per thread cost
+  // +11% on the C2 tree vs the narrow layer's 32-lane split, and the small
+  // tile would need the same order to stay bit-identical)
+  constexpr bool FUSE = SPK_FUSE_FINAL && RL && MODE == MODE_AFFINE && CF::NG <= 32 && MMAX <= 64;
   for (int l = 0; l < net.n_layers; ++l) {
     const LayerDev<T>& L = net.L[l];
     const bool last = (l == net.n_layers - 1);
     if (L.narrow) {
       narrow_layer<T, C, MMAX, MODE, Emit, SM, RL>(L, X, NBUF, tid, last, L.gamma_next, emit);
+    } else if (FUSE && l + 2 == net.n_layers && net.L[l + 1].narrow && net.L[l + 1].m_out == 1 &&
+               net.L[l + 1].n_act == 0) {
+      using E = typename std::remove_reference<Emit>::type;
+      generic_layer<T, C, MMAX, MODE, SM, RL, FUSE, E>(L, X, ring, tid, false, L.gamma_next, l, &net.L[l + 1],
+                                                       &emit);
+      break;
     } else {
       generic_layer<T, C, MMAX, MODE, SM, RL>(L, X, ring, tid, last, L.gamma_next, l);
     }
