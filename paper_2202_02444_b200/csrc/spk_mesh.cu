@@ -7,8 +7,9 @@
 //    the children interleaved (a0, b0, a1, b1, ...) as meshing.py:152-162
 //    builds them; ballot/prefix compaction as in the tree build.
 // 2. Dense stage per chunk of surviving blocks: the (S+1)^3 corner lattice of
-//    every block (meshgrid 'ij' order, meshing.py:87-97) goes through the
-//    point-evaluation pass; per cell the case code (bit c set when corner c
+//    every block (meshgrid 'ij' order, meshing.py:87-97); the chunk's distinct
+//    grid corners (blocks share face lattices) go through the point-evaluation
+//    pass once and are scattered back; per cell the case code (bit c set when corner c
 //    < 0), triangle count from the reference's generated TRI_TABLE
 //    (mc_tables.py:72-95), exclusive scan, and emission of every triangle
 //    vertex as (global edge key, interpolated position) in exactly the
@@ -32,6 +33,10 @@
 namespace spk {
 
 constexpr int MK = 256;
+
+#ifndef SPK_MESH_DEDUP
+#define SPK_MESH_DEDUP 1  // evaluate each distinct grid corner of a chunk once
+#endif
 
 struct GridDev {
   double lo[3], hi[3], step[3];
@@ -114,6 +119,37 @@ __global__ void corner_points_kernel(long long nb, const int* __restrict__ org, 
   pts[q * 3 + 0] = grid_coord(G, 0, org[b * 3 + 0] + a);
   pts[q * 3 + 1] = grid_coord(G, 1, org[b * 3 + 1] + bb);
   pts[q * 3 + 2] = grid_coord(G, 2, org[b * 3 + 2] + c);
+}
+
+// global grid index of every corner of the chunk's lattices (the dedup key)
+__global__ void corner_keys_kernel(long long nb, const int* __restrict__ org, int S, long long np1,
+                                   unsigned long long* __restrict__ keys, long long* __restrict__ idx) {
+  const int P = S + 1;
+  const long long q = (long long)blockIdx.x * MK + threadIdx.x;
+  if (q >= nb * P * P * P) return;
+  const long long b = q / (P * P * P);
+  const int r = (int)(q % (P * P * P));
+  const int a = r / (P * P), bb = (r / P) % P, c = r % P;
+  keys[q] = (unsigned long long)(((long long)(org[b * 3 + 0] + a) * np1 + (org[b * 3 + 1] + bb)) * np1 +
+                                 (org[b * 3 + 2] + c));
+  idx[q] = q;
+}
+
+// unique corners of a sorted key run: the head of each run writes its point
+__global__ void unique_points_kernel(long long n, const unsigned long long* __restrict__ sk,
+                                     const long long* __restrict__ sidx, const int* __restrict__ runid,
+                                     const double* __restrict__ pts, double* __restrict__ upts) {
+  const long long q = (long long)blockIdx.x * MK + threadIdx.x;
+  if (q >= n || !(q == 0 || sk[q] != sk[q - 1])) return;
+  const long long u = runid[q] - 1, src = sidx[q];
+  for (int x = 0; x < 3; ++x) upts[u * 3 + x] = pts[src * 3 + x];
+}
+
+// every lattice corner takes its unique point's value
+__global__ void scatter_values_kernel(long long n, const long long* __restrict__ sidx, const int* __restrict__ runid,
+                                      const double* __restrict__ uvals, double* __restrict__ vals) {
+  const long long q = (long long)blockIdx.x * MK + threadIdx.x;
+  if (q < n) vals[sidx[q]] = uvals[runid[q] - 1];
 }
 
 SPK_DEV int cell_case(const double* __restrict__ v, int P, int a, int b, int c) {
@@ -421,11 +457,51 @@ int spk_mesh_extract_shard(const spk_net* net, int policy, int n_keep, int preci
     if (pool.err != cudaSuccess) { rc = cuda_fail(pool.err, "mesh alloc"); break; }
     const long long np_ = cb * pts_per, nc = cb * cells_per;
     corner_points_kernel<<<(int)((np_ + MK - 1) / MK), MK, 0, st>>>(cb, corg, S, G, pts);
-    cudaEventRecord(ev0, st);
-    rc = spk_eval_batch(net, precision, np_, pts, vals, st);
-    cudaEventRecord(ev1, st);
-    if (rc != SPK_OK) break;
-    mesh->evals += np_;
+    long long n_eval = np_;
+    if (SPK_MESH_DEDUP && cb > 1) {
+      // adjacent surviving blocks share their face lattices: evaluate every
+      // distinct grid corner of the chunk once (sort by global index, unique,
+      // evaluate, scatter back) -- the values are deterministic per point, so
+      // the mesh is unchanged; ~30% fewer evaluations on dense regions
+      const int gblk = (int)((np_ + MK - 1) / MK);
+      unsigned long long* ck = pool.get<unsigned long long>(np_);
+      unsigned long long* sk = pool.get<unsigned long long>(np_);
+      long long* ci = pool.get<long long>(np_);
+      long long* si = pool.get<long long>(np_);
+      int* head = pool.get<int>(np_);
+      int* runid = pool.get<int>(np_);
+      if (pool.err != cudaSuccess) { rc = cuda_fail(pool.err, "mesh alloc"); break; }
+      corner_keys_kernel<<<gblk, MK, 0, st>>>(cb, corg, S, (long long)G.n + 1, ck, ci);
+      size_t tb = 0, tb2 = 0;
+      const int key_bits = 64 - __builtin_clzll((unsigned long long)((long long)(G.n + 1) * (G.n + 1) * (G.n + 1)));
+      cub::DeviceRadixSort::SortPairs(nullptr, tb, ck, sk, ci, si, (int)np_, 0, key_bits, st);
+      cub::DeviceScan::InclusiveSum(nullptr, tb2, head, runid, (int)np_, st);
+      void* tmp = pool.get<char>(std::max(tb, tb2));
+      if (pool.err != cudaSuccess) { rc = cuda_fail(pool.err, "mesh alloc"); break; }
+      cub::DeviceRadixSort::SortPairs(tmp, tb, ck, sk, ci, si, (int)np_, 0, key_bits, st);
+      run_head_kernel<<<gblk, MK, 0, st>>>(np_, sk, head);
+      cub::DeviceScan::InclusiveSum(tmp, tb2, head, runid, (int)np_, st);
+      int nu = 0;
+      cudaMemcpyAsync(&nu, runid + np_ - 1, 4, cudaMemcpyDeviceToHost, st);
+      e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) { rc = cuda_fail(e, "mesh corner dedup"); break; }
+      double* upts = pool.get<double>((long long)nu * 3);
+      double* uvals = pool.get<double>(nu);
+      if (pool.err != cudaSuccess) { rc = cuda_fail(pool.err, "mesh alloc"); break; }
+      unique_points_kernel<<<gblk, MK, 0, st>>>(np_, sk, si, runid, pts, upts);
+      cudaEventRecord(ev0, st);
+      rc = spk_eval_batch(net, precision, nu, upts, uvals, st);
+      cudaEventRecord(ev1, st);
+      if (rc != SPK_OK) break;
+      scatter_values_kernel<<<gblk, MK, 0, st>>>(np_, si, runid, uvals, vals);
+      n_eval = nu;
+    } else {
+      cudaEventRecord(ev0, st);
+      rc = spk_eval_batch(net, precision, np_, pts, vals, st);
+      cudaEventRecord(ev1, st);
+      if (rc != SPK_OK) break;
+    }
+    mesh->evals += n_eval;
     cell_count_kernel<<<(int)((nc + MK - 1) / MK), MK, 0, st>>>(cb, S, vals, cnt);
     size_t tmp_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, off, (int)nc, st);

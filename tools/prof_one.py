@@ -4,6 +4,7 @@
     python tools/prof_one.py c5 [n]    # n on-device cubes through 8x256 (default 2^20)
     python tools/prof_one.py c1        # 64^3 grid through 4x32
     python tools/prof_one.py c5_64 [n] # n on-device cubes through 8x64 (default 2^20)
+    python tools/prof_one.py c5_512 [n] # n on-device cubes through 8x512 (default 2^17)
 """
 import sys
 
@@ -28,9 +29,9 @@ def main():
         n = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 20
         net = synth.config_net("C5_256")
         run = lambda: sp.bound_random_cubes(net, n, seed=1, half=1 / 64)
-    elif which == "c5_64":
-        n = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 20
-        net = synth.config_net("C5_64")
+    elif which in ("c5_64", "c5_512"):
+        n = int(sys.argv[2]) if len(sys.argv) > 2 else (1 << 20 if which == "c5_64" else 1 << 17)
+        net = synth.config_net("C5_64" if which == "c5_64" else "C5_512")
         run = lambda: sp.bound_random_cubes(net, n, seed=1, half=1 / 64)
     elif which in ("eval256", "eval512"):
         net = synth.config_net("C2" if which == "eval256" else "C4")
