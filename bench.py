@@ -414,6 +414,7 @@ def run_ours(args, rank, world, local_rank):
         return out
 
     extra["C2_tree_fp64"] = clocked(bench_c2_fp64, torch, sp, spatial, net, bounds, flush)
+    extra["C2_build_spatial_tree_api"] = clocked(bench_tree_api, torch, sp, spatial, net, bounds)
     extra["C5_8x256_16M"] = clocked(bench_c5, torch, sp, synth, "C5_256", 16 << 20, flush, peak_tf)
     extra["C5_8x64_16M"] = clocked(bench_c5, torch, sp, synth, "C5_64", 16 << 20, flush, peak_tf)
     extra["C5_8x512_4M"] = clocked(bench_c5, torch, sp, synth, "C5_512", 4 << 20, flush, peak_tf)
@@ -478,6 +479,20 @@ def bench_c2_fp64(torch, sp, spatial, net, bounds, flush):
     dt = float(np.median(ts))
     return {"nodes": arr.n_nodes, "boxes_per_s": arr.n_nodes / dt, "ms": dt * 1e3,
             "bound_kernel_ms": arr.bound_ms, "precision": "fp64"}
+
+
+def bench_tree_api(torch, sp, spatial, net, bounds):
+    """The reference-signature call (spatial.py:214): build_spatial_tree(...)
+    -> root TreeNode.  Nodes are materialised lazily from the host level
+    arrays on first access (a full Python traversal of the 524,287 nodes costs
+    ~7 s whichever way they are built; eager construction alone took 6.7 s)."""
+    spatial.build_spatial_tree(net, bounds, policy=sp.AFFINE_FIXED, max_depth=10)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    root = spatial.build_spatial_tree(net, bounds, policy=sp.AFFINE_FIXED, max_depth=DEPTH)
+    dt = time.perf_counter() - t0
+    return {"nodes": (1 << (DEPTH + 1)) - 1, "seconds": dt, "root_children": len(root.children or ()),
+            "api": "build_spatial_tree(net, AABB([-1]*3,[1]*3), policy=AFFINE_FIXED, max_depth=18)"}
 
 
 def bench_host_calls(sp, synth):
