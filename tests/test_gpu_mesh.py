@@ -49,16 +49,20 @@ def test_dense_matches_hierarchical(net_paths):
     assert h.point_evals < d.point_evals
 
 
-def test_mesh_fp32_connectivity(net_paths):
-    """FP32 evaluation: same triangles on every cell whose corner signs agree."""
-    net = sp.load_network(net_paths["relu_sdf"])
+@pytest.mark.parametrize("netname", ["relu_sdf", "elu_sdf"])
+def test_mesh_fp32_connectivity(net_paths, netname):
+    """FP32 evaluation (the north-star rule): the triangles of every grid cell
+    whose 8 corner signs agree between FP32 and FP64 are identical."""
+    from tests.mesh_rules import agreeing_triangle_sets
+
+    net = sp.load_network(net_paths[netname])
     a = meshing.extract_mesh_arrays(net, BOUNDS, 6, 3, "affine-fixed", precision="fp64")
     b = meshing.extract_mesh_arrays(net, BOUNDS, 6, 3, "affine-fixed", precision="fp32")
-    ka = {tuple(r) for r in meshing.triangle_key_set(a.triangles, a.vertex_keys)}
-    kb = {tuple(r) for r in meshing.triangle_key_set(b.triangles, b.vertex_keys)}
-    diff = len(ka ^ kb)
-    assert diff <= 0.001 * len(ka), diff
-    print(f"MESH fp32 vs fp64 differing triangles: {diff} of {len(ka)}")
+    ka, kb, na, nb, bad = agreeing_triangle_sets(net, a, b, 6)
+    assert len(ka) > 0
+    np.testing.assert_array_equal(ka, kb)
+    print(f"MESH {netname} fp32 vs fp64: {len(ka)} triangles identical on agreeing cells; "
+          f"{na} / {nb} on {bad} disagreeing cells")
 
 
 def test_mesh_edge_cases(net_paths):
