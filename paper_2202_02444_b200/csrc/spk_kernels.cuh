@@ -140,7 +140,7 @@ SPK_DEV void prep_inputs(const NetDev<T>& net, const BoxInput& in, long long n, 
         packed[C - 1] = st.e;
       }
     }
-    T* dst = X + (size_t)k * CF::RS + b * CP;
+    T* dst = X + CF::xrow(k) + b * CP;
 #pragma unroll
     for (int c = 0; c < CP; ++c) dst[c] = packed[c];
   }

@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(NT, (Cfg<T, C, MMAX>::MINB))
         for (int a = 0; a < net.n_pre; ++a) apply_act<T, C, MODE>(st, net.pre_act[a]);
         pack_next<T, C, MODE>(st, net.gamma_first, packed);
       }
-      T* dst = X + (size_t)k * CF::RS + b * CP;
+      T* dst = X + CF::xrow(k) + b * CP;
 #pragma unroll
       for (int c = 0; c < CP; ++c) dst[c] = packed[c];
     }

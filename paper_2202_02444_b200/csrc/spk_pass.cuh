@@ -81,6 +81,9 @@ constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reducti
 #ifndef SPK_TEAM_MIN_NS
 #define SPK_TEAM_MIN_NS 4  // ring depth from which layer boundaries are team-local
 #endif
+#ifndef SPK_X_SKEW
+#define SPK_X_SKEW 0  // skewed X rows on wide FP32 tiles (conflict-free epilogue stores; measured C2 +0.8%: off)
+#endif
 #ifndef SPK_FUSE_FINAL
 #define SPK_FUSE_FINAL 1  // ReLU-specialised passes: width-1 output layer folded into the last epilogue
 #endif
@@ -105,6 +108,7 @@ constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reducti
 constexpr int kScalarUnroll = SPK_SCALAR_UNROLL;  // FP64 K loop unroll (A/B knob)
 constexpr int NSTAGE_MIN = 3;   // W tile ring depth floor (deeper when tiles are small)
 constexpr size_t SMEM_BUDGET = 210 * 1024;  // leaves room for the symbolic kernel's extras
+constexpr size_t SMEM_MAX_OPTIN = 227 * 1024;  // sm_100 opt-in limit of dynamic shared memory per CTA
 
 enum Mode : int {
   MODE_POINT = 0,
@@ -190,12 +194,29 @@ struct Cfg {
   // X row stride (elements): 16-byte aligned rows, and an odd number of
   // 16-byte units per row so the epilogue's vector stores spread over banks
   static constexpr int RS0 = ((NB * CP * (int)sizeof(T) + 15) / 16) * 16 / (int)sizeof(T);
-  static constexpr int RS = ((RS0 * (int)sizeof(T) / 16) % 2 == 1) ? RS0 : RS0 + 16 / (int)sizeof(T);
-  static constexpr int XS = MMAX * RS;                   // elements of X
   // a thread's TI neurons: TI/G groups of G consecutive neurons (G elements
   // = one vector load); group q of neuron-group ng starts at q*NG*G + ng*G,
   // so a warp's vector loads of a W row are contiguous (bank-conflict free)
   static constexpr int G = TI < VEC ? TI : VEC;
+  // Skewed rows (wide FP32 tiles, SPK_X_SKEW): in the epilogue the lanes of a
+  // warp write rows G = 4 apart, so with any row stride that is a multiple of
+  // 16 bytes only 2 of the 8 16-byte bank slots are hit (measured: 73% of the
+  // epilogue's store wavefronts were conflict replays on the C2 level).  Row r
+  // is shifted by ((r / 4) mod 8) 16-byte units: 8 consecutive lanes then hit
+  // 8 distinct slots, for 28 extra floats per row.  Readers of a whole row
+  // (the K loop: broadcast) only add the row's shift.
+  static constexpr int SKEW0 =
+      (SPK_X_SKEW && sizeof(T) == 4 && SM == 0 && NG >= 32 && G == 4 && KT % 32 == 0) ? 16 / (int)sizeof(T) : 0;
+  static constexpr size_t SKEW_BYTES =
+      sizeof(T) * ((size_t)MMAX * (RS0 + 7 * SKEW0) + (size_t)NSTAGE_MIN * KT * MMAX + NB * NARROW_MAX * CP + MMAX) +
+      4096;
+  static constexpr int SKEW = (SKEW0 && SKEW_BYTES <= SMEM_MAX_OPTIN) ? SKEW0 : 0;
+  static constexpr int RS = SKEW ? RS0 + 7 * SKEW
+                                 : (((RS0 * (int)sizeof(T) / 16) % 2 == 1) ? RS0 : RS0 + 16 / (int)sizeof(T));
+  static constexpr int XS = MMAX * RS;                   // elements of X
+  // element offset of X row r
+  SPK_DEV static int xrow(int r) { return r * RS + (SKEW ? ((r >> 2) & 7) * SKEW : 0); }
+  // (K loops address row t*KT + kk as xrow(t*KT) + xrow(kk): needs KT % 32 == 0)
   static constexpr int NBUF = NB * NARROW_MAX * CP;      // narrow-layer staging
   // W ring depth: as many KT x MMAX tiles as fit beside X (small nets keep
   // every tile of the network resident and never re-stream W)
@@ -222,6 +243,7 @@ struct Cfg {
   static constexpr size_t LIVE_BYTES = LIVE ? (size_t)2 * NBG * LW * 4 + (size_t)(NT / 32) * LLIST * 4 : 0;
   static constexpr size_t SMEM = sizeof(T) * (size_t)(XS + NS * TILE + NBUF + MMAX) + 2 * 16 * 8 + 64 + LIVE_BYTES;
   static_assert(NG >= 1 && NG <= NT && NT % NG == 0, "tile shape");
+  static_assert(!SKEW || KT % 32 == 0, "skewed rows need 32-row W tiles");
   static_assert((TB * CP * sizeof(T)) % 16 == 0, "vector loads of X");
   static_assert(TI % G == 0, "W vector groups");
   SPK_DEV static int neuron(int ng, int ti) { return (ti / G) * (NG * G) + ng * G + (ti % G); }
@@ -643,7 +665,7 @@ SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, W
 #pragma unroll
     for (int q = 0; q < TI / CF::G; ++q)
       wd[q] = *reinterpret_cast<const WV*>(Ws + kk * MMAX + q * (CF::NG * CF::G) + ng * CF::G);
-    const float4* xp = reinterpret_cast<const float4*>(Xt + (size_t)kk * CF::RS);
+    const float4* xp = reinterpret_cast<const float4*>(Xt + CF::xrow(kk));
     float4* xd = reinterpret_cast<float4*>(x);
 #pragma unroll
     for (int q = 0; q < (int)(TB * CP * sizeof(T) / 16); ++q) xd[q] = xp[q];
@@ -679,7 +701,7 @@ SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, W
         w[q * CF::G + e + 1] = v.y;
       }
     }
-    const V2* xp = reinterpret_cast<const V2*>(Xt + (size_t)kk * CF::RS);
+    const V2* xp = reinterpret_cast<const V2*>(Xt + CF::xrow(kk));
 #pragma unroll
     for (int q = 0; q < TB * CP / 2; ++q) {
       const V2 v = xp[q];
@@ -695,7 +717,7 @@ SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, W
 
   for (int t = 0; t < L.ntiles; ++t) {
     const T* __restrict__ Ws = ring.acquire();
-    const T* __restrict__ Xt = X + (size_t)(t * KT) * CF::RS + bg * TB * CP;
+    const T* __restrict__ Xt = X + CF::xrow(t * KT) + bg * TB * CP;
     // rows past m_in are zero in X and W: stop at m_in (rounded to the
     // double-buffer pair), e.g. 4 k-steps instead of KT for the 3-input layer
     int k_end = L.m_in - t * KT;
@@ -914,7 +936,7 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
 #pragma unroll
     for (int q = 0; q < TI / CF::G; ++q)
       wd[q] = *reinterpret_cast<const WV*>(Ws + kk * MMAX + q * (CF::NG * CF::G) + ng * CF::G);
-    const ulonglong2* xp = reinterpret_cast<const ulonglong2*>(Xt + (size_t)kk * CF::RS);
+    const ulonglong2* xp = reinterpret_cast<const ulonglong2*>(Xt + CF::xrow(kk));
 #pragma unroll
     for (int q = 0; q < XQ / 2; ++q) {
       const ulonglong2 v = xp[q];
@@ -991,7 +1013,7 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
   auto tiles = [&](auto rec) {
   for (int t = 0; t < L.ntiles; ++t) {
     const float* __restrict__ Ws = ring.acquire();
-    const float* __restrict__ Xt = X + (size_t)(t * KT) * CF::RS + bg * TB * CP;
+    const float* __restrict__ Xt = X + CF::xrow(t * KT) + bg * TB * CP;
     int k_end = L.m_in - t * KT;
     k_end = k_end > KT ? KT : ((k_end + 1) & ~1);
     // live rows of this tile only (bits past m_in are never set); a dense tile
@@ -1232,7 +1254,7 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
 #pragma unroll
         for (int tb = 0; tb < TB; ++tb) out[tb * CP] = T(0);
       }
-      float4* dst = reinterpret_cast<float4*>(X + (size_t)i * CF::RS + bg * TB * CP);
+      float4* dst = reinterpret_cast<float4*>(X + CF::xrow(i) + bg * TB * CP);
       const float4* srcv = reinterpret_cast<const float4*>(out);
 #pragma unroll
       for (int q = 0; q < (int)(TB * CP * sizeof(T) / 16); ++q) dst[q] = srcv[q];
@@ -1287,7 +1309,7 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
       }
     }
     if constexpr (FF) continue;  // nothing goes back to X
-    float4* dst = reinterpret_cast<float4*>(X + (size_t)i * CF::RS + bg * TB * CP);
+    float4* dst = reinterpret_cast<float4*>(X + CF::xrow(i) + bg * TB * CP);
     const float4* srcv = reinterpret_cast<const float4*>(out);
 #pragma unroll
     for (int q = 0; q < (int)(TB * CP * sizeof(T) / 16); ++q) dst[q] = srcv[q];
@@ -1394,7 +1416,7 @@ SPK_DEV void narrow_layer(const LayerDev<T>& L, T* __restrict__ X, T* __restrict
     if (live) {
       for (int k = l; k < L.m_in; k += LP) {
         const T wk = __ldg(wrow + k);
-        const T* xk = X + (size_t)k * CF::RS + b * CP;
+        const T* xk = X + CF::xrow(k) + b * CP;
         if (C == 1) {
           p[0] = Num<T>::fma_rn(wk, xk[0], p[0]);
         } else {
@@ -1437,7 +1459,7 @@ SPK_DEV void narrow_layer(const LayerDev<T>& L, T* __restrict__ X, T* __restrict
 #pragma unroll
       for (int c = 0; c < CP; ++c) out[c] = T(0);
       pack_next<T, C, MODE>(st, gamma_next, out);
-      T* dst = X + (size_t)i * CF::RS + b * CP;
+      T* dst = X + CF::xrow(i) + b * CP;
 #pragma unroll
       for (int c = 0; c < CP; ++c) dst[c] = out[c];
     }
@@ -1447,7 +1469,7 @@ SPK_DEV void narrow_layer(const LayerDev<T>& L, T* __restrict__ X, T* __restrict
     const int r_end = ((L.m_out + KT - 1) / KT) * KT;
     const int w = nbox * CP;
     const int n = (r_end - L.m_out) * w;
-    for (int q = tl; q < n; q += NW * 32) X[(size_t)(L.m_out + q / w) * CF::RS + b0 * CP + q % w] = T(0);
+    for (int q = tl; q < n; q += NW * 32) X[CF::xrow(L.m_out + q / w) + b0 * CP + q % w] = T(0);
   }
   sync();
 }

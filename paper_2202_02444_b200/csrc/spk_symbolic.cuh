@@ -66,7 +66,7 @@ SPK_DEV void sym_activation(int act, int m_out, int& nsym, const SymParams& P, T
 #pragma unroll
   for (int ti = 0; ti < TI; ++ti) {
     const int i = CF::neuron(ng, ti);
-    T* row = X + (size_t)i * CF::RS + bg * CP;
+    T* row = X + CF::xrow(i) + bg * CP;
     if (i >= m_out) {
       continue;
     }
@@ -205,7 +205,7 @@ SPK_DEV void sym_activation(int act, int m_out, int& nsym, const SymParams& P, T
   for (int ti = 0; ti < TI; ++ti) {
     const int i = CF::neuron(ng, ti);
     if (i >= m_out) continue;
-    T* row = X + (size_t)i * CF::RS + bg * CP;
+    T* row = X + CF::xrow(i) + bg * CP;
     const int* kept = KEPT + bg * KC;
     const int* slot_old = SLOTOLD + bg * KC;
     const T g = NEWG[bg * MMAX + i];
@@ -246,7 +246,7 @@ SPK_DEV void sym_layer(const LayerDev<T>& L, int& nsym, const SymParams& P, T* _
 #pragma unroll
   for (int ti = 0; ti < TI; ++ti) {
     const int i = CF::neuron(ng, ti);
-    T* row = X + (size_t)i * CF::RS + bg * CP;
+    T* row = X + CF::xrow(i) + bg * CP;
     const bool valid = i < L.m_out;
     const T be = valid ? L.berr[i] : T(0);
 #pragma unroll
@@ -264,7 +264,7 @@ SPK_DEV void sym_layer(const LayerDev<T>& L, int& nsym, const SymParams& P, T* _
   for (int ti = 0; ti < TI; ++ti) {
     const int i = CF::neuron(ng, ti);
     if (i >= L.m_out) continue;
-    T* row = X + (size_t)i * CF::RS + bg * CP;
+    T* row = X + CF::xrow(i) + bg * CP;
     T rA = T(0);
 #pragma unroll
     for (int j = 0; j < KC; ++j) rA = Num<T>::add_ru(rA, fabs(row[1 + j]));
