@@ -329,7 +329,7 @@ int run_pass(const spk_net* cnet, int mode, int S, int precision, const BoxInput
                         n <= (long long)sm * 8 && in.perm == nullptr;
     // a few hundred boxes on a width-256 net (the top tree levels): the
     // small tile, one neuron per thread, a box pair per CTA, 2 CTAs per SM
-    const bool small = SPK_SMALL_TILE && (mode == MODE_INTERVAL || (mode == MODE_AFFINE && S >= 3)) &&
+    const bool small = SPK_SMALL_TILE && (mode == MODE_INTERVAL || (mode == MODE_AFFINE && S == 3)) &&
                        net->mmax == 256 && n <= (long long)sm * 4 && in.perm == nullptr && !in.spread;
     if (small) {
       BoxInput in2 = in;
@@ -370,7 +370,7 @@ int bound_aabb_internal(const spk_net* net, int policy, int n_keep, int precisio
                         int8_t* cls, cudaStream_t st, int pair_order) {
   int mode;
   if (int rc = check_policy(policy, n_keep, &mode)) return rc;
-  if (net->input_dim > 3) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "AABB path supports d <= 3");
+  if (net->input_dim > MAX_AXES) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "AABB path supports d <= 8");
   if (n_cap <= 0) return n_cap < 0 ? fail(SPK_ERR_DIMENSION, "negative batch") : SPK_OK;
   BoxInput in{IN_AABB, net->input_dim, box_lo, box_hi, 0, 0, 0.0, n_dev};
   // sibling-pair processing order: fused pass only (K3F reads its own inputs)
@@ -514,13 +514,12 @@ int spk_bound_batch(const spk_net* net, int policy, int n_keep, int precision, i
   if (n == 0) return SPK_OK;
   if (mode < 0) return launch_symbolic(net, -mode, n_keep, precision, n, s, centers, axes, lo, hi, cls,
                                        (cudaStream_t)stream);
-  if (s > 3 && mode == MODE_AFFINE) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "more than 3 box axes");
+  if (s > MAX_AXES) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "more than 8 box axes");
   BoxInput in{IN_BOXES, s, centers, axes, 0, 0, 0.0, nullptr};
   BoundOutput o{lo, hi, cls};
   if (mode == MODE_INTERVAL) {
     // interval only needs the hull: pass all s axes through the radius sum
     in.s = s;
-    if (s > 3) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "more than 3 box axes");
   }
   return run_pass(net, mode, s, precision, in, o, n, (cudaStream_t)stream);
 }
@@ -531,7 +530,7 @@ int spk_bound_aabb(const spk_net* net, int policy, int n_keep, int precision, in
   if (!net) return fail(SPK_ERR_INVALID_PARAMETER, "null net");
   int mode;
   if (int rc = check_policy(policy, n_keep, &mode)) return rc;
-  if (net->input_dim > 3) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "AABB path supports d <= 3");
+  if (net->input_dim > MAX_AXES) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "AABB path supports d <= 8");
   if (n <= 0) return n < 0 ? fail(SPK_ERR_DIMENSION, "negative batch") : SPK_OK;
   return bound_aabb_internal(net, policy, n_keep, precision, n, nullptr, box_lo, box_hi, lo, hi, cls,
                              (cudaStream_t)stream);
@@ -544,7 +543,7 @@ int spk_bound_random_cubes(const spk_net* net, int policy, int n_keep, int preci
   int mode;
   if (int rc = check_policy(policy, n_keep, &mode)) return rc;
   if (mode < 0) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "random cubes: interval / affine-fixed only");
-  if (net->input_dim > 3) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "random cubes support d <= 3");
+  if (net->input_dim > MAX_AXES) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "random cubes support d <= 8");
   if (!(half >= 0.0)) return fail(SPK_ERR_INVALID_PARAMETER, "half-extent must be >= 0");
   if (n <= 0) return SPK_OK;
   BoxInput in{IN_RANDOM, net->input_dim, nullptr, nullptr, (long long)first_index, seed, half, nullptr};

@@ -94,29 +94,31 @@ __global__ void __launch_bounds__(NT) full_bound_kernel(const NetDev<T> net, con
     if (tid < d) {
       const int k = tid;
       double centre;
-      double ax[3] = {0.0, 0.0, 0.0};
+      constexpr int CI = MAX_AXES + 2;  // base, up to MAX_AXES axis symbols, error
+      double ax[MAX_AXES];
+      for (int j = 0; j < MAX_AXES; ++j) ax[j] = 0.0;
       int n_ax = 0;
       if (in.kind == IN_BOXES) {
         centre = in.a[box * d + k];
-        n_ax = in.s < 3 ? in.s : 3;
+        n_ax = in.s < MAX_AXES ? in.s : MAX_AXES;
         for (int j = 0; j < n_ax; ++j) ax[j] = in.b[(box * in.s + j) * d + k];
       } else if (in.kind == IN_AABB) {
         const double l = in.a[box * d + k], h = in.b[box * d + k];
         centre = (l + h) / 2.0;
-        n_ax = d < 3 ? d : 3;
+        n_ax = d < MAX_AXES ? d : MAX_AXES;
         ax[k] = (h - l) / 2.0;
       } else {
         centre = random_coord(in.seed, in.first + box, k, d);
-        n_ax = d < 3 ? d : 3;
+        n_ax = d < MAX_AXES ? d : MAX_AXES;
         ax[k] = in.half;
       }
-      State<T, 5, MODE_AFFINE> st;
-      input_state<T, 5, MODE_AFFINE>(centre, ax, n_ax, 1, st);
-      T packed[5];
-      pack_next<T, 5, MODE_AFFINE>(st, net.gamma_first, packed);
+      State<T, CI, MODE_AFFINE> st;
+      input_state<T, CI, MODE_AFFINE>(centre, ax, n_ax, 1, st);
+      T packed[CI];
+      pack_next<T, CI, MODE_AFFINE>(st, net.gamma_first, packed);
       cur[k] = packed[0];
-      for (int j = 0; j < s0; ++j) cur[(size_t)(1 + j) * M + k] = j < 3 ? packed[1 + j] : T(0);
-      V[k] = packed[4];
+      for (int j = 0; j < s0; ++j) cur[(size_t)(1 + j) * M + k] = j < MAX_AXES ? packed[1 + j] : T(0);
+      V[k] = packed[CI - 1];
     }
     __syncthreads();
     int ncol = 1 + s0, m_in = d;
@@ -367,7 +369,7 @@ static int launch_full_t(const spk_net* cnet, const BoxInput& in, const BoundOut
 int launch_full(const spk_net* net, int precision, const BoxInput& in, const BoundOutput& out, long long n, int s0,
                 int need, int n_keep, cudaStream_t st) {
   if (net->mmax > FULL_MMAX) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "affine-full: layer width beyond 512");
-  if (s0 > 3) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "more than 3 box axes");
+  if (s0 > MAX_AXES) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "more than 8 box axes");
   if ((int)net->layers.size() > MAX_LAYERS) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "too many layers");
   DeviceGuard g(net->device);
   return precision == SPK_FP64 ? launch_full_t<double>(net, in, out, n, s0, need, n_keep, st)

@@ -103,28 +103,30 @@ SPK_DEV void prep_inputs(const NetDev<T>& net, const BoxInput& in, long long n, 
     if (k < d && gb >= 0) {
       State<T, C, MODE> st;
       double centre;
-      double ax[3] = {0.0, 0.0, 0.0};
+      double ax[MAX_AXES];
+#pragma unroll
+      for (int j = 0; j < MAX_AXES; ++j) ax[j] = 0.0;
       int n_ax = 0;
       if (in.kind == IN_BOXES || in.kind == IN_POINTS) {
         centre = in.a[gb * d + k];
         if (in.kind == IN_BOXES) {
-          n_ax = in.s < 3 ? in.s : 3;
+          n_ax = in.s < MAX_AXES ? in.s : MAX_AXES;
 #pragma unroll
-          for (int j = 0; j < 3; ++j)
+          for (int j = 0; j < MAX_AXES; ++j)
             if (j < n_ax) ax[j] = in.b[(gb * in.s + j) * d + k];
         }
       } else if (in.kind == IN_AABB) {
         const double l = in.a[gb * d + k], h = in.b[gb * d + k];
         centre = (l + h) / 2.0;  // spatial.py:182-183, exact halving
-        n_ax = d < 3 ? d : 3;
+        n_ax = d < MAX_AXES ? d : MAX_AXES;
 #pragma unroll
-        for (int j = 0; j < 3; ++j)
+        for (int j = 0; j < MAX_AXES; ++j)
           if (j == k) ax[j] = (h - l) / 2.0;
       } else {
         centre = random_coord(in.seed, in.first + gb, k, d);
-        n_ax = d < 3 ? d : 3;
+        n_ax = d < MAX_AXES ? d : MAX_AXES;
 #pragma unroll
-        for (int j = 0; j < 3; ++j)
+        for (int j = 0; j < MAX_AXES; ++j)
           if (j == k) ax[j] = in.half;
       }
       input_state<T, C, MODE>(centre, ax, n_ax, 1, st);
@@ -266,13 +268,13 @@ struct KTOf {
     if constexpr (sizeof(T) == 4 && MMAX == 256) {                                                    \
       if (in.small && mode == MODE_INTERVAL)                                                          \
         return launch_bound<T, 2, MMAX, MODE_INTERVAL, 1>(net, in, out, n, sm, st);                   \
-      if (in.small && mode == MODE_AFFINE && S >= 3)                                                  \
+      if (in.small && mode == MODE_AFFINE && S == 3)                                                  \
         return net.relu_net ? launch_bound<T, 5, MMAX, MODE_AFFINE, 1, 1>(net, in, out, n, sm, st)     \
                             : launch_bound<T, 5, MMAX, MODE_AFFINE, 1>(net, in, out, n, sm, st);       \
     }                                                                                                 \
     /* ReLU-only nets, FP32 affine cubes (the configs): the specialised pass */                       \
     if constexpr (sizeof(T) == 4 && SPK_RELU_SPECIAL)                                                 \
-      if (mode == MODE_AFFINE && S >= 3 && net.relu_net)                                              \
+      if (mode == MODE_AFFINE && S == 3 && net.relu_net)                                              \
         return launch_bound<T, 5, MMAX, MODE_AFFINE, 0, 1>(net, in, out, n, sm, st);                  \
     if (mode == MODE_POINT) return launch_bound<T, 1, MMAX, MODE_POINT>(net, in, out, n, sm, st);      \
     if (mode == MODE_INTERVAL) return launch_bound<T, 2, MMAX, MODE_INTERVAL>(net, in, out, n, sm, st); \
@@ -280,7 +282,8 @@ struct KTOf {
       case 0: return launch_bound<T, 2, MMAX, MODE_AFFINE>(net, in, out, n, sm, st);                  \
       case 1: return launch_bound<T, 3, MMAX, MODE_AFFINE>(net, in, out, n, sm, st);                  \
       case 2: return launch_bound<T, 4, MMAX, MODE_AFFINE>(net, in, out, n, sm, st);                  \
-      default: return launch_bound<T, 5, MMAX, MODE_AFFINE>(net, in, out, n, sm, st);                 \
+      case 3: return launch_bound<T, 5, MMAX, MODE_AFFINE>(net, in, out, n, sm, st);                  \
+      default: return launch_bound<T, MAX_AXES + 2, MMAX, MODE_AFFINE>(net, in, out, n, sm, st);      \
     }                                                                                                 \
   }
 

@@ -27,6 +27,12 @@
 namespace spk {
 
 constexpr int MAX_LAYERS = 24;
+// Box axes of the fused affine pass: s <= 3 run tiles with exactly s symbol
+// columns; 4 <= s <= MAX_AXES run the MAX_AXES-column tile with zero columns
+// for the missing axes (exact zeros: identical bounds).  Higher-dimensional
+// nets (input_dim <= MAX_AXES) thereby get the reference's exact affine
+// forms of their boxes (range_core.py:547-568 is generic in d).
+constexpr int MAX_AXES = 8;
 constexpr int MAX_ACTS = 4;
 constexpr int NT = 256;         // threads per CTA (8 warps)
 constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reduction path

@@ -251,7 +251,7 @@ int spk_certified_radii(const spk_net* net, int policy, int n_keep, int precisio
   if (n < 0) return fail(SPK_ERR_DIMENSION, "negative point count");
   if (n > (int64_t)INT32_MAX) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "too many points in one call");
   const int d = net->input_dim;
-  if (d > 3) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "certified radii support d <= 3");
+  if (d > MAX_AXES) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "certified radii support d <= 8");
   if (!(floor_r > 0.0)) return fail(SPK_ERR_INVALID_PARAMETER, "floor must be positive");
   if (stats) stats[0] = stats[1] = 0;
   if (n == 0) return SPK_OK;
@@ -310,7 +310,7 @@ int spk_intersect(const spk_net* net_a, const spk_net* net_b, int policy, int n_
     return fail(SPK_ERR_INVALID_PARAMETER, "null argument");
   const int d = net_a->input_dim;
   if (net_b->input_dim != d) return fail(SPK_ERR_DIMENSION, "networks of different input dimension");
-  if (d > 3) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "intersection supports d <= 3");
+  if (d > MAX_AXES) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "intersection supports d <= 8");
   if (net_a->device != net_b->device) return fail(SPK_ERR_INVALID_PARAMETER, "networks on different devices");
   if (!(delta > 0.0)) return fail(SPK_ERR_INVALID_PARAMETER, "delta must be positive");
   DeviceGuard g(net_a->device);

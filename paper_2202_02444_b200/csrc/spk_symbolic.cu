@@ -88,7 +88,7 @@ static int run_sym(const spk_net* cnet, int policy, int n_keep, int precision, c
 int launch_symbolic(const spk_net* net, int policy, int n_keep, int precision, long long n, int s,
                     const double* centers, const double* axes, double* lo, double* hi, int8_t* cls,
                     cudaStream_t st) {
-  if (s > 3) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "more than 3 box axes");
+  if (s > MAX_AXES) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "more than 8 box axes");
   BoxInput in{IN_BOXES, s, centers, axes, 0, 0, 0.0, nullptr};
   BoundOutput o{lo, hi, cls};
   return run_sym(net, policy, n_keep, precision, in, o, n, s, st);

@@ -353,7 +353,7 @@ int spk_tree_build_ex(const spk_net* net, int policy, int n_keep, int precision,
   if (!(band >= 0.0)) return fail(SPK_ERR_INVALID_PARAMETER, "band must be >= 0");
   *out = nullptr;
   const int d = net->input_dim;
-  if (d > 3) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "tree build supports d <= 3");
+  if (d > MAX_AXES) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "tree build supports d <= 8");
   if (!(delta > 0.0)) return fail(SPK_ERR_INVALID_PARAMETER, "delta must be positive");
   if (max_depth > 60) return fail(SPK_ERR_DEPTH_OVERFLOW, "fixed depth exceeds 60");
   if (n_roots < 1 || start_depth < 0) return fail(SPK_ERR_INVALID_PARAMETER, "need >= 1 root, start_depth >= 0");
