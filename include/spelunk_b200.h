@@ -179,6 +179,13 @@ int spk_tree_build_band(const spk_net* net, int policy, int n_keep, int precisio
 int spk_tree_build_ex(const spk_net* net, int policy, int n_keep, int precision, int64_t n_roots,
                       const double* root_lo, const double* root_hi, int start_depth, int max_depth,
                       double delta, double band, int flags, void* stream, spk_tree** out);
+/* flags for spk_tree_build_ex: SPK_TREE_HOST_MIRROR (above), and
+ * SPK_TREE_LEVEL_CAP(c), 0 <= c < 255: stop after c levels below the roots --
+ * nodes that would split at the last level stay UNKNOWN internal nodes
+ * (label 0, no face sign), tiny ones still become face-signed leaves.  Used
+ * by the sharded builder to refine in segments and rebalance the open
+ * frontier across GPUs between segments. */
+#define SPK_TREE_LEVEL_CAP(c) (((c) + 1) << 8)
 int spk_tree_destroy(spk_tree* tree);
 int spk_tree_info(const spk_tree* tree, int* n_levels, int64_t* n_nodes, int64_t* bound_evals);
 /* copy one level into caller buffers (host or device, any may be NULL) */

@@ -48,7 +48,7 @@ __global__ void tree_mark_kernel(const long long* __restrict__ n_dev, int d, con
                                  const double* __restrict__ hi, const int8_t* __restrict__ label,
                                  const double* __restrict__ blo, const double* __restrict__ bhi, double band,
                                  int depth, int max_depth, double stop_extent, uint8_t* __restrict__ flag,
-                                 int* __restrict__ block_split, int* __restrict__ block_small) {
+                                 int* __restrict__ block_split, int* __restrict__ block_small, bool capped) {
   const long long n = *n_dev;
   const long long i = (long long)blockIdx.x * TB_THREADS + threadIdx.x;
   uint8_t f = 0;
@@ -61,6 +61,10 @@ __global__ void tree_mark_kernel(const long long* __restrict__ n_dev, int d, con
       for (int k = 0; k < d; ++k) ext = fmax(ext, hi[i * d + k] - lo[i * d + k]);
       f = ext < stop_extent ? 2 : 1;
     }
+    // level cap (segmented builds): nothing splits at the last level; open
+    // nodes stay UNKNOWN internal nodes for the next segment, tiny ones
+    // still become face-signed leaves
+    if (capped && f == 1) f = 0;
   }
   if (i < n) flag[i] = f;
   __shared__ int ws[TB_THREADS / 32], wt[TB_THREADS / 32];
@@ -371,6 +375,8 @@ int spk_tree_build_ex(const spk_net* net, int policy, int n_keep, int precision,
   tree->start_depth = start_depth;
   const double stop = delta / std::sqrt((double)d);
   const bool fixed = max_depth >= 0;
+  // SPK_TREE_LEVEL_CAP(c): at most c levels below the roots (segmented builds)
+  const int level_cap = ((flags >> 8) & 0xff) - 1;
   // Level sizes stay on the device: kernels read their live count from
   // d_cnt[level] and are launched for a capacity bound (2x the previous
   // level).  The host only synchronises in convergence mode (to detect the
@@ -447,11 +453,12 @@ int spk_tree_build_ex(const spk_net* net, int policy, int n_keep, int precision,
     }
     int* bsplit = counts;
     int* bsmall = counts + nb;
+    const bool capped = level_cap >= 0 && lv >= level_cap;
     tree_mark_kernel<<<nb, TB_THREADS, 0, st>>>(n_dev, d, cur.lo, cur.hi, cur.label, cur.blo, cur.bhi, band, depth,
-                                                max_depth, stop, flag, bsplit, bsmall);
+                                                max_depth, stop, flag, bsplit, bsmall, capped);
     tree_sum_kernel<<<1, TB_THREADS, 0, st>>>(nb, bsplit, bsmall, k_dev, m_dev, d_cnt + lv + 1);
     // capacity of the next level
-    const bool last_fixed = fixed && depth >= max_depth;
+    const bool last_fixed = (fixed && depth >= max_depth) || capped;
     long long next_cap = last_fixed ? 0 : 2 * cur_cap;
     long long k_exact = -1;
     if (!fixed || next_cap > kAsyncCap) {

@@ -246,3 +246,125 @@ def merge_mesh_parts_t(parts):
     uk2, _, first2 = first_occurrence(vk)
     vertices = vp[first2][torch.searchsorted(uk2, vertex_keys)]
     return vertices, triangles, vertex_keys
+
+
+# --------------------------------------------------------------------------
+# Frontier rebalancing (segmented refinement below the cut).
+
+def _order_keys(parents, root_keys, j0: int, n_roots: int):
+    """Order keys of a segment's levels 1.. from its roots' keys (level j0 of
+    the tree below the cut): key_j = b_j 2^(j-1) R + key_(j-1)(parent)."""
+    keys = [np.asarray(root_keys, np.int64)]
+    for l in range(1, len(parents)):
+        j = j0 + l
+        if (j - 1) + int(np.ceil(np.log2(max(2, n_roots)))) >= 62:
+            raise OverflowError("tree too deep for 64-bit order keys")
+        par = np.asarray(parents[l], np.int64)
+        bit = np.zeros(len(par), np.int64)
+        bit[len(par) // 2:] = 1
+        keys.append(bit * ((1 << (j - 1)) * int(n_roots)) + keys[-1][par])
+    return keys
+
+
+def allgather_sizes(n: int, device=None):
+    """Every rank's count (one small all_gather)."""
+    import torch
+    import torch.distributed as dist
+
+    if device is None:
+        device = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([int(n)], dtype=torch.int64, device=device)
+    out = [torch.zeros_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    return [int(x.item()) for x in out]
+
+
+def rebalance_frontier(lo, hi, keys, sizes, rank: int, world: int):
+    """Redistribute the open frontier evenly: one all_gather of every rank's
+    (corners, key) rows -- NCCL over NVLink on GPUs -- and each rank keeps its
+    contiguous slice of the concatenation (rank order).  Returns the new
+    (lo, hi, keys)."""
+    import torch
+
+    d = lo.shape[1] if lo.ndim == 2 else 0
+    rows = np.concatenate([lo, hi, keys[:, None].astype(np.float64)], axis=1) if len(keys) else \
+        np.zeros((0, 2 * d + 1))
+    # keys travel as exact integers inside FP64 rows (< 2^53 is checked)
+    if len(keys) and int(keys.max()) >= (1 << 53):
+        raise OverflowError("order key beyond 2^53")
+    import torch.distributed as dist
+
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    allr = np.concatenate(allgather_rows(rows, dev), axis=0)
+    total = allr.shape[0]
+    first, count = shard_range(total, rank, world)
+    mine = allr[first:first + count]
+    return mine[:, :d].copy(), mine[:, d:2 * d].copy(), mine[:, 2 * d].astype(np.int64)
+
+
+def refine_segmented(build_segment, lo, hi, root_keys, n_roots: int, segment_levels: int, stop: float,
+                     cut: int, max_depth, rank: int, world: int, imbalance: float = 1.25):
+    """Refine this rank's frontier below the cut in segments, rebalancing the
+    open frontier between segments when max/mean > imbalance.
+
+    build_segment(lo, hi, j0) -> levels [(lo, hi, bound_lo, bound_hi, label,
+    face, parent)] of a capped build rooted at the given nodes (level 0 = the
+    roots, at depth cut + j0).  Returns ((sizes per level j = 1..J, f rows,
+    i rows [key, label, face]) in the gather's packed layout, record)."""
+    import torch.distributed as dist
+
+    distributed = dist.is_available() and dist.is_initialized() and world > 1
+    lo = np.asarray(lo, np.float64)
+    hi = np.asarray(hi, np.float64)
+    d = lo.shape[1]
+    keys = np.asarray(root_keys, np.int64)
+    per_level = {}
+    record = []
+    j0 = 0
+    while True:
+        sizes = allgather_sizes(len(keys)) if distributed else [len(keys)]
+        total = sum(sizes)
+        if total == 0:
+            break
+        mean = total / len(sizes)
+        moved = False
+        if distributed and max(sizes) > imbalance * mean:
+            lo, hi, keys = rebalance_frontier(lo, hi, keys, sizes, rank, world)
+            moved = True
+        record.append({"level": cut + j0, "sizes": sizes, "rebalanced": moved})
+        if len(keys) == 0:
+            lo, hi, keys = np.zeros((0, d)), np.zeros((0, d)), np.zeros(0, np.int64)
+            j0 += segment_levels
+            continue
+        levels = build_segment(lo, hi, j0)
+        lkeys = _order_keys([l[6] for l in levels], keys, j0, n_roots)
+        for l in range(1, len(levels)):
+            llo, lhi, blo, bhi, lab, face, _ = levels[l]
+            f = np.concatenate([llo, lhi, blo[:, None], bhi[:, None]], axis=1)
+            i = np.stack([lkeys[l], lab.astype(np.int64), face.astype(np.int64)], axis=1)
+            per_level.setdefault(j0 + l, []).append((f, i))
+        # the capped last level: nodes that would split are the next segment's roots
+        if len(levels) == segment_levels + 1:
+            llo, lhi, _, _, lab, _, _ = levels[-1]
+            open_ = lab == 0
+            if max_depth is None:
+                open_ &= (lhi - llo).max(axis=1) >= stop
+            else:
+                open_ &= (cut + j0 + segment_levels) < max_depth
+            lo, hi, keys = llo[open_], lhi[open_], lkeys[-1][open_]
+        else:
+            lo, hi, keys = np.zeros((0, d)), np.zeros((0, d)), np.zeros(0, np.int64)
+        j0 += segment_levels
+    J = max(per_level) if per_level else 0
+    sizes, fs, is_ = [], [], []
+    for j in range(1, J + 1):
+        parts = per_level.get(j, [])
+        f = np.concatenate([p[0] for p in parts], axis=0) if parts else np.zeros((0, 2 * d + 2))
+        i = np.concatenate([p[1] for p in parts], axis=0) if parts else np.zeros((0, 3), np.int64)
+        sizes.append(len(f))
+        fs.append(f)
+        is_.append(i)
+    packed = (np.asarray(sizes, np.int64),
+              np.concatenate(fs, axis=0) if fs else np.zeros((0, 2 * d + 2)),
+              np.concatenate(is_, axis=0) if is_ else np.zeros((0, 3), np.int64))
+    return packed, record

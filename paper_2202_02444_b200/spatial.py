@@ -229,7 +229,7 @@ class _DeviceView:
 
 
 def _build(net, roots_lo, roots_hi, start_depth, delta, policy, max_depth, precision, to_host, device=None,
-           band: float = 0.0):
+           band: float = 0.0, level_cap: int | None = None):
     pcode, n_keep = policy_code(policy)
     dn = device_net(net, device)
     roots_lo = np.ascontiguousarray(roots_lo, dtype=np.float64)
@@ -241,7 +241,8 @@ def _build(net, roots_lo, roots_hi, start_depth, delta, policy, max_depth, preci
     _lib.call(
         "spk_tree_build_ex", dn.ptr, pcode, n_keep, _precision_code(precision), roots_lo.shape[0],
         roots_lo.ctypes.data, roots_hi.ctypes.data, int(start_depth),
-        -1 if max_depth is None else int(max_depth), float(delta), float(band), _HOST_MIRROR if to_host else 0,
+        -1 if max_depth is None else int(max_depth), float(delta), float(band),
+        (_HOST_MIRROR if to_host else 0) | (0 if level_cap is None else (int(level_cap) + 1) << 8),
         stream, C.byref(handle),
     )
     owner = _TreeHandle(handle)
@@ -453,6 +454,55 @@ def build_spatial_tree_sharded(net, bounds: AABB, max_depth: int, policy, rank: 
     return sub
 
 
+def build_spatial_tree_rebalanced(net, bounds: AABB, rank: int, world: int, delta: float = 0.001,
+                                  policy=AFFINE_FULL, max_depth: int | None = None, precision: str = "fp32",
+                                  min_roots_per_rank: int = 64, segment_levels: int = 4, imbalance: float = 1.25,
+                                  device=None) -> TreeArrays:
+    """Sharded build with frontier rebalancing (north-star item: NCCL over
+    NVLink "only for frontier rebalancing and the final gather").  Below the
+    redundant top cut every rank refines its frontier slice in segments of
+    `segment_levels` levels (spk_tree_build_ex with SPK_TREE_LEVEL_CAP); after
+    each segment the ranks all_gather their open-frontier sizes and, when the
+    largest exceeds `imbalance` x the mean, redistribute the open nodes (AABB
+    corners + order key) evenly with one all_gather -- convergence-mode
+    builds refine unevenly over space, so static slices drift apart.  Node
+    bounds are per node, so the tree is the unsharded one node for node;
+    `gather_spatial_tree` reassembles it (order keys travel with the nodes).
+    The result holds this rank's rows below the cut (meta["packed"]) and the
+    rebalancing record (meta["rebalance"])."""
+    from .shard import first_cut, refine_segmented, split_frontier
+
+    _check_domain(net, bounds)
+    cut = first_cut(world, min_roots_per_rank, max_depth if max_depth is not None else 60)
+    while True:
+        top = build_spatial_tree_arrays(net, bounds, delta, policy, cut, precision, to_host=True)
+        n_open = int((_np(top.levels[-1].label) == 0).sum())
+        if (max_depth is not None and cut >= max_depth) or n_open >= min_roots_per_rank * world or n_open == 0:
+            break
+        cut += 1
+    # NOTE: the top levels were built in fixed-depth mode; in convergence mode
+    # a node above the cut can be a tiny leaf, which fixed mode would split.
+    last = top.levels[-1]
+    open_idx = np.flatnonzero(_np(last.label) == 0)
+    mine = split_frontier(np.arange(len(open_idx)), rank, world)
+    lo0, hi0 = _np(last.lo)[open_idx[mine]], _np(last.hi)[open_idx[mine]]
+
+    def segment(lo, hi, j0):
+        sub = _build(net, lo, hi, cut + j0, delta, policy, max_depth, precision, True, device,
+                     level_cap=segment_levels)
+        return [(_np(l.lo), _np(l.hi), _np(l.bound_lo), _np(l.bound_hi), _np(l.label), _np(l.face),
+                 _np(l.parent)) for l in sub.levels]
+
+    d = net.input_dim
+    stop = delta / np.sqrt(float(d))
+    packed, record = refine_segmented(segment, lo0, hi0, np.asarray(mine, np.int64), len(open_idx),
+                                      segment_levels, stop, cut, max_depth, rank, world, imbalance)
+    meta = dict(cut=cut, top=top.levels, open_idx=open_idx, rank=rank, world=world, packed=packed,
+                rebalance=record, top_nodes=top.n_nodes)
+    own = int(packed[0].sum()) if len(packed[0]) else 0
+    return TreeArrays(top.levels, 0, meta=meta, n_nodes=own)
+
+
 def _pack_subtree(arr: TreeArrays):
     """A sharded build's own levels below the cut as (level sizes (J, 1),
     f64 rows [lo, hi, bound_lo, bound_hi], i64 rows [key, label, face])."""
@@ -552,7 +602,12 @@ def gather_spatial_tree(arr: TreeArrays, device=None, to_host: bool = True) -> T
     if device is None:
         lv0 = arr.levels[0].label
         device = lv0.device if dv.is_tensor(lv0) else "cpu"
-    mine = _pack_subtree_t(arr, device)
+    if "packed" in arr.meta:  # rebalanced build: rows computed during the refinement
+        sz, f_rows, i_rows = arr.meta["packed"]
+        mine = tuple(torch.from_numpy(np.ascontiguousarray(x)).to(device)
+                     for x in (np.asarray(sz, np.int64).reshape(-1, 1), f_rows, i_rows))
+    else:
+        mine = _pack_subtree_t(arr, device)
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         packed = list(zip(*[allgather_tensor(x, device) for x in mine]))
     else:

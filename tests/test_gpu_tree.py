@@ -236,3 +236,23 @@ def test_narrow_warp_live_masks_are_exact(net_paths, netname):
                                       torch.from_numpy(c[perm] + h[perm]).cuda(), policy)
         np.testing.assert_array_equal(lo_b.cpu().numpy(), lo_a.cpu().numpy()[perm])
         np.testing.assert_array_equal(hi_b.cpu().numpy(), hi_a.cpu().numpy()[perm])
+
+
+@pytest.mark.parametrize("mode", ["convergence", "fixed"])
+def test_segmented_build_equals_unsharded(net_paths, mode):
+    """The rebalancing builder refines in capped segments (SPK_TREE_LEVEL_CAP)
+    and reassembles by order key: in one process (no rebalancing needed) the
+    gathered tree equals the unsharded build array for array."""
+    net = sp.load_network(net_paths["relu_sdf"])
+    b = spatial.AABB(-np.ones(3), np.ones(3))
+    kw = dict(delta=0.02, max_depth=None) if mode == "convergence" else dict(delta=1.0, max_depth=9)
+    full = spatial.build_spatial_tree_arrays(net, b, policy=sp.AFFINE_FIXED, precision="fp64", to_host=True, **kw)
+    arr = spatial.build_spatial_tree_rebalanced(net, b, 0, 1, policy=sp.AFFINE_FIXED, precision="fp64",
+                                                min_roots_per_rank=16, segment_levels=3, **kw)
+    got = spatial.gather_spatial_tree(arr, device="cpu")
+    assert got.n_levels == full.n_levels
+    for g, f in zip(got.levels, full.levels):
+        for k in ("lo", "hi", "bound_lo", "bound_hi", "label", "face"):
+            np.testing.assert_array_equal(np.asarray(getattr(g, k)), np.asarray(getattr(f, k)))
+        if len(f) and f.parent[0] >= 0:
+            np.testing.assert_array_equal(np.asarray(g.parent), np.asarray(f.parent))

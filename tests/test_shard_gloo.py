@@ -244,3 +244,70 @@ def test_gather_mesh_gloo():
     np.testing.assert_array_equal(t, want_t)
     np.testing.assert_array_equal(k, want_k)
     np.testing.assert_array_equal(v, want_v)
+
+
+# ---------------------------------------------------------------- rebalancing
+def _oracle_segment(net, delta, cut, seg):
+    """Capped segment build with the oracle standing in for the device:
+    the full convergence subtree truncated to seg levels below the roots."""
+    def build(lo, hi, j0):
+        lv = orc.tree_levels(net, lo, hi, "affine-fixed", delta=delta, start_depth=cut + j0)[: seg + 1]
+        return [(l["lo"], l["hi"], *orc.bound_aabbs(net, l["lo"], l["hi"], "affine-fixed"), l["label"], l["face"],
+                 l["parent"]) for l in lv]
+    return build
+
+
+def _rebalance_worker(rank, world, port, delta, seg, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2202_02444_b200.spatial import TreeArrays, TreeLevel, gather_spatial_tree
+
+        net = orc.load_net(NET)
+        cut = 3
+        top = orc.tree_levels(net, -np.ones(3), np.ones(3), "affine-fixed", max_depth=cut)
+        open_idx = np.flatnonzero(top[-1]["label"] == 0)
+        # deliberately unbalanced start: rank 0 takes every root
+        mine = np.arange(len(open_idx)) if rank == 0 else np.zeros(0, np.int64)
+        stop = delta / np.sqrt(3.0)
+        packed, record = shard.refine_segmented(_oracle_segment(net, delta, cut, seg), top[-1]["lo"][open_idx[mine]],
+                                                top[-1]["hi"][open_idx[mine]], mine, len(open_idx), seg, stop, cut,
+                                                None, rank, world, imbalance=1.1)
+
+        def level(l):
+            blo, bhi = orc.bound_aabbs(net, l["lo"], l["hi"], "affine-fixed")
+            return TreeLevel(l["lo"], l["hi"], blo, bhi, l["label"], l["face"], l["parent"])
+
+        arr = TreeArrays([level(l) for l in top], 0,
+                         meta=dict(cut=cut, top=[level(l) for l in top], open_idx=open_idx, packed=packed))
+        tree = gather_spatial_tree(arr, device="cpu")
+        if rank == 0:
+            out_q.put(([(l.lo, l.hi, l.label, l.face, l.parent) for l in tree.levels], record))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_rebalanced_convergence_build_gloo():
+    """Segmented refinement with frontier rebalancing (all_gather of the open
+    nodes when max/mean > 1.1) from a maximally unbalanced start reproduces
+    the unsharded convergence-mode tree node for node."""
+    delta, seg, world = 0.08, 2, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rebalance_worker, args=(r, world, port, delta, seg, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    levels, record = q.get(timeout=900)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert any(r["rebalanced"] for r in record)
+    full = orc.tree_levels(orc.load_net(NET), -np.ones(3), np.ones(3), "affine-fixed", delta=delta)
+    assert len(levels) == len(full)
+    for got, ref in zip(levels, full):
+        for g, k in zip(got, ("lo", "hi", "label", "face", "parent")):
+            if k == "parent" and ref["parent"][0] < 0:
+                continue
+            np.testing.assert_array_equal(g, ref[k])
