@@ -302,6 +302,7 @@ struct Pool {
     for (void* p : owned) cudaFreeAsync(p, st);
     owned.clear();
   }
+  ~Pool() { release(); }  // stream-ordered frees: safe while kernels still read
 };
 
 // exclusive per-CUDA-block offsets of a small count array (host side)
@@ -448,13 +449,17 @@ int spk_mesh_extract_shard(const spk_net* net, int policy, int n_keep, int preci
   const long long cells_per = (long long)S * S * S, pts_per = (long long)P * P * P;
   const long long CH = std::max<long long>(1, std::min<long long>(nb, (16ll << 20) / pts_per));
   for (long long b0 = 0; rc == SPK_OK && b0 < nb; b0 += CH) {
+    // per-chunk scratch (lattice points, values, counts, corner dedup) is
+    // released at the end of the chunk (stream-ordered): memory stays
+    // O(chunk), not O(mesh) -- a 1024^3 extraction has ~100 chunks
+    Pool cp{st};
     const long long cb = std::min(CH, nb - b0);
     const int* corg = org + b0 * 3;
-    double* pts = pool.get<double>(cb * pts_per * 3);
-    double* vals = pool.get<double>(cb * pts_per);
-    int* cnt = pool.get<int>(cb * cells_per);
-    int* off = pool.get<int>(cb * cells_per);
-    if (pool.err != cudaSuccess) { rc = cuda_fail(pool.err, "mesh alloc"); break; }
+    double* pts = cp.get<double>(cb * pts_per * 3);
+    double* vals = cp.get<double>(cb * pts_per);
+    int* cnt = cp.get<int>(cb * cells_per);
+    int* off = cp.get<int>(cb * cells_per);
+    if (cp.err != cudaSuccess) { rc = cuda_fail(cp.err, "mesh alloc"); break; }
     const long long np_ = cb * pts_per, nc = cb * cells_per;
     corner_points_kernel<<<(int)((np_ + MK - 1) / MK), MK, 0, st>>>(cb, corg, S, G, pts);
     long long n_eval = np_;
@@ -464,20 +469,20 @@ int spk_mesh_extract_shard(const spk_net* net, int policy, int n_keep, int preci
       // evaluate, scatter back) -- the values are deterministic per point, so
       // the mesh is unchanged; ~30% fewer evaluations on dense regions
       const int gblk = (int)((np_ + MK - 1) / MK);
-      unsigned long long* ck = pool.get<unsigned long long>(np_);
-      unsigned long long* sk = pool.get<unsigned long long>(np_);
-      long long* ci = pool.get<long long>(np_);
-      long long* si = pool.get<long long>(np_);
-      int* head = pool.get<int>(np_);
-      int* runid = pool.get<int>(np_);
-      if (pool.err != cudaSuccess) { rc = cuda_fail(pool.err, "mesh alloc"); break; }
+      unsigned long long* ck = cp.get<unsigned long long>(np_);
+      unsigned long long* sk = cp.get<unsigned long long>(np_);
+      long long* ci = cp.get<long long>(np_);
+      long long* si = cp.get<long long>(np_);
+      int* head = cp.get<int>(np_);
+      int* runid = cp.get<int>(np_);
+      if (cp.err != cudaSuccess) { rc = cuda_fail(cp.err, "mesh alloc"); break; }
       corner_keys_kernel<<<gblk, MK, 0, st>>>(cb, corg, S, (long long)G.n + 1, ck, ci);
       size_t tb = 0, tb2 = 0;
       const int key_bits = 64 - __builtin_clzll((unsigned long long)((long long)(G.n + 1) * (G.n + 1) * (G.n + 1)));
       cub::DeviceRadixSort::SortPairs(nullptr, tb, ck, sk, ci, si, (int)np_, 0, key_bits, st);
       cub::DeviceScan::InclusiveSum(nullptr, tb2, head, runid, (int)np_, st);
-      void* tmp = pool.get<char>(std::max(tb, tb2));
-      if (pool.err != cudaSuccess) { rc = cuda_fail(pool.err, "mesh alloc"); break; }
+      void* tmp = cp.get<char>(std::max(tb, tb2));
+      if (cp.err != cudaSuccess) { rc = cuda_fail(cp.err, "mesh alloc"); break; }
       cub::DeviceRadixSort::SortPairs(tmp, tb, ck, sk, ci, si, (int)np_, 0, key_bits, st);
       run_head_kernel<<<gblk, MK, 0, st>>>(np_, sk, head);
       cub::DeviceScan::InclusiveSum(tmp, tb2, head, runid, (int)np_, st);
@@ -485,9 +490,9 @@ int spk_mesh_extract_shard(const spk_net* net, int policy, int n_keep, int preci
       cudaMemcpyAsync(&nu, runid + np_ - 1, 4, cudaMemcpyDeviceToHost, st);
       e = cudaStreamSynchronize(st);
       if (e != cudaSuccess) { rc = cuda_fail(e, "mesh corner dedup"); break; }
-      double* upts = pool.get<double>((long long)nu * 3);
-      double* uvals = pool.get<double>(nu);
-      if (pool.err != cudaSuccess) { rc = cuda_fail(pool.err, "mesh alloc"); break; }
+      double* upts = cp.get<double>((long long)nu * 3);
+      double* uvals = cp.get<double>(nu);
+      if (cp.err != cudaSuccess) { rc = cuda_fail(cp.err, "mesh alloc"); break; }
       unique_points_kernel<<<gblk, MK, 0, st>>>(np_, sk, si, runid, pts, upts);
       cudaEventRecord(ev0, st);
       rc = spk_eval_batch(net, precision, nu, upts, uvals, st);
@@ -505,8 +510,8 @@ int spk_mesh_extract_shard(const spk_net* net, int policy, int n_keep, int preci
     cell_count_kernel<<<(int)((nc + MK - 1) / MK), MK, 0, st>>>(cb, S, vals, cnt);
     size_t tmp_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, off, (int)nc, st);
-    void* tmp = pool.get<char>(tmp_bytes);
-    if (pool.err != cudaSuccess) { rc = cuda_fail(pool.err, "mesh alloc"); break; }
+    void* tmp = cp.get<char>(tmp_bytes);
+    if (cp.err != cudaSuccess) { rc = cuda_fail(cp.err, "mesh alloc"); break; }
     cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, off, (int)nc, st);
     int last_cnt = 0, last_off = 0;
     cudaMemcpyAsync(&last_cnt, cnt + nc - 1, 4, cudaMemcpyDeviceToHost, st);
@@ -520,7 +525,7 @@ int spk_mesh_extract_shard(const spk_net* net, int policy, int n_keep, int preci
     unsigned long long* keys = nullptr;
     double* pos = nullptr;
     if (ntri > 0) {
-      keys = pool.get<unsigned long long>(ntri * 3);
+      keys = pool.get<unsigned long long>(ntri * 3);  // kept until the dedup below
       pos = pool.get<double>(ntri * 9);
       if (pool.err != cudaSuccess) { rc = cuda_fail(pool.err, "mesh alloc"); break; }
       cell_emit_kernel<<<(int)((nc + MK - 1) / MK), MK, 0, st>>>(cb, S, corg, vals, off, 0, G, keys, pos);
