@@ -401,6 +401,10 @@ def run_ours(args, rank, world, local_rank):
     _lib.call("spk_ffma_peak", 20000, C.byref(pk), torch.cuda.current_stream().cuda_stream)
     peak_tf = pk.value / 1e12
     achieved_tf = kernel_boxes * flop_box / (kernel_ms / 1e3) / 1e12
+    # nominal FFMA peak at the SM clock sampled during the timed region
+    # (2 FLOP x 128 lanes x SMs x f); MEASURED_PEAKS.json has no FP32 entry
+    sm_mhz = (clock.summary().get("sm_mhz") or 1965.0)
+    nominal_tf = 2 * 128 * torch.cuda.get_device_properties(dev).multi_processor_count * sm_mhz * 1e6 / 1e12
     traffic = load_traffic().get("C2_bound_kernel_bytes_per_launch")
 
     # ---- extra workloads (single GPU, rank 0), each with its own clock record
@@ -452,6 +456,7 @@ def run_ours(args, rank, world, local_rank):
                      "kernel": "spk::bound_kernel<float,5,256,AFFINE> (all tree levels)",
                      "flop_per_box": flop_box,
                      "peak_source": "measured FFMA probe (spk_ffma_peak) on this GPU at run time",
+                     "peak_nominal": nominal_tf, "frac_nominal": achieved_tf / nominal_tf,
                      "flop_counting": "algorithmic (dense) FLOPs; the kernel skips X rows that are exactly zero "
                                       "(ReLU-inactive neurons of both boxes of a sibling pair) with identical "
                                       "results -- it executes ~69% of the dense FMAs on the depth-18 level "
