@@ -47,7 +47,9 @@ _ERR = {1: DimensionMismatch, 2: UnsupportedActivation, 3: InvalidParameter, 4: 
 _PRECISION = {"fp32": 0, "fp64": 1}[os.environ.get("SPELUNK_B200_PRECISION", "fp64")]
 
 _handles: dict[int, tuple] = {}
-_lock = threading.Lock()
+# re-entrant: a weakref.finalize callback (_drop) can run from a garbage
+# collection triggered inside _handle while this thread holds the lock
+_lock = threading.RLock()
 _calls = [0]
 
 
