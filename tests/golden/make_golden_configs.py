@@ -20,6 +20,8 @@ they rebuilt the same net.  Output: tests/golden/configs.npz.
   C4  ELU 3->8x512->1 occupancy net: extract_mesh (meshing.py:111-169), m=4
       and m=5, dense_levels=3, affine-fixed (passed explicitly: the reference
       default affine-full needs 4,099 symbols).
+  C2  the headline net (8x256 ReLU) at depth 12: build_spatial_tree levels
+      (AABBs, labels) and each level's range_bound_batch bounds.
   C5  4096 cubes of half-extent 1/64 with centres from the on-device stream
       (synth.random_cube_centres, seed 5): range_bound_batch
       (range_core.py:547-642) for the 8-layer width-64 and width-512 nets,
@@ -103,6 +105,31 @@ def job_c4(m):
     return ("C4", m, mesh.vertices, mesh.triangles)
 
 
+def job_c2(depth):
+    """The headline config itself at a depth the reference finishes in
+    seconds: build_spatial_tree (spatial.py:214-289), affine-fixed, with each
+    level's node bounds from range_bound_batch (the same boxes the tree
+    bounded)."""
+    import spelunk as ref
+
+    net, _ = ref_net("C2")
+    root = ref.build_spatial_tree(net, ref.AABB(np.full(3, -1.0), np.full(3, 1.0)), policy=ref.AFFINE_FIXED,
+                                  max_depth=depth)
+    levels, frontier = [], [root]
+    while frontier:
+        lo = np.array([n.aabb.lo for n in frontier])
+        hi = np.array([n.aabb.hi for n in frontier])
+        lab = np.array([{"positive": 1, "negative": -1}.get(n.sign.value, 0) for n in frontier], np.int8)
+        axes = np.zeros((len(frontier), 3, 3))
+        axes[:, np.arange(3), np.arange(3)] = (hi - lo) / 2.0
+        blo, bhi = ref.range_bound_batch(net, (lo + hi) / 2.0, axes, ref.AFFINE_FIXED)
+        levels.append((lo, hi, lab, blo, bhi))
+        nxt_lo = [c for n in frontier if n.children for c in n.children[:1]]
+        nxt_hi = [c for n in frontier if n.children for c in n.children[1:]]
+        frontier = nxt_lo + nxt_hi
+    return ("C2", depth, levels)
+
+
 def job_c5(tag, policy):
     import spelunk as ref
 
@@ -119,7 +146,7 @@ def job_c5(tag, policy):
 def main():
     t0 = time.time()
     out = {}
-    for tag in ("C3", "C4", "C5_64", "C5_512"):
+    for tag in ("C2", "C3", "C4", "C5_64", "C5_512"):
         out[f"configs/{tag}/fingerprint"] = ref_net(tag)[1]
     pos, dirs = c3_rays()
     out["configs/C3/position"] = pos
@@ -136,6 +163,7 @@ def main():
         for tag in ("C5_64", "C5_512"):
             for pol in ("affine-fixed", "interval"):
                 jobs.append(pool.submit(job_c5, tag, pol))
+        jobs.append(pool.submit(job_c2, 12))
         c3 = {}
         for f in jobs:
             r = f.result()
@@ -144,6 +172,10 @@ def main():
             elif r[0] == "C4":
                 out[f"configs/C4/m{r[1]}/vertices"] = r[2]
                 out[f"configs/C4/m{r[1]}/triangles"] = r[3]
+            elif r[0] == "C2":
+                for k, (lo, hi, lab, blo, bhi) in enumerate(r[2]):
+                    for name, v in (("lo", lo), ("hi", hi), ("label", lab), ("bound_lo", blo), ("bound_hi", bhi)):
+                        out[f"configs/C2/d{r[1]}/{k}/{name}"] = v
             else:
                 out[f"configs/{r[1]}/{r[2]}/lo"] = r[3]
                 out[f"configs/{r[1]}/{r[2]}/hi"] = r[4]

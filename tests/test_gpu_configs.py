@@ -29,7 +29,7 @@ import numpy as np
 import pytest
 
 import paper_2202_02444_b200 as sp
-from paper_2202_02444_b200 import meshing, synth
+from paper_2202_02444_b200 import meshing, spatial, synth
 from paper_2202_02444_b200.camera import default_camera
 from paper_2202_02444_b200.spatial import AABB
 from tests.mesh_rules import agreeing_triangle_sets
@@ -57,6 +57,35 @@ def config_net(gold, tag):
         np.testing.assert_array_equal(np.array([p.size, p.sum(), (p * p).sum()]), gold[f"{tag}/fingerprint"])
         _NETS[tag] = net
     return _NETS[tag]
+
+
+# ---------------------------------------------------------------- C2
+def test_c2_tree_matches_reference(gold):
+    """The headline config itself (8x256 ReLU, affine-fixed) against the
+    reference's build_spatial_tree at depth 12 (8,191 nodes): FP64 topology,
+    AABBs and labels identical, node bounds within 1e-8 * S (the sound FP64
+    padding); FP32 labels equal wherever both are definite, bounds contain the
+    reference's and stay within the C2 band of tests/test_gpu_fullsize.py."""
+    net = config_net(gold, "C2")
+    b = AABB(-np.ones(3), np.ones(3))
+    for precision in ("fp64", "fp32"):
+        arr = spatial.build_spatial_tree_arrays(net, b, policy=sp.AFFINE_FIXED, max_depth=12, precision=precision,
+                                                to_host=True)
+        assert arr.n_levels == 13
+        for k, lv in enumerate(arr.levels):
+            g = lambda name: gold[f"C2/d12/{k}/{name}"]
+            np.testing.assert_array_equal(lv.lo, g("lo"))
+            np.testing.assert_array_equal(lv.hi, g("hi"))
+            wl, wh = g("bound_lo"), g("bound_hi")
+            S = np.maximum(1.0, np.maximum(np.abs(wl), np.abs(wh)))
+            assert np.all(lv.bound_lo <= wl + 1e-12 * S) and np.all(lv.bound_hi >= wh - 1e-12 * S)
+            if precision == "fp64":
+                np.testing.assert_array_equal(lv.label, g("label"))
+                assert np.max(np.abs(lv.bound_lo - wl) / S) <= 1e-8
+            else:
+                both = (lv.label != 0) & (g("label") != 0)
+                np.testing.assert_array_equal(lv.label[both], g("label")[both])
+                assert np.max(np.abs(lv.bound_lo - wl) / (S + wh - wl)) <= 0.06
 
 
 # ---------------------------------------------------------------- C3
