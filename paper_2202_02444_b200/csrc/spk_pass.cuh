@@ -96,6 +96,9 @@ constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reducti
 #ifndef SPK_ONE_BLOCK
 #define SPK_ONE_BLOCK 1  // FP32 nets of width <= SPK_SUB_F32: accumulate onto the bias, no partials
 #endif
+#ifndef SPK_ONE_BLOCK_W64
+#define SPK_ONE_BLOCK_W64 0  // width-64 FP32 nets: one summation block per layer + running-error layer (measured: C5_64 +7.5% time for only 1.3x tighter -- off)
+#endif
 #ifndef SPK_NARROW_TI4
 #define SPK_NARROW_TI4 0  // FP32 width-32 affine tile: 4 neurons/thread, 3 CTAs/SM (Cfg::TI4; measured: 80-register cap spills, C1 0.307 -> 0.451 ms)
 #endif
@@ -195,7 +198,10 @@ struct Cfg {
   static constexpr int KT_RAW = 32768 / (MMAX * (int)sizeof(T));
   static constexpr int KT = (sizeof(T) == 4 && MMAX == 64) ? SPK_KT_F32_W64
                                                             : (KT_RAW > MMAX ? MMAX : (KT_RAW < 1 ? 1 : KT_RAW));
-  static constexpr int SUB = sizeof(T) == 4 ? SPK_SUB_F32 : 1 << 20;  // blocked-sum length (FP32)
+  // blocked-sum length (FP32); width-64 nets sum each layer as one block
+  // (the single-block loop: no partial registers, which lets the narrow
+  // 128-register tile carry the running-error layer)
+  static constexpr int SUB = sizeof(T) == 4 ? ((MMAX == 64 && SPK_ONE_BLOCK_W64) ? 64 : SPK_SUB_F32) : 1 << 20;
   static constexpr int TILE = KT * MMAX;                 // elements per W tile
   // X row stride (elements): 16-byte aligned rows, and an odd number of
   // 16-byte units per row so the epilogue's vector stores spread over banks
@@ -900,7 +906,7 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
   // every layer is a single block, so the products accumulate straight onto
   // the bias -- an (m_in + 1)-term chain inside the same gamma_{m_in + 2}
   // budget -- with no partial registers, zeroing or flushes
-  constexpr bool ONEBLK = SPK_ONE_BLOCK && MMAX <= CF::SUB && !RUN;
+  constexpr bool ONEBLK = SPK_ONE_BLOCK && MMAX <= CF::SUB;
   int since = 0;
   // partial sums -> running sums (a fresh block re-initialises the partials)
   auto flush = [&](auto rec) {
@@ -971,7 +977,7 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
             // all-zero rows the live-row masks skip -- results stay identical
             // for any batch composition
             float b_, a_, x0_, x1_;
-            f2_split(partp[ti][g][0], b_, a_);
+            f2_split(ONEBLK ? accp[ti][g][0] : partp[ti][g][0], b_, a_);
             f2_split(xv, x0_, x1_);
             erun[ti][g] = __fmaf_ru(fabsf(b_), x0_ != 0.f ? 1.f : 0.f, erun[ti][g]);
           }
@@ -1226,7 +1232,7 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
   // (the small tile, SM = 1, runs the same bound as the big tiles of its
   // width, so every processing order of a batch stays bit-identical)
   constexpr bool RE = SPK_RUNERR && SPK_PACKED_F32 && sizeof(T) == 4 && MODE == MODE_AFFINE && C >= 3 &&
-                      (CF::MINB == 1 || SM == 1);
+                      (CF::MINB == 1 || SM == 1 || (MMAX == 64 && MMAX <= CF::SUB));
   const T gamma_base = RE ? L.gamma_base_next : T(-1);
   dense_kloop<T, C, MMAX, (MODE >= MODE_MI ? 1 : -1), CF::TEAMSYNC, SM, RE>(L, X, ring, tid, acc, m_cur);
 
