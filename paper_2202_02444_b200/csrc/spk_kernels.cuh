@@ -142,9 +142,10 @@ SPK_DEV void prep_inputs(const NetDev<T>& net, const BoxInput& in, long long n, 
         packed[C - 1] = st.e;
       }
     }
-    T* dst = X + CF::xrow(k) + b * CP;
+    T* dst = X + CF::xrow(k) + (b / CF::TB) * CF::GS;
 #pragma unroll
-    for (int c = 0; c < CP; ++c) dst[c] = packed[c];
+    for (int c = 0; c < CP; ++c)
+      if (!CF::IL || c < C) dst[CF::xcol(b % CF::TB, c)] = packed[c];
   }
 }
 

@@ -87,6 +87,9 @@ constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reducti
 #ifndef SPK_TEAM_MIN_NS
 #define SPK_TEAM_MIN_NS 4  // ring depth from which layer boundaries are team-local
 #endif
+#ifndef SPK_IL_X
+#define SPK_IL_X 0  // interleaved box-group columns on the wide FP32 affine tile (Cfg::IL; measured C2 +12% with the 4th ring stage and team-local syncs, +5.7% without: off)
+#endif
 #ifndef SPK_X_SKEW
 #define SPK_X_SKEW 0  // skewed X rows on wide FP32 tiles (conflict-free epilogue stores; measured C2 +0.8%: off)
 #endif
@@ -118,6 +121,7 @@ constexpr int kScalarUnroll = SPK_SCALAR_UNROLL;  // FP64 K loop unroll (A/B kno
 constexpr int NSTAGE_MIN = 3;   // W tile ring depth floor (deeper when tiles are small)
 constexpr size_t SMEM_BUDGET = 210 * 1024;  // leaves room for the symbolic kernel's extras
 constexpr size_t SMEM_MAX_OPTIN = 227 * 1024;  // sm_100 opt-in limit of dynamic shared memory per CTA
+constexpr size_t SMEM_BUDGET_IL = 225 * 1024;  // interleaved bound tiles (no symbolic extras)
 
 enum Mode : int {
   MODE_POINT = 0,
@@ -203,9 +207,20 @@ struct Cfg {
   // 128-register tile carry the running-error layer)
   static constexpr int SUB = sizeof(T) == 4 ? ((MMAX == 64 && SPK_ONE_BLOCK_W64) ? 64 : SPK_SUB_F32) : 1 << 20;
   static constexpr int TILE = KT * MMAX;                 // elements per W tile
+  // Interleaved box-group columns (SPK_IL_X; FP32 affine cubes on the wide
+  // two-box tile): a box group's 10 values per X row are [b0.base b0.A1 b0.A2
+  // b0.A3 | b1.base b1.A1 b1.A2 b1.A3 | b0.err b1.err] -- the K loop's f32x2
+  // pairs stay 8-byte aligned without the per-box pad column (CP = 6), so X
+  // shrinks by 1/6 and the W ring gains a stage (3 -> 4 at width 256, which
+  // also enables the team-local layer boundaries); 5 LDS.64 / STS.64 per
+  // row segment instead of 3 LDS.128 / STS.128.
+  static constexpr bool IL = SPK_IL_X && sizeof(T) == 4 && C == 5 && TB == 2 && SM == 0;
+  static constexpr int GS = IL ? 10 : TB * CP;           // elements of a box group's row segment
+  // offset of column c of the group's box tb within its row segment
+  SPK_DEV static constexpr int xcol(int tb, int c) { return IL ? (c < 4 ? tb * 4 + c : 8 + tb) : tb * CP + c; }
   // X row stride (elements): 16-byte aligned rows, and an odd number of
   // 16-byte units per row so the epilogue's vector stores spread over banks
-  static constexpr int RS0 = ((NB * CP * (int)sizeof(T) + 15) / 16) * 16 / (int)sizeof(T);
+  static constexpr int RS0 = ((NBG * GS * (int)sizeof(T) + 15) / 16) * 16 / (int)sizeof(T);
   // a thread's TI neurons: TI/G groups of G consecutive neurons (G elements
   // = one vector load); group q of neuron-group ng starts at q*NG*G + ng*G,
   // so a warp's vector loads of a W row are contiguous (bank-conflict free)
@@ -232,8 +247,14 @@ struct Cfg {
   static constexpr int NBUF = NB * NARROW_MAX * CP;      // narrow-layer staging
   // W ring depth: as many KT x MMAX tiles as fit beside X (small nets keep
   // every tile of the network resident and never re-stream W)
+  // (the interleaved tiles are never used by the symbolic kernel, whose
+  // extras the 210 KB budget leaves room for; upper bound of the live-row
+  // mask area, exact size LIVE_BYTES below)
+  static constexpr long long LIVE_BYTES_EST = 2ll * NBG * (MMAX / 32 > 0 ? MMAX / 32 : 1) * 4 + (NT / 32) * 40 * 4;
   static constexpr long long NS_FIT =
-      ((long long)SMEM_BUDGET / MINB - (long long)sizeof(T) * (XS + NBUF) - 1024) / ((long long)sizeof(T) * TILE);
+      ((long long)(IL ? SMEM_BUDGET_IL : SMEM_BUDGET) / MINB - (long long)sizeof(T) * (XS + NBUF) - 1024 -
+       (long long)LIVE_BYTES_EST) /
+      ((long long)sizeof(T) * TILE);
   static constexpr int NS = NS_FIT < NSTAGE_MIN ? NSTAGE_MIN : (NS_FIT > 16 ? 16 : (int)NS_FIT);
   // + one W row of slack: the K loops prefetch the fragment two rows ahead
   // unconditionally (a predicated prefetch made ptxas copy fragments), so the
@@ -729,7 +750,7 @@ SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, W
 
   for (int t = 0; t < L.ntiles; ++t) {
     const T* __restrict__ Ws = ring.acquire();
-    const T* __restrict__ Xt = X + CF::xrow(t * KT) + bg * TB * CP;
+    const T* __restrict__ Xt = X + CF::xrow(t * KT) + bg * CF::GS;
     // rows past m_in are zero in X and W: stop at m_in (rounded to the
     // double-buffer pair), e.g. 4 k-steps instead of KT for the 3-input layer
     int k_end = L.m_in - t * KT;
@@ -855,7 +876,10 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
   constexpr int NP = POINT ? TB / 2 : NRN / 2;     // packed pairs (per box; boxes for POINT)
   constexpr int NBOX = POINT ? 1 : TB;             // pair groups
   constexpr bool ODD = !POINT && (NRN % 2 == 1);
-  constexpr int XQ = TB * CP / 2;                  // x fragment as f32x2 words
+  constexpr int XQ = CF::GS / 2;                   // x fragment as f32x2 words
+  // f32x2 word and lane of column c of the group's box tb (Cfg::xcol)
+  constexpr auto xword = [](int tb, int c) { return CF::xcol(tb, c) / 2; };
+  constexpr auto xlane = [](int tb, int c) { return CF::xcol(tb, c) % 2; };
   static_assert(POINT ? (TB % 2 == 0) : (CP % 2 == 0), "pair alignment");
   constexpr bool RUN = RE && !POINT && NP >= 1 && BIAS2 < 0;
   static_assert(RE == RUN, "running error bound: affine columns (base in pair 0) only");
@@ -948,12 +972,18 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
 #pragma unroll
     for (int q = 0; q < TI / CF::G; ++q)
       wd[q] = *reinterpret_cast<const WV*>(Ws + kk * MMAX + q * (CF::NG * CF::G) + ng * CF::G);
-    const ulonglong2* xp = reinterpret_cast<const ulonglong2*>(Xt + CF::xrow(kk));
+    if constexpr (CF::IL) {  // 40-byte segments: 8-byte aligned words
+      const unsigned long long* x8 = reinterpret_cast<const unsigned long long*>(Xt + CF::xrow(kk));
 #pragma unroll
-    for (int q = 0; q < XQ / 2; ++q) {
-      const ulonglong2 v = xp[q];
-      xq[2 * q] = v.x;
-      xq[2 * q + 1] = v.y;
+      for (int q = 0; q < XQ; ++q) xq[q] = x8[q];
+    } else {
+      const ulonglong2* xp = reinterpret_cast<const ulonglong2*>(Xt + CF::xrow(kk));
+#pragma unroll
+      for (int q = 0; q < XQ / 2; ++q) {
+        const ulonglong2 v = xp[q];
+        xq[2 * q] = v.x;
+        xq[2 * q + 1] = v.y;
+      }
     }
   };
   // one k-step; FIRST: the first step of a fresh block writes the partials
@@ -967,7 +997,7 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
       for (int g = 0; g < NBOX; ++g)
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-          const f32x2 xv = xq[POINT ? p : (g * CP) / 2 + p];
+          const f32x2 xv = xq[POINT ? p : xword(g, 2 * p)];
           f32x2& dst = ONEBLK ? accp[ti][g][p] : partp[ti][g][p];
           dst = (FIRST && !ONEBLK) ? f2_mul(w[ti], xv) : f2_fma(w[ti], xv, dst);
           if (REC && p == 0) {
@@ -986,8 +1016,8 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
 #pragma unroll
         for (int tb = 0; tb < TB; ++tb) {
           float lo, hi;
-          f2_split(xq[(tb * CP + C - 1) / 2], lo, hi);
-          const float xe = ((C - 1) % 2 == 0) ? lo : hi;
+          f2_split(xq[xword(tb, C - 1)], lo, hi);
+          const float xe = xlane(tb, C - 1) == 0 ? lo : hi;
           if (!PE) {
             acce[ti][tb] = __fmaf_ru(fabsf(w[ti]), xe, acce[ti][tb]);
           } else if (ti % 2 == 1) {
@@ -995,9 +1025,10 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
           }
           if (ODD) {
             float ol, oh;
-            f2_split(xq[(tb * CP + 2 * NP) / 2], ol, oh);
+            f2_split(xq[xword(tb, 2 * NP)], ol, oh);
+            const float xo = xlane(tb, 2 * NP) == 0 ? ol : oh;
             float& dso = ONEBLK ? acco[ti][tb] : parto[ti][tb];
-            dso = (FIRST && !ONEBLK) ? __fmul_rn(w[ti], ol) : __fmaf_rn(w[ti], ol, dso);
+            dso = (FIRST && !ONEBLK) ? __fmul_rn(w[ti], xo) : __fmaf_rn(w[ti], xo, dso);
           }
         }
       }
@@ -1025,7 +1056,7 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
   auto tiles = [&](auto rec) {
   for (int t = 0; t < L.ntiles; ++t) {
     const float* __restrict__ Ws = ring.acquire();
-    const float* __restrict__ Xt = X + CF::xrow(t * KT) + bg * TB * CP;
+    const float* __restrict__ Xt = X + CF::xrow(t * KT) + bg * CF::GS;
     int k_end = L.m_in - t * KT;
     k_end = k_end > KT ? KT : ((k_end + 1) & ~1);
     // live rows of this tile only (bits past m_in are never set); a dense tile
@@ -1321,10 +1352,20 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
       }
     }
     if constexpr (FF) continue;  // nothing goes back to X
-    float4* dst = reinterpret_cast<float4*>(X + CF::xrow(i) + bg * TB * CP);
-    const float4* srcv = reinterpret_cast<const float4*>(out);
+    if constexpr (CF::IL) {
+      // interleaved segment: 5 pairs (Cfg::xcol)
+      float2* d2 = reinterpret_cast<float2*>(X + CF::xrow(i) + bg * CF::GS);
+      d2[0] = make_float2(out[0], out[1]);
+      d2[1] = make_float2(out[2], out[3]);
+      d2[2] = make_float2(out[CP + 0], out[CP + 1]);
+      d2[3] = make_float2(out[CP + 2], out[CP + 3]);
+      d2[4] = make_float2(out[4], out[CP + 4]);
+    } else {
+      float4* dst = reinterpret_cast<float4*>(X + CF::xrow(i) + bg * TB * CP);
+      const float4* srcv = reinterpret_cast<const float4*>(out);
 #pragma unroll
-    for (int q = 0; q < (int)(TB * CP * sizeof(T) / 16); ++q) dst[q] = srcv[q];
+      for (int q = 0; q < (int)(TB * CP * sizeof(T) / 16); ++q) dst[q] = srcv[q];
+    }
     if (LV) {
       const bool nz = nz_rule && !ring.group_empty;
       live_bits |= (nz ? 1u : 0u) << (ti % CF::G);
@@ -1428,13 +1469,14 @@ SPK_DEV void narrow_layer(const LayerDev<T>& L, T* __restrict__ X, T* __restrict
     if (live) {
       for (int k = l; k < L.m_in; k += LP) {
         const T wk = __ldg(wrow + k);
-        const T* xk = X + CF::xrow(k) + b * CP;
+        const T* xk = X + CF::xrow(k) + (b / CF::TB) * CF::GS;
+        const int bt = b % CF::TB;
         if (C == 1) {
-          p[0] = Num<T>::fma_rn(wk, xk[0], p[0]);
+          p[0] = Num<T>::fma_rn(wk, xk[CF::xcol(bt, 0)], p[0]);
         } else {
 #pragma unroll
-          for (int c = 0; c < C - 1; ++c) p[c] = Num<T>::fma_rn(wk, xk[c], p[c]);
-          p[C - 1] = Num<T>::fma_ru(fabs(wk), xk[C - 1], p[C - 1]);
+          for (int c = 0; c < C - 1; ++c) p[c] = Num<T>::fma_rn(wk, xk[CF::xcol(bt, c)], p[c]);
+          p[C - 1] = Num<T>::fma_ru(fabs(wk), xk[CF::xcol(bt, C - 1)], p[C - 1]);
         }
       }
     }
@@ -1471,17 +1513,18 @@ SPK_DEV void narrow_layer(const LayerDev<T>& L, T* __restrict__ X, T* __restrict
 #pragma unroll
       for (int c = 0; c < CP; ++c) out[c] = T(0);
       pack_next<T, C, MODE>(st, gamma_next, out);
-      T* dst = X + CF::xrow(i) + b * CP;
+      T* dst = X + CF::xrow(i) + (b / CF::TB) * CF::GS;
 #pragma unroll
-      for (int c = 0; c < CP; ++c) dst[c] = out[c];
+      for (int c = 0; c < CP; ++c)
+        if (!CF::IL || c < C) dst[CF::xcol(b % CF::TB, c)] = out[c];
     }
   }
   if (!last) {
     // zero the rows a following generic layer reads beyond m_out (own columns)
     const int r_end = ((L.m_out + KT - 1) / KT) * KT;
-    const int w = nbox * CP;
+    const int w = (nbox / CF::TB) * CF::GS;  // the team's boxes are whole groups
     const int n = (r_end - L.m_out) * w;
-    for (int q = tl; q < n; q += NW * 32) X[CF::xrow(L.m_out + q / w) + b0 * CP + q % w] = T(0);
+    for (int q = tl; q < n; q += NW * 32) X[CF::xrow(L.m_out + q / w) + (b0 / CF::TB) * CF::GS + q % w] = T(0);
   }
   sync();
 }
