@@ -87,6 +87,12 @@ constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reducti
 #ifndef SPK_TEAM_MIN_NS
 #define SPK_TEAM_MIN_NS 4  // ring depth from which layer boundaries are team-local
 #endif
+#ifndef SPK_LIVE_F64
+#define SPK_LIVE_F64 1  // live-row masks on the FP64 wide tiles (scalar K loop)
+#endif
+#ifndef SPK_LIVE_DENSE_F64
+#define SPK_LIVE_DENSE_F64 12  // FP64 tiles (KT rows) with more live rows than this x KT/16 run dense
+#endif
 #ifndef SPK_IL_X
 #define SPK_IL_X 0  // interleaved box-group columns on the wide FP32 affine tile (Cfg::IL; measured C2 +12% with the 4th ring stage and team-local syncs, +5.7% without: off)
 #endif
@@ -269,8 +275,14 @@ struct Cfg {
   // Narrow nets (NG < 32: a warp holds 32/NG box groups) use one mask per
   // warp -- the union over its box groups, so a skipped row is zero for every
   // box the warp computes (needs a G-neuron group's mask word fixed by ti).
-  static constexpr bool LIVE = SPK_LIVE_ROWS && sizeof(T) == 4 && KT == 32 && C >= 2 &&
-                               (NG >= 32 || (SPK_LIVE_WARP && C >= 3 && 32 % (NG * G) == 0));
+  // FP64 wide tiles (SPK_LIVE_F64): the 16-row W tiles (width 256) use their
+  // half of the 32-row mask word, same exactness argument (C2 FP64 build
+  // 105.3 -> 96.7 ms); the 8-row tiles of width 512 lost 4% to the list
+  // overhead (C5_512 FP64 1289 -> 1339 ms) and stay dense.
+  static constexpr bool LIVE =
+      SPK_LIVE_ROWS && C >= 2 &&
+      ((sizeof(T) == 4 && KT == 32 && (NG >= 32 || (SPK_LIVE_WARP && C >= 3 && 32 % (NG * G) == 0))) ||
+       (sizeof(T) == 8 && SPK_LIVE_F64 && SM == 0 && NG >= 32 && KT >= 16 && KT <= 32 && 32 % KT == 0));
   static constexpr int LW = MMAX / 32;  // mask words per box group
   static constexpr int LLIST = 40;  // per-warp live-row list (<= 32 rows + 2 pad entries)
   static constexpr size_t LIVE_BYTES = LIVE ? (size_t)2 * NBG * LW * 4 + (size_t)(NT / 32) * LLIST * 4 : 0;
@@ -642,7 +654,8 @@ SPK_DEV State<T, C, MODE> state_from(const T* col, T be) {
 // gamma_{SUB + ceil(m_in/SUB) + 1} instead of gamma_{m_in + 1}.
 template <typename T, int C, int MMAX, int BIAS2 = -1, bool TEAMS = false, int SM = 0>
 SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, WRing<T, C, MMAX, SM>& ring, int tid,
-                                T (&acc)[Cfg<T, C, MMAX, SM>::TI][Cfg<T, C, MMAX, SM>::TB][C]) {
+                                T (&acc)[Cfg<T, C, MMAX, SM>::TI][Cfg<T, C, MMAX, SM>::TB][C],
+                                const uint32_t* live = nullptr) {
   using CF = Cfg<T, C, MMAX, SM>;
   constexpr int TI = CF::TI, TB = CF::TB, CP = CF::CP, KT = CF::KT;
   const int ng = tid % CF::NG, bg = tid / CF::NG;
@@ -755,6 +768,40 @@ SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, W
     // double-buffer pair), e.g. 4 k-steps instead of KT for the 3-input layer
     int k_end = L.m_in - t * KT;
     k_end = k_end > KT ? KT : ((k_end + 1) & ~1);
+    if constexpr (CF::LIVE && DIRECT) {
+      // live-row masks (FP64): rows that are exactly zero for the whole box
+      // group are skipped -- an FMA with an exact zero leaves the in-place
+      // accumulators unchanged -- so sparse tiles run a row list
+      if (live != nullptr) {
+        const uint32_t word = live[(t * KT) >> 5];
+        uint32_t m = KT >= 32 ? word : ((word >> ((t * KT) & 31)) & ((1u << (KT & 31)) - 1u));
+        if (__popc(m) <= SPK_LIVE_DENSE_F64 * KT / 16) {
+          if (m != 0u) {
+            if (__popc(m) & 1) m |= ~m & (m + 1u);  // pad to pairs with an exactly-zero row (< KT)
+            const int cnt = __popc(m), lane = tid & 31;
+            int* lst = reinterpret_cast<int*>(ring.live + 2 * CF::NBG * CF::LW) + (tid >> 5) * CF::LLIST;
+            __syncwarp();
+            if ((m >> lane) & 1u) lst[__popc(m & ((1u << lane) - 1u))] = lane;
+            if (lane < 2) lst[cnt + lane] = 0;  // prefetch past the last pair reads row 0 (unused)
+            __syncwarp();
+            T w0[TI], x0[TB * CP], w1[TI], x1[TB * CP];
+            int2 kk = *reinterpret_cast<const int2*>(lst);
+            load_frag_e(Ws, Xt, kk.x, w0, x0);
+#pragma unroll 1
+            for (int p = 0; p < cnt; p += 2) {
+              load_frag_e(Ws, Xt, kk.y, w1, x1);
+              const int2 nx = *reinterpret_cast<const int2*>(lst + p + 2);
+              fma_step(w0, x0);
+              load_frag_e(Ws, Xt, nx.x, w0, x0);
+              fma_step(w1, x1);
+              kk = nx;
+            }
+          }
+          ring.release(tid);
+          continue;
+        }
+      }
+    }
     if (UNROLLED && k_end == KT) {
 #pragma unroll 1
       for (int k0 = 0; k0 < KT; k0 += CH) {
@@ -1179,7 +1226,7 @@ SPK_DEV void dense_kloop(const LayerDev<T>& L, const T* __restrict__ X, WRing<T,
   if constexpr (sizeof(T) == 4 && SPK_PACKED_F32) {
     dense_kloop_f32<C, MMAX, BIAS2, TEAMS, SM, RE>(L, X, ring, tid, acc, live);
   } else {
-    dense_kloop_scalar<T, C, MMAX, BIAS2, TEAMS, SM>(L, X, ring, tid, acc);
+    dense_kloop_scalar<T, C, MMAX, BIAS2, TEAMS, SM>(L, X, ring, tid, acc, live);
   }
 }
 
