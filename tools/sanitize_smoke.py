@@ -1,6 +1,9 @@
 """Small run of every kernel family, for compute-sanitizer (one tool per run):
 fused bound (interval / fixed / truncate / full, FP32 + FP64), point eval, tree
-build (fixed + convergence), fused and unfused march, marching cubes."""
+build (fixed + convergence), fused and unfused march, marching cubes; round 2
+adds the width-256/512 instantiations (fused ReLU, running-error layer, FP64
+live-row masks, small-batch tile), large-capacity truncate (top-k), 5-axis
+boxes and a mesh shard."""
 import sys
 
 import numpy as np
@@ -27,4 +30,19 @@ cam = sp.Camera(np.array([1.6, 1.2, 2.0]), np.zeros(3), np.array([0.0, 1.0, 0.0]
 sp.cast_camera(net, cam, sp.RayCastParams(t_max=3.0), "affine-fixed", precision="fp32")
 sp.cast_camera(net, cam, sp.RayCastParams(t_max=3.0), "affine-truncate:8", precision="fp32")
 meshing.extract_mesh_arrays(net, b, 4, 3, "affine-fixed")
+# round 2 paths
+w256 = synth.random_mlp(256, 3, "relu", "torch-uniform", seed=2)
+w512 = synth.random_mlp(512, 2, "relu", "torch-uniform", seed=3)
+c3, a3 = c[:300], a[:300]
+for prec in ("fp32", "fp64"):
+    sp.range_bound_batch(w256, c3, a3, "affine-fixed", precision=prec)
+    sp.range_bound_batch(w512, c3[:100], a3[:100], "affine-fixed", precision=prec)
+sp.range_bound_batch(w256, c3[:64], a3[:64], "affine-truncate:32", precision="fp64")
+spatial.build_spatial_tree_arrays(w256, b, policy="affine-fixed", max_depth=4)
+hd = synth.random_mlp(32, 2, "relu", "ref-normal", seed=1, input_dim=5)
+c5 = rng.uniform(-1, 1, (200, 5))
+a5 = np.zeros((200, 5, 5))
+a5[:, np.arange(5), np.arange(5)] = 0.05
+sp.range_bound_batch(hd, c5, a5, "affine-fixed", precision="fp32")
+meshing.extract_mesh_sharded(net, b, 4, 1, 2, 3, "affine-fixed", precision="fp32")
 print("sanitize smoke done")
