@@ -391,6 +391,12 @@ def run_ours(args, rank, world, local_rank):
             sharded["C3_siren_rays_interval_256sq_fp64"] = bench_c3_sharded(torch, sp, synth, 256, rank, world,
                                                                             coll_dev, barrier)
 
+    # ---- e2e at N>1: the multi-GPU public API (sharded build + final gather
+    # to host arrays on every rank), max over ranks; rank 0 reports it
+    e2e_sharded = None
+    if world > 1:
+        e2e_sharded = bench_e2e_tree_sharded(torch, sp, spatial, net, bounds, args, rank, world, coll_dev, barrier)
+
     if rank != 0:
         return None
 
@@ -432,7 +438,7 @@ def run_ours(args, rank, world, local_rank):
         extra["F1_frustum_relu_sdf_1024sq"] = clocked(bench_frustum, torch, sp, 1024)
 
     # ---- e2e through the public API (host arrays out)
-    e2e = bench_e2e_tree(torch, sp, spatial, net, bounds, args)
+    e2e = e2e_sharded if e2e_sharded is not None else bench_e2e_tree(torch, sp, spatial, net, bounds, args)
 
     # ---- CPU baseline: oracle port on the host cores, bounded sample
     cpu = None
@@ -743,6 +749,37 @@ def bench_e2e_tree(torch, sp, spatial, net, bounds, args):
     return {"value": n / dt, "unit": UNIT, "h2d_bytes_per_step": 48, "d2h_bytes_per_step": int(d2h),
             "api": "build_spatial_tree_arrays(net, AABB([-1]*3,[1]*3), policy=AFFINE_FIXED, max_depth=18, "
                    "to_host=True)", "ms": dt * 1e3}
+
+
+def bench_e2e_tree_sharded(torch, sp, spatial, net, bounds, args, rank, world, coll_dev, barrier):
+    """N GPUs through the public API: build_spatial_tree_sharded on every rank,
+    then gather_spatial_tree(to_host=True) -- every rank ends with the whole
+    unsharded tree as host arrays.  Wall time between barriers, max over ranks."""
+    from paper_2202_02444_b200.shard import reduce_time_units
+
+    def run():
+        part = spatial.build_spatial_tree_sharded(net, bounds, DEPTH, sp.AFFINE_FIXED, rank, world,
+                                                  precision="fp32", to_host=False)
+        return spatial.gather_spatial_tree(part, device=coll_dev, to_host=True)
+
+    tree = run()
+    ts = []
+    for _ in range(max(1, min(args.steps, 3))):
+        del tree
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        tree = run()
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+        barrier()
+    dt, _ = reduce_time_units(float(np.median(ts)), 0.0, device=coll_dev)
+    n = tree.n_nodes
+    d2h = sum(l.lo.nbytes + l.hi.nbytes + l.bound_lo.nbytes + l.bound_hi.nbytes + l.label.nbytes +
+              l.face.nbytes + l.parent.nbytes for l in tree.levels)
+    return {"value": n / dt, "unit": UNIT, "h2d_bytes_per_step": 48, "d2h_bytes_per_step": int(d2h),
+            "api": f"build_spatial_tree_sharded(rank, world={world}) + gather_spatial_tree(to_host=True) on "
+                   "every rank", "ms": dt * 1e3}
 
 
 def cpu_baseline(sp):
