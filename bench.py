@@ -64,22 +64,33 @@ def reference_kind():
     return "reference" if (REF_PKG / "spelunk" / "range_core.py").exists() else "port"
 
 
+def _ref_path():
+    if str(REF_PKG) not in sys.path:
+        sys.path.insert(0, str(REF_PKG))
+
+
+def _ref_net(net_doc):
+    """The reference's own NetworkSpec (baseline/_ref) for a network document."""
+    _ref_path()
+    from spelunk.network import ActivationKind, DenseLayer, NetworkSpec
+
+    layers = []
+    for L in net_doc["layers"]:
+        if L["type"] == "dense":
+            layers.append(DenseLayer(np.asarray(L["weights"], np.float64), np.asarray(L["bias"], np.float64)))
+        else:
+            layers.append(ActivationKind(L["type"] if L["type"] != "activation" else L["kind"]))
+    return NetworkSpec(int(net_doc["input_dim"]), tuple(layers), net_doc.get("output_semantics", "sdf"),
+                       net_doc.get("name", "net"))
+
+
 def _ref_bounder(net_doc, kind):
     """range_bound_batch(centres, axes) of the reference (or the port)."""
     if kind == "reference":
-        if str(REF_PKG) not in sys.path:
-            sys.path.insert(0, str(REF_PKG))
+        _ref_path()
         import spelunk
-        from spelunk.network import ActivationKind, DenseLayer, NetworkSpec
 
-        layers = []
-        for L in net_doc["layers"]:
-            if L["type"] == "dense":
-                layers.append(DenseLayer(np.asarray(L["weights"], np.float64), np.asarray(L["bias"], np.float64)))
-            else:
-                layers.append(ActivationKind(L["type"] if L["type"] != "activation" else L["kind"]))
-        net = NetworkSpec(int(net_doc["input_dim"]), tuple(layers), net_doc.get("output_semantics", "sdf"),
-                          net_doc.get("name", "net"))
+        net = _ref_net(net_doc)
         return lambda c, a: spelunk.range_bound_batch(net, c, a, spelunk.AFFINE_FIXED)
     from oracle import spelunk_oracle as orc
 
@@ -109,6 +120,35 @@ def _cpu_worker(args):
     return len(centers) * reps, dt
 
 
+def _cpu_ray_worker(args):
+    """One single-BLAS-thread process marching its rays with the reference's
+    _march_arrays (rays.py:88-138; cast_rays' own kernel)."""
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    net_doc, origins, dirs, kind, policy = args
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(1):
+        if kind == "reference":
+            _ref_path()
+            from spelunk.range_core import parse_policy
+            from spelunk.rays import RayCastParams, _march_arrays
+
+            net = _ref_net(net_doc)
+            pol = parse_policy(policy)
+            run = lambda o, d: _march_arrays(net, o, d, RayCastParams(), pol)
+        else:
+            from oracle import spelunk_oracle as orc
+
+            onet = orc.net_from_json_doc(net_doc)
+            run = lambda o, d: orc.march(onet, o, d, orc.MarchParams(), policy)
+        run(origins[:1], dirs[:1])  # warm
+        t0 = time.perf_counter()
+        hit, t, steps = run(origins, dirs)[:3]
+        dt = time.perf_counter() - t0
+    return len(origins), int(np.sum(steps)), dt
+
+
 class CpuPool:
     def __init__(self, procs, kind):
         import multiprocessing as mp
@@ -130,6 +170,14 @@ class CpuPool:
         boxes = sum(r[0] for r in res)
         busy = max(r[1] for r in res)
         return boxes, busy, wall
+
+    def run_rays(self, net_doc, origins, dirs, policy):
+        parts = [(net_doc, o, d, self.kind, policy) for o, d in zip(np.array_split(origins, self.procs),
+                                                          np.array_split(dirs, self.procs)) if len(o)]
+        t0 = time.perf_counter()
+        res = self.pool.map(_cpu_ray_worker, parts)
+        wall = time.perf_counter() - t0
+        return sum(r[0] for r in res), sum(r[1] for r in res), wall
 
     def close(self):
         self.pool.close()
@@ -444,6 +492,7 @@ def run_ours(args, rank, world, local_rank):
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         cpu = cpu_baseline(sp)
+        extra["cpu_reference"] = cpu_reference_extras(extra)
 
     ck = clock.summary()
     return {
@@ -780,6 +829,59 @@ def bench_e2e_tree_sharded(torch, sp, spatial, net, bounds, args, rank, world, c
     return {"value": n / dt, "unit": UNIT, "h2d_bytes_per_step": 48, "d2h_bytes_per_step": int(d2h),
             "api": f"build_spatial_tree_sharded(rank, world={world}) + gather_spatial_tree(to_host=True) on "
                    "every rank", "ms": dt * 1e3}
+
+
+def cpu_reference_extras(extra):
+    """The reference on the host cores for the other two CPU-comparable
+    metrics (SURVEY.md §8(d) "CPU reference timing"): C1 in full (4x32,
+    64^3 grid, affine-fixed) and C3 rays on a bounded sample (16x16 centre
+    crop of the 256^2 default camera, interval, FP64), each beside the GPU
+    number of the same workload in `extra`."""
+    from paper_2202_02444_b200 import network, synth
+
+    model, cores = cpu_info()
+    kind = reference_kind()
+    pool = CpuPool(cores, kind)
+    out = {"kind": kind, "cores": cores, "cpu": model}
+    # C1: the whole grid, 4096-box chunks per process
+    doc = network.network_to_doc(synth.config_net("C1"))
+    centers, axes = synth.grid_cubes(64)
+    per_proc = -(-len(centers) // cores)
+    pool.run(doc, centers[: cores * 64], axes[: cores * 64], 64)  # spawn + import warm-up
+    boxes, busy, wall = pool.run(doc, centers, axes, per_proc)
+    gpu = extra.get("C1_4x32_64cubed", {}).get("boxes_per_s")
+    out["C1_4x32_64cubed"] = {"boxes": boxes, "boxes_per_s": boxes / wall, "wall_s": wall,
+                              "gpu_over_cpu": (gpu / (boxes / wall)) if gpu else None}
+    # C3: reference camera rays (camera.py pixel_dirs) through _march_arrays
+    res, crop = 256, 16
+    pos, look, up = np.array([1.6, 1.2, 2.0]), np.zeros(3), np.array([0.0, 1.0, 0.0])
+    if kind == "reference":
+        _ref_path()
+        from spelunk.camera import Camera
+
+        all_dirs = Camera(pos, look, up, 40.0, (res, res)).pixel_dirs()
+    else:
+        from oracle import spelunk_oracle as orc
+
+        all_dirs = orc.pixel_dirs(pos, look, up, 40.0, res, res)
+    doc3 = network.network_to_doc(synth.config_net("C3"))
+    for policy, crop, gkey in (("interval", 16, "C3_siren_rays_interval_256sq_fp64"),
+                               ("affine-truncate:16", 4, "C3_siren_rays_truncate16_128sq_fp64")):
+        r0 = (res - crop) // 2
+        dirs = np.ascontiguousarray(np.asarray(all_dirs)[r0:r0 + crop, r0:r0 + crop].reshape(-1, 3))
+        origins = np.tile(pos, (len(dirs), 1))
+        rays, ray_steps, wall = pool.run_rays(doc3, origins, dirs, policy)
+        g = extra.get(gkey, {})
+        gpu_steps = (g["ray_steps"] / (g["ms"] / 1e3)) if g else None
+        out["C3_siren_rays_" + policy.replace("affine-", "").replace(":", "") + "_fp64"] = {
+            "rays": rays, "ray_steps": ray_steps, "steps_per_ray": ray_steps / rays, "rays_per_s": rays / wall,
+            "ray_steps_per_s": ray_steps / wall, "wall_s": wall,
+            "sample": f"{crop}x{crop} centre crop of the {res}^2 default camera, {cores} procs, reference "
+                      f"rays._march_arrays (the kernel of cast_rays), {policy}",
+            "gpu_rays_per_s": g.get("rays_per_s"), "gpu_ray_steps_per_s": gpu_steps,
+            "gpu_over_cpu_ray_steps": (gpu_steps / (ray_steps / wall)) if gpu_steps else None}
+    pool.close()
+    return out
 
 
 def cpu_baseline(sp):
