@@ -256,3 +256,36 @@ def test_segmented_build_equals_unsharded(net_paths, mode):
             np.testing.assert_array_equal(np.asarray(getattr(g, k)), np.asarray(getattr(f, k)))
         if len(f) and f.parent[0] >= 0:
             np.testing.assert_array_equal(np.asarray(g.parent), np.asarray(f.parent))
+
+
+def test_fp64_live_masks_are_exact():
+    """FP64 width-256 tiles skip X rows that are zero for both boxes of a box
+    group (16-row W tiles, round 2).  Coherent sibling-like batches (many rows
+    skipped) and the same boxes permuted (dense tiles) must give bit-identical
+    FP64 bounds, and those match the oracle."""
+    import torch
+
+    from oracle import spelunk_oracle as orc
+    from paper_2202_02444_b200 import synth
+
+    net = synth.random_mlp(256, 4, "relu", "torch-uniform", seed=5)
+    rng = np.random.default_rng(12)
+    n = 20_000
+    c = rng.uniform(-1, 1, (n, 3))
+    c = c[np.lexsort((c[:, 0], c[:, 1], np.round(c[:, 2] * 8)))]
+    h = np.full((n, 1), 1.0 / 128)
+    perm = rng.permutation(n)
+    for policy in ("affine-fixed", "interval"):
+        lo_a, hi_a, _ = sp.bound_aabb(net, torch.from_numpy(c - h).cuda(), torch.from_numpy(c + h).cuda(), policy,
+                                      precision="fp64")
+        lo_b, hi_b, _ = sp.bound_aabb(net, torch.from_numpy(c[perm] - h[perm]).cuda(),
+                                      torch.from_numpy(c[perm] + h[perm]).cuda(), policy, precision="fp64")
+        lo_a, hi_a = lo_a.cpu().numpy(), hi_a.cpu().numpy()
+        np.testing.assert_array_equal(lo_b.cpu().numpy(), lo_a[perm])
+        np.testing.assert_array_equal(hi_b.cpu().numpy(), hi_a[perm])
+        sel = rng.choice(n, 256, replace=False)
+        axes = np.zeros((256, 3, 3))
+        axes[:, np.arange(3), np.arange(3)] = 1.0 / 128
+        wl, wh = orc.bound_batch(orc.as_oracle_net(net), c[sel], axes, policy)
+        s = np.maximum(1.0, np.maximum(np.abs(wl), np.abs(wh)))
+        assert np.all(np.abs(lo_a[sel] - wl) <= 1e-10 * s) and np.all(np.abs(hi_a[sel] - wh) <= 1e-10 * s)
