@@ -35,6 +35,7 @@ baseline/_ref is absent it falls back to the pinned NumPy oracle port
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -325,16 +326,23 @@ def timed(fn, torch, flush, barrier):
     of microseconds on the device) without a host sync in between, so the
     host prepares fn's first launch while the flush runs: the event pair
     measures fn's device time, not the Python launch latency of its first
-    kernel (the e2e number measures the API end to end)."""
+    kernel (the e2e number measures the API end to end).  Python's cyclic
+    garbage collector runs before the step, not inside it (a collection pass
+    mid-build stalls the launching thread while the GPU drains)."""
+    gc.collect()
     barrier()
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    flush()
-    e0.record()
-    out = fn()
-    e1.record()
-    torch.cuda.synchronize()
+    gc.disable()
+    try:
+        flush()
+        e0.record()
+        out = fn()
+        e1.record()
+        torch.cuda.synchronize()
+    finally:
+        gc.enable()
     barrier()
     return e0.elapsed_time(e1) / 1e3, out
 
