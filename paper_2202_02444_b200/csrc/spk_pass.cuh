@@ -87,6 +87,12 @@ constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reducti
 #ifndef SPK_TEAM_MIN_NS
 #define SPK_TEAM_MIN_NS 4  // ring depth from which layer boundaries are team-local
 #endif
+#ifndef SPK_DEFER_RELEASE
+#define SPK_DEFER_RELEASE 1  // WRing::DEFER: examine the release atomic one tile later
+#endif
+#ifndef SPK_DEFER_MIN_NS
+#define SPK_DEFER_MIN_NS 4  // ... on rings of at least this many stages
+#endif
 #ifndef SPK_LIVE_F64
 #define SPK_LIVE_F64 1  // live-row masks on the FP64 wide tiles (scalar K loop)
 #endif
@@ -422,12 +428,42 @@ struct WRing {
     mbar_wait(&full[st], resident() ? 0u : ph);  // resident stages complete once and stay complete
     return stages + (size_t)st * CF::TILE;
   }
+  // Deferred release decision (SPK_DEFER_RELEASE, rings of >= 4 stages):
+  // lane 0 examines its atomic's result at the warp's next release (or at
+  // settle(), after the layer's last tile), so the shared-memory atomic's
+  // round trip overlaps a tile of FMAs instead of stalling the warp.  The
+  // refill goes out one tile later, which the deep ring absorbs; the stage's
+  // counter is reset before its refill is issued, and no warp can release the
+  // stage again before that refill lands, so the count stays exact.
+  // measured: C5 width 64 -2%; width-512 point pass +1%, and on the 3-stage
+  // rings (C2, C5 width 512) +6%: on for narrow nets only
+  static constexpr bool DEFER = SPK_DEFER_RELEASE && CF::NS >= SPK_DEFER_MIN_NS && MMAX <= 64;
+  unsigned pend_old = 0u;
+  int pend_st = -1;
+  long long pend_next = 0;
+  SPK_DEV void settle() {
+    if (DEFER && pend_st >= 0) {
+      if (pend_old == NT / 32 - 1) {
+        released[pend_st] = 0u;
+        if (pend_next + CF::NS < total) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(pend_next + CF::NS);
+        }
+      }
+      pend_st = -1;
+    }
+  }
   // the calling warp is done reading the current stage
   SPK_DEV void release(int tid) {
     if (!resident()) {
       __syncwarp();
       if ((tid & 31) == 0) {
-        if (atomicAdd(&released[st], 1u) == NT / 32 - 1) {
+        if constexpr (DEFER) {
+          settle();
+          pend_old = atomicAdd(&released[st], 1u);
+          pend_st = st;
+          pend_next = next;
+        } else if (atomicAdd(&released[st], 1u) == NT / 32 - 1) {
           released[st] = 0u;
           if (next + CF::NS < total) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -838,6 +874,7 @@ SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, W
     }
     ring.release(tid);  // this warp is done with the stage
   }
+  ring.settle();
   if (since > 0) flush();
   if (DIRECT) {
     T bias_r[TI];
@@ -1180,6 +1217,7 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
     }
     ring.release(tid);
   }
+  ring.settle();
   if (since > 0) flush(rec);
   };
   if (RUN && re_layer) {
