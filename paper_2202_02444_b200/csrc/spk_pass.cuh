@@ -87,6 +87,9 @@ constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reducti
 #ifndef SPK_TEAM_MIN_NS
 #define SPK_TEAM_MIN_NS 4  // ring depth from which layer boundaries are team-local
 #endif
+#ifndef SPK_KT_POINT512
+#define SPK_KT_POINT512 1  // Cfg::PT32: 32-row W tiles for FP32 width-512 point passes (C4 evaluation -10.7%)
+#endif
 #ifndef SPK_DEFER_RELEASE
 #define SPK_DEFER_RELEASE 1  // WRing::DEFER: examine the release atomic one tile later
 #endif
@@ -212,8 +215,13 @@ struct Cfg {
   static constexpr int NBG = NT / NG;
   static constexpr int NB = NBG * TB;
   static constexpr int KT_RAW = 32768 / (MMAX * (int)sizeof(T));
+  // FP32 width-512 point passes (X is one column: 72 KB): 32-row W tiles in
+  // a 2-stage ring instead of 16-row tiles in 5 -- half the per-tile ring
+  // traffic (mbarrier waits and release atomics were ~20% of the stall
+  // samples); same blocked-sum order, bit-identical values
+  static constexpr bool PT32 = SPK_KT_POINT512 && sizeof(T) == 4 && MMAX == 512 && C == 1 && SM == 0;
   static constexpr int KT = (sizeof(T) == 4 && MMAX == 64) ? SPK_KT_F32_W64
-                                                            : (KT_RAW > MMAX ? MMAX : (KT_RAW < 1 ? 1 : KT_RAW));
+                            : (PT32 ? 32 : (KT_RAW > MMAX ? MMAX : (KT_RAW < 1 ? 1 : KT_RAW)));
   // blocked-sum length (FP32); width-64 nets sum each layer as one block
   // (the single-block loop: no partial registers, which lets the narrow
   // 128-register tile carry the running-error layer)
@@ -267,7 +275,8 @@ struct Cfg {
       ((long long)(IL ? SMEM_BUDGET_IL : SMEM_BUDGET) / MINB - (long long)sizeof(T) * (XS + NBUF) - 1024 -
        (long long)LIVE_BYTES_EST) /
       ((long long)sizeof(T) * TILE);
-  static constexpr int NS = NS_FIT < NSTAGE_MIN ? NSTAGE_MIN : (NS_FIT > 16 ? 16 : (int)NS_FIT);
+  static constexpr int NS_MIN = PT32 ? 2 : NSTAGE_MIN;
+  static constexpr int NS = NS_FIT < NS_MIN ? NS_MIN : (NS_FIT > 16 ? 16 : (int)NS_FIT);
   // + one W row of slack: the K loops prefetch the fragment two rows ahead
   // unconditionally (a predicated prefetch made ptxas copy fragments), so the
   // last step may read one row past the last ring stage (values unused)
