@@ -75,6 +75,22 @@ static int kt_for(int mmax) {
 }
 
 template <typename T>
+static int pad_for(int mmax) {
+  switch (mmax) {
+    case 32: return KTOf<T, 32>::PAD;
+    case 64: return KTOf<T, 64>::PAD;
+    case 128: return KTOf<T, 128>::PAD;
+    case 256: return KTOf<T, 256>::PAD;
+    default: return KTOf<T, 512>::PAD;
+  }
+}
+
+// W tiles of a dense layer in host (KT-row) units: the layer's rows padded to
+// a multiple of PAD, the largest tile any kernel of this width reads
+// (Cfg::KT_PAD), so kernels with PAD-row tiles see whole pairs of host tiles.
+static int layer_tiles(int m_in, int kt, int pad) { return ((m_in + pad - 1) / pad) * (pad / kt); }
+
+template <typename T>
 static int sub_for(int mmax) {
   switch (mmax) {
     case 32: return KTOf<T, 32>::SUB;
@@ -128,6 +144,7 @@ int build_device_net(spk_net* net, DevNet<T>& dn) {
   const bool fp32 = sizeof(T) == 4;
   const int mmax = net->mmax;
   const int KT = kt_for<T>(mmax);
+  const int PADR = pad_for<T>(mmax);
   const int tile = KT * mmax;
   NetDev<T> nd;
   std::memset(&nd, 0, sizeof(nd));
@@ -161,7 +178,7 @@ int build_device_net(spk_net* net, DevNet<T>& dn) {
         n_eff = std::max(n_eff, 8 + lg + 1);
       }
     } else {
-      const int nt = (L.m_in + KT - 1) / KT;
+      const int nt = layer_tiles(L.m_in, KT, PADR);
       const int sub = sub_for<T>(mmax);
       n_eff = std::min(sub, L.m_in) + (L.m_in + sub - 1) / sub + 1;
       for (int t = 0; t < nt; ++t) {
@@ -243,7 +260,7 @@ int build_device_net(spk_net* net, DevNet<T>& dn) {
     D.m_in = L.m_in;
     D.m_out = L.m_out;
     D.narrow = (l + 1 == net->layers.size()) && L.m_out <= NARROW_MAX;
-    D.ntiles = D.narrow ? 0 : (L.m_in + KT - 1) / KT;
+    D.ntiles = D.narrow ? 0 : layer_tiles(L.m_in, KT, PADR);
     D.n_act = (int)L.acts.size();
     for (int a = 0; a < D.n_act; ++a) D.act[a] = act_code(net, L.acts[a]);
     D.w = D.narrow ? d_small + offs[l].w : nullptr;

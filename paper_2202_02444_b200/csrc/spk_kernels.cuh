@@ -212,7 +212,8 @@ __global__ void __launch_bounds__(NT, (Cfg<T, C, MMAX, SM>::MINB))
     mbar_fence_init();
   }
   __syncthreads();
-  WRing<T, C, MMAX, SM> ring{Wst, full, released, net.wtiles, net.tiles_per_pass, mine * net.tiles_per_pass, 0};
+  const int per_pass = net.tiles_per_pass / CF::TSCALE;
+  WRing<T, C, MMAX, SM> ring{Wst, full, released, net.wtiles, per_pass, mine * per_pass, 0};
   if (CF::LIVE) ring.live = reinterpret_cast<uint32_t*>(released + 16);
   ring.prologue(tid);
 
@@ -258,7 +259,8 @@ cudaError_t dispatch_bound(int mode, int S, const NetDev<T>& net, const BoxInput
 
 template <typename T, int MMAX>
 struct KTOf {
-  static constexpr int KT = Cfg<T, 1, MMAX>::KT;
+  static constexpr int KT = Cfg<T, 1, MMAX>::KT_BASE;   // host tile rows
+  static constexpr int PAD = Cfg<T, 1, MMAX>::KT_PAD;   // layers padded to a multiple of this
   static constexpr int SUB = Cfg<T, 1, MMAX>::SUB;
 };
 

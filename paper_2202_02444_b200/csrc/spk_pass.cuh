@@ -219,9 +219,18 @@ struct Cfg {
   // a 2-stage ring instead of 16-row tiles in 5 -- half the per-tile ring
   // traffic (mbarrier waits and release atomics were ~20% of the stall
   // samples); same blocked-sum order, bit-identical values
+  //
+  // The host lays W out once per network in KT_BASE-row tiles with every
+  // layer padded to a multiple of KT_PAD rows (the largest KT of any kernel
+  // of this width), so a kernel with KT = TSCALE * KT_BASE reads the same
+  // array as whole pairs of tiles: its tile counts are the host's / TSCALE.
   static constexpr bool PT32 = SPK_KT_POINT512 && sizeof(T) == 4 && MMAX == 512 && C == 1 && SM == 0;
-  static constexpr int KT = (sizeof(T) == 4 && MMAX == 64) ? SPK_KT_F32_W64
-                            : (PT32 ? 32 : (KT_RAW > MMAX ? MMAX : (KT_RAW < 1 ? 1 : KT_RAW)));
+  static constexpr int KT_BASE = (sizeof(T) == 4 && MMAX == 64) ? SPK_KT_F32_W64
+                                 : (KT_RAW > MMAX ? MMAX : (KT_RAW < 1 ? 1 : KT_RAW));
+  static constexpr int KT_PAD = (SPK_KT_POINT512 && sizeof(T) == 4 && MMAX == 512 && SM == 0) ? 32 : KT_BASE;
+  static constexpr int KT = PT32 ? 32 : KT_BASE;
+  static constexpr int TSCALE = KT / KT_BASE;
+  static_assert(KT % KT_BASE == 0 && KT_PAD % KT == 0, "host tile layout");
   // blocked-sum length (FP32); width-64 nets sum each layer as one block
   // (the single-block loop: no partial registers, which lets the narrow
   // 128-register tile carry the running-error layer)
@@ -806,7 +815,7 @@ SPK_DEV void dense_kloop_scalar(const LayerDev<T>& L, const T* __restrict__ X, W
   constexpr bool UNROLLED = SPK_UNROLL_BLOCK && DIRECT && (KT % CH) == 0 && (CF::G % 2) == 0 &&
                             ((TB * CP) % 2) == 0;
 
-  for (int t = 0; t < L.ntiles; ++t) {
+  for (int t = 0; t < L.ntiles / CF::TSCALE; ++t) {
     const T* __restrict__ Ws = ring.acquire();
     const T* __restrict__ Xt = X + CF::xrow(t * KT) + bg * CF::GS;
     // rows past m_in are zero in X and W: stop at m_in (rounded to the
@@ -1147,7 +1156,7 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
   };
 
   auto tiles = [&](auto rec) {
-  for (int t = 0; t < L.ntiles; ++t) {
+  for (int t = 0; t < L.ntiles / CF::TSCALE; ++t) {
     const float* __restrict__ Ws = ring.acquire();
     const float* __restrict__ Xt = X + CF::xrow(t * KT) + bg * CF::GS;
     int k_end = L.m_in - t * KT;

@@ -305,7 +305,8 @@ __global__ void __launch_bounds__(NT, 1)
     mbar_fence_init();
   }
   __syncthreads();
-  WRing<T, C, MMAX> ring{Wst, full, released, net.wtiles, net.tiles_per_pass, mine * net.tiles_per_pass, 0};
+  const int per_pass = net.tiles_per_pass / Cfg<T, C, MMAX>::TSCALE;
+  WRing<T, C, MMAX> ring{Wst, full, released, net.wtiles, per_pass, mine * per_pass, 0};
   ring.prologue(tid);
 
   for (long long tile = blockIdx.x; tile < nbt; tile += gridDim.x) {
