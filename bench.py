@@ -484,6 +484,12 @@ def run_ours(args, rank, world, local_rank):
     extra["C5_8x256_16M"] = clocked(bench_c5, torch, sp, synth, "C5_256", 16 << 20, flush, peak_tf)
     extra["C5_8x64_16M"] = clocked(bench_c5, torch, sp, synth, "C5_64", 16 << 20, flush, peak_tf)
     extra["C5_8x512_4M"] = clocked(bench_c5, torch, sp, synth, "C5_512", 4 << 20, flush, peak_tf)
+    # FP32 bounds + FP64 re-bound of near-certifiable UNKNOWN boxes: the
+    # reference's labels (tests/test_gpu_refine.py) at close to FP32 cost
+    extra["C2_tree_fp32_refine"] = clocked(bench_c2_fp64, torch, sp, spatial, net, bounds, flush, "fp32-refine")
+    extra["C5_8x64_16M_fp32_refine"] = clocked(bench_c5, torch, sp, synth, "C5_64", 16 << 20, flush, peak_tf,
+                                               "fp32-refine")
+    extra["C5_8x64_16M_fp64"] = clocked(bench_c5, torch, sp, synth, "C5_64", 16 << 20, flush, peak_tf, "fp64")
     extra["C1_4x32_64cubed"] = clocked(bench_c1, torch, sp, synth, flush, peak_tf)
     extra["host_range_bound_batch_4096"] = clocked(bench_host_calls, sp, synth)
     if not args.no_mesh:
@@ -534,11 +540,13 @@ def run_ours(args, rank, world, local_rank):
     }
 
 
-def bench_c2_fp64(torch, sp, spatial, net, bounds, flush):
+def bench_c2_fp64(torch, sp, spatial, net, bounds, flush, precision="fp64"):
     """The headline build with the FP64 kernels -- the reference's arithmetic
-    (sound-padded FP64; topology identical to the reference's tree)."""
+    (sound-padded FP64; topology identical to the reference's tree) -- or
+    with precision="fp32-refine" (FP32, near-certifiable UNKNOWN nodes
+    re-bounded in FP64)."""
     run = lambda: spatial.build_spatial_tree_arrays(net, bounds, policy=sp.AFFINE_FIXED, max_depth=DEPTH,
-                                                    precision="fp64", to_host=False)
+                                                    precision=precision, to_host=False)
     run()
     ts = []
     for _ in range(2):
@@ -546,7 +554,7 @@ def bench_c2_fp64(torch, sp, spatial, net, bounds, flush):
         ts.append(dt)
     dt = float(np.median(ts))
     return {"nodes": arr.n_nodes, "boxes_per_s": arr.n_nodes / dt, "ms": dt * 1e3,
-            "bound_kernel_ms": arr.bound_ms, "precision": "fp64"}
+            "bound_kernel_ms": arr.bound_ms, "precision": precision}
 
 
 def bench_tree_api(torch, sp, spatial, net, bounds):
@@ -592,14 +600,14 @@ def bench_host_calls(sp, synth):
             "api": "range_bound_batch(net, centers[4096,3], axes[4096,3,3], AFFINE_FIXED) with NumPy arrays"}
 
 
-def bench_c5(torch, sp, synth, tag, n, flush, peak_tf):
+def bench_c5(torch, sp, synth, tag, n, flush, peak_tf, precision="fp32"):
     net = synth.config_net(tag)
     dn = sp.network.device_net(net)
     lo = torch.empty(n, dtype=torch.float64, device="cuda")
     hi = torch.empty(n, dtype=torch.float64, device="cuda")
     cls = torch.empty(n, dtype=torch.int8, device="cuda")
     out = (lo, hi, cls)
-    run = lambda: sp.bound_random_cubes(net, n, seed=1, half=1.0 / 64, out=out)
+    run = lambda: sp.bound_random_cubes(net, n, seed=1, half=1.0 / 64, out=out, precision=precision)
     run()
     ts = []
     for _ in range(3):
@@ -610,7 +618,7 @@ def bench_c5(torch, sp, synth, tag, n, flush, peak_tf):
     cert = float((cls != 0).float().mean().item())
     return {"boxes": n, "boxes_per_s": n / dt, "ms": dt * 1e3, "tflops": n * flop / dt / 1e12,
             "frac_of_ffma_peak": n * flop / dt / 1e12 / peak_tf, "certified_fraction": cert,
-            "half_extent": 1 / 64}
+            "half_extent": 1 / 64, "precision": precision}
 
 
 def bench_c1(torch, sp, synth, flush, peak_tf):

@@ -73,7 +73,15 @@ enum {
   SPK_POLICY_AFFINE_TRUNCATE = 3
 };
 
-enum { SPK_FP32 = 0, SPK_FP64 = 1 };
+/* precisions.  SPK_FP32_REFINE: FP32 bounds, then the boxes the FP32 pass
+ * leaves UNKNOWN within tau * (S + w) of a certification (S = max(1, |lo|,
+ * |hi|), w = hi - lo; tau: spk_refine_band) are re-bounded in FP64 in
+ * place -- sound either way, and the label is the FP64 (reference-precision)
+ * decision wherever the FP32 rounding budget could have cost one.  Applies to
+ * interval / affine-fixed bounds (spk_bound_batch, spk_bound_aabb,
+ * spk_bound_random_cubes, tree levels, mesh block pruning); point values and
+ * the symbol-carrying policies run FP32. */
+enum { SPK_FP32 = 0, SPK_FP64 = 1, SPK_FP32_REFINE = 2 };
 
 /* sign classes (range_core.py:42-45, 504-509) */
 enum { SPK_NEGATIVE = -1, SPK_UNKNOWN = 0, SPK_POSITIVE = 1 };
@@ -115,6 +123,19 @@ int spk_net_destroy(spk_net* net);
 int spk_net_debug_corrupt_relu(spk_net* net, int on);
 /* widest layer, number of dense layers, and sum_l m_in*m_out (FLOP model) */
 int spk_net_info(const spk_net* net, int* max_width, int* n_dense, int64_t* macs);
+
+/* SPK_FP32_REFINE band.  By default (-1) each net calibrates its own band on
+ * first use, per policy: 3 x the largest FP32 excess over its FP64 enclosure,
+ * in units of S + w, seen on 8192 random cubes (one host sync per net and
+ * policy).  tau >= 0 forces a process-wide band, tau = -1 only queries,
+ * tau = -2 returns to per-net calibration.  *previous (optional) receives the
+ * old setting (-1 = calibrated).  Replaces nothing in the reference (FP64
+ * throughout, range_core.py:547-642). */
+int spk_refine_band(double tau, double* previous);
+/* The band SPK_FP32_REFINE uses for this net and policy (interval /
+ * affine-fixed): the forced band if one is set, else the net's calibrated
+ * band (calibrating it now, on the stream, if it has not been yet). */
+int spk_net_refine_band(const spk_net* net, int policy, void* stream, double* tau);
 
 /* Bound the network over n oriented boxes (device pointers).
  * centers: n x d; axes: n x s x d (all-zero rows are padding,

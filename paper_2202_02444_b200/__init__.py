@@ -41,6 +41,8 @@ from .range_core import (
     bound_aabb,
     bound_random_cubes,
     classify,
+    refine_band,
+    net_refine_band,
     interval_forward,
     interval_forward_batch,
     parse_policy,

@@ -22,7 +22,7 @@ LIB_PATH = Path(os.environ.get("SPK_LIB_PATH") or Path(__file__).resolve().paren
 OK, ERR_DIM, ERR_ACT, ERR_PARAM, ERR_DEPTH, ERR_CUDA, ERR_SHAPE, ERR_OOM = range(8)
 OP_DENSE, OP_RELU, OP_ELU, OP_SIN, OP_TANH, OP_IDENTITY = range(6)
 POLICY_INTERVAL, POLICY_AFFINE_FIXED, POLICY_AFFINE_FULL, POLICY_AFFINE_TRUNCATE = range(4)
-FP32, FP64 = 0, 1
+FP32, FP64, FP32_REFINE = 0, 1, 2
 
 _EXC = {
     ERR_DIM: E.DimensionMismatch,
@@ -47,6 +47,8 @@ f64 = C.c_double
 SIGNATURES = {
     "spk_last_error": ([], C.c_char_p),
     "spk_version": ([], i32),
+    "spk_refine_band": ([f64, vp], i32),
+    "spk_net_refine_band": ([vp, i32, vp, vp], i32),
     "spk_device_sm_count": ([], i32),
     "spk_ffma_peak": ([i32, vp, vp], i32),
     "spk_net_create": ([i32, i32, vp, vp, vp, i64, i32, vp], i32),

@@ -2,6 +2,7 @@
 // validation mirroring the reference's exceptions, dispatch to the fused
 // kernels, and the host-pointer pipelined path.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -313,8 +314,166 @@ cudaError_t dispatch_any(int mmax, int mode, int S, const NetDev<T>& nd, const B
   }
 }
 
+// ------------------------------------------------- FP64 certification refinement
+// SPK_FP32_REFINE: the FP32 pass bounds every box; boxes it leaves UNKNOWN but
+// whose enclosure reaches within tau * (S + w) of certification (-lo or hi <=
+// tau (S + w), S = max(1, |lo|, |hi|), w = hi - lo) are re-bounded by the FP64
+// pass, which reads them through a processing order (BoxInput::perm) and a
+// device-side count, and overwrites their lo / hi / class in place.  FP32 and
+// FP64 bounds are both sound, so every box's result stays sound; the FP64
+// pass (the reference's precision) decides the boxes where the FP32 rounding
+// budget could have cost a certification.  Per-box results do not depend on
+// which other boxes are refined or in which order (each box's bound is
+// independent of its batch).
+// process-wide override of the per-net band (< 0: calibrate per net)
+static std::atomic<double> g_refine_tau{-1.0};
+
+__global__ void refine_select_kernel(const double* __restrict__ lo, const double* __restrict__ hi,
+                                     long long n_cap, const long long* __restrict__ n_dev, double tau,
+                                     int* __restrict__ idx, long long* __restrict__ cnt) {
+  const long long n = n_dev ? *n_dev : n_cap;
+  const int lane = threadIdx.x & 31;
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += (long long)gridDim.x * blockDim.x) {
+    const long long i = base + threadIdx.x;
+    bool c = false;
+    if (i < n) {
+      const double l = lo[i], h = hi[i];
+      if (!(l > 0.0) && !(h < 0.0)) {  // UNKNOWN (NaN bounds never qualify below)
+        const double s = fmax(1.0, fmax(fabs(l), fabs(h)));
+        const double band = tau * (s + (h - l));
+        c = (-l <= band) || (h <= band);
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, c);
+    if (m == 0u) continue;
+    long long b0 = 0;
+    if (lane == 0) b0 = (long long)atomicAdd(reinterpret_cast<unsigned long long*>(cnt), (unsigned long long)__popc(m));
+    b0 = __shfl_sync(0xffffffffu, b0, 0);
+    if (c) idx[b0 + __popc(m & ((1u << lane) - 1u))] = (int)i;
+  }
+}
+
+static int run_pass_once(const spk_net* cnet, int mode, int S, int precision, const BoxInput& in,
+                         const BoundOutput& out, long long n, cudaStream_t st);
+
+// max over boxes of the FP32 excess over the FP64 enclosure in units of
+// S + w (finite bounds only); non-negative doubles order like their bits
+__global__ void refine_excess_kernel(const double* __restrict__ b32, const double* __restrict__ b64, int n,
+                                     unsigned long long* __restrict__ out) {
+  double m = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double l3 = b32[i], h3 = b32[n + i], l6 = b64[i], h6 = b64[n + i];
+    const double s = fmax(1.0, fmax(fabs(l6), fabs(h6)));
+    const double r = fmax(l6 - l3, h3 - h6) / (s + (h6 - l6));
+    if (isfinite(r) && r > m) m = r;
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+// The refine band of a net and mode: the FP32 excess over FP64 depends on the
+// network (measured max / (S + w): 1e-5 on the 7x32 golden nets, 1.1e-3 on
+// C5_64, 5.4e-2 on the 8x256 / 8x512 configs; tools/excess_dist.py), so a
+// fixed band either misses certifications (wide deep nets) or re-bounds most
+// boxes (narrow nets).  Calibrated once per (net, mode), on first use: 4096
+// random cubes over [-1, 1]^d at each of two half-extents (2^-6 and 2^-14:
+// the ratio grows as boxes shrink, towards the point budget), bounded in
+// both precisions; band = 3 x the largest ratio seen.  One host sync per net
+// and mode.  The band only selects which boxes the FP64 pass re-bounds:
+// every result stays sound whatever it is.
+static int refine_tau_for(spk_net* net, int mode, cudaStream_t st, double* tau) {
+  const double forced = g_refine_tau.load();
+  if (forced >= 0.0) {
+    *tau = forced;
+    return SPK_OK;
+  }
+  const int slot = mode == MODE_INTERVAL ? 0 : 1;
+  std::lock_guard<std::mutex> lk(net->calib_mu);
+  if (net->refine_tau[slot] >= 0.0) {
+    *tau = net->refine_tau[slot];
+    return SPK_OK;
+  }
+  constexpr int NC = 4096;
+  const double halves[2] = {0.015625, 6.103515625e-05};
+  void* scratch = nullptr;
+  cudaError_t e = cudaMallocAsync(&scratch, 8 * NC * sizeof(double) + 16, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(refine calibration)");
+  double* b32 = static_cast<double*>(scratch);   // [lo(2NC), hi(2NC)]
+  double* b64 = b32 + 4 * NC;
+  unsigned long long* mx = reinterpret_cast<unsigned long long*>(b64 + 4 * NC);
+  int rc = SPK_OK;
+  for (int h = 0; h < 2 && rc == SPK_OK; ++h) {
+    BoxInput in{IN_RANDOM, net->input_dim, nullptr, nullptr, (long long)h * NC, 0x5EEDull, halves[h], nullptr};
+    BoundOutput o32{b32 + h * NC, b32 + 2 * NC + h * NC, nullptr};
+    BoundOutput o64{b64 + h * NC, b64 + 2 * NC + h * NC, nullptr};
+    rc = run_pass_once(net, mode, net->input_dim, SPK_FP32, in, o32, NC, st);
+    if (rc == SPK_OK) rc = run_pass_once(net, mode, net->input_dim, SPK_FP64, in, o64, NC, st);
+  }
+  unsigned long long bits = 0;
+  if (rc == SPK_OK) {
+    e = cudaMemsetAsync(mx, 0, sizeof(unsigned long long), st);
+    if (e == cudaSuccess) {
+      refine_excess_kernel<<<16, 256, 0, st>>>(b32, b64, 2 * NC, mx);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&bits, mx, sizeof(bits), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "refine calibration");
+  }
+  const cudaError_t ef = cudaFreeAsync(scratch, st);
+  if (rc == SPK_OK && ef != cudaSuccess) rc = cuda_fail(ef, "cudaFreeAsync(refine calibration)");
+  if (rc != SPK_OK) return rc;
+  double ratio;
+  std::memcpy(&ratio, &bits, sizeof(ratio));
+  net->refine_tau[slot] = std::min(0.25, 3.0 * ratio);
+  *tau = net->refine_tau[slot];
+  return SPK_OK;
+}
+
 int run_pass(const spk_net* cnet, int mode, int S, int precision, const BoxInput& in,
              const BoundOutput& out, long long n, cudaStream_t st) {
+  if (precision != SPK_FP32_REFINE) return run_pass_once(cnet, mode, S, precision, in, out, n, st);
+  // point values and missing outputs: plain FP32
+  if (mode == MODE_POINT || out.lo == nullptr || out.hi == nullptr || n <= 0)
+    return run_pass_once(cnet, mode, S, SPK_FP32, in, out, n, st);
+  if (int rc = run_pass_once(cnet, mode, S, SPK_FP32, in, out, n, st)) return rc;
+  spk_net* net = const_cast<spk_net*>(cnet);
+  DeviceGuard g(net->device);
+  const int sm = sm_count_for(net->device);
+  double tau = 0.0;
+  if (int rc = refine_tau_for(net, mode, st, &tau)) return rc;
+  // candidates: n_cap indices + the device count (16-byte aligned)
+  void* scratch = nullptr;
+  const size_t idx_bytes = (((size_t)n * sizeof(int)) + 15) & ~(size_t)15;
+  cudaError_t e = cudaMallocAsync(&scratch, idx_bytes + 16, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(refine)");
+  int* idx = static_cast<int*>(scratch);
+  long long* cnt = reinterpret_cast<long long*>(static_cast<char*>(scratch) + idx_bytes);
+  e = cudaMemsetAsync(cnt, 0, sizeof(long long), st);
+  if (e == cudaSuccess) {
+    const long long blocks = std::min<long long>((n + 255) / 256, (long long)sm * 8);
+    refine_select_kernel<<<(int)blocks, 256, 0, st>>>(out.lo, out.hi, n, in.n_dev, tau, idx, cnt);
+    e = cudaGetLastError();
+  }
+  int rc = SPK_OK;
+  if (e != cudaSuccess) {
+    rc = cuda_fail(e, "refine select");
+  } else {
+    BoxInput in2 = in;
+    in2.perm = idx;
+    in2.n_dev = cnt;
+    in2.pair_order = 0;
+    in2.spread = 0;
+    in2.small = 0;
+    rc = run_pass_once(cnet, mode, S, SPK_FP64, in2, out, n, st);
+  }
+  const cudaError_t ef = cudaFreeAsync(scratch, st);
+  if (rc == SPK_OK && ef != cudaSuccess) rc = cuda_fail(ef, "cudaFreeAsync(refine)");
+  return rc;
+}
+
+static int run_pass_once(const spk_net* cnet, int mode, int S, int precision, const BoxInput& in,
+                         const BoundOutput& out, long long n, cudaStream_t st) {
   spk_net* net = const_cast<spk_net*>(cnet);
   DeviceGuard g(net->device);
   const int sm = sm_count_for(net->device);
@@ -426,6 +585,25 @@ extern "C" {
 
 const char* spk_last_error(void) { return g_last_error.c_str(); }
 int spk_version(void) { return 100; }
+
+int spk_net_refine_band(const spk_net* net, int policy, void* stream, double* tau) {
+  if (!net || !tau) return fail(SPK_ERR_INVALID_PARAMETER, "null argument");
+  int mode;
+  if (int rc = check_policy(policy, 1, &mode)) return rc;
+  if (mode < 0) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "refinement covers interval / affine-fixed");
+  if (net->input_dim > MAX_AXES) return fail(SPK_ERR_UNSUPPORTED_SHAPE, "refinement supports d <= 8");
+  spk_net* n = const_cast<spk_net*>(net);
+  DeviceGuard g(n->device);
+  return refine_tau_for(n, mode, (cudaStream_t)stream, tau);
+}
+
+int spk_refine_band(double tau, double* previous) {
+  if (std::isnan(tau) || std::isinf(tau)) return fail(SPK_ERR_INVALID_PARAMETER, "refine band must be finite");
+  // tau >= 0: fixed band; -1: query only; -2: back to per-net calibration
+  const double old = tau == -2.0 ? g_refine_tau.exchange(-1.0) : (tau < 0.0 ? g_refine_tau.load() : g_refine_tau.exchange(tau));
+  if (previous) *previous = old;
+  return SPK_OK;
+}
 
 int spk_device_sm_count(void) {
   int dev = 0;

@@ -91,6 +91,10 @@ struct spk_net {
   std::vector<int> pre_acts;
   std::vector<spk::HostLayer> layers;
   std::mutex mu;
+  // SPK_FP32_REFINE: per-mode calibrated band (interval, affine-fixed; < 0 =
+  // not yet calibrated), spk_abi.cu refine_tau_for
+  std::mutex calib_mu;
+  double refine_tau[2] = {-1.0, -1.0};
   spk::DevNet<float> f32;
   spk::DevNet<double> f64;
   template <typename T> spk::DevNet<T>& dev();

@@ -6,7 +6,10 @@ sm_100a kernels behind the C-ABI.
 signature and return types: FP64 NumPy in, FP64 NumPy out.  CUDA tensors are
 accepted too and stay on the device (the throughput path).  `precision`
 selects the kernel arithmetic: "fp32" (default: FP32 FFMA with directed
-rounding, sound) or "fp64".
+rounding, sound), "fp64", or "fp32-refine" (FP32, then the boxes FP32 leaves
+UNKNOWN within a calibrated band of a certification re-bounded in FP64: the
+labels are the reference-precision decisions at close to FP32 cost;
+`refine_band`).
 """
 
 from __future__ import annotations
@@ -176,6 +179,38 @@ def _trim_axes(axes):
         nz = np.any(axes != 0.0, axis=(0, 2))
         keep = int(np.flatnonzero(nz).max()) + 1 if nz.any() else 0
     return axes[:, :keep, :]
+
+
+def refine_band(tau=None) -> float:
+    """Get (and, given tau, set) the band of precision "fp32-refine": UNKNOWN
+    boxes whose FP32 bound comes within tau * (S + w) of certifying (-lo or
+    hi <= tau (S + w), S = max(1, |lo|, |hi|)) are re-bounded in FP64.
+    Default ("auto", reported as -1): each net calibrates its own band on
+    first use (3 x its largest FP32 excess over FP64 on 8192 random cubes).
+    A float >= 0 forces a process-wide band.  Returns the previous setting."""
+    prev = C.c_double(0.0)
+    if tau is None:
+        _lib.call("spk_refine_band", -1.0, C.byref(prev))  # query only
+        return prev.value
+    if isinstance(tau, str):
+        if tau != "auto":
+            raise InvalidParameter(f"unknown refine band {tau!r}")
+        _lib.call("spk_refine_band", -2.0, C.byref(prev))
+        return prev.value
+    if not (float(tau) >= 0.0) or not np.isfinite(tau):
+        raise InvalidParameter("refine band must be finite and >= 0")
+    _lib.call("spk_refine_band", float(tau), C.byref(prev))
+    return prev.value
+
+
+def net_refine_band(net, policy=AFFINE_FIXED, device=None) -> float:
+    """The band "fp32-refine" uses for this net and policy (calibrating the
+    net's band now if no process-wide band is forced)."""
+    pcode, _ = policy_code(policy)
+    dn = device_net(net, device)
+    out = C.c_double(0.0)
+    _lib.call("spk_net_refine_band", dn.ptr, pcode, dv.stream_ptr(device), C.byref(out))
+    return out.value
 
 
 def range_bound_batch(net, centers, axes, policy=AFFINE_FIXED, precision: str = "fp32",
