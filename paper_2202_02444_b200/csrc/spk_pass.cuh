@@ -123,6 +123,9 @@ constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reducti
 #ifndef SPK_RUNERR
 #define SPK_RUNERR 1  // FP32 affine K loops: running (a-posteriori) rounding bound of the base column
 #endif
+#ifndef SPK_F64_BASE
+#define SPK_F64_BASE 0  // ... in FP64 instead (DFMA base column on those layers; measured C2 +20%, excess 5.4 -> 4.6%: off)
+#endif
 #ifndef SPK_FUSED_RELU
 #define SPK_FUSED_RELU 1  // affine-fixed ReLU layers: fused rule + pack, straddle branch behind a warp vote
 #endif
@@ -988,11 +991,21 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
   // runtime per layer (LayerDev::runerr, set by the host for the leading wide
   // layers whose budgets dominate): the K loop below exists in both forms
   const bool re_layer = RUN && L.runerr;
-  float erun[RUN ? TI : 1][RUN ? TB : 1];
+  // F64B: the running-error layers accumulate their base column in FP64
+  // instead (one DFMA per (neuron, box) and k-step on the FP64 pipe, beside
+  // the FP32 pipe's packed columns): the FP64 sum's own rounding (<= gamma_n
+  // of 2^-53, ~1e-14 relative) sits inside the pack's a-priori weight-rounding
+  // charge (gamma_base_next = 2^-24 (1 + 1e-6)), and the final FP64 -> FP32
+  // rounding of the base is charged exactly, |b64 - RN(b64)|, so the layer's
+  // base column costs ~u |base| instead of Wilkinson's u sum_k |s_k|.  Skipped
+  // all-zero rows add exact zeros, so results stay order-independent.
+  constexpr bool F64B = RUN && SPK_F64_BASE;
+  float erun[RUN && !F64B ? TI : 1][RUN && !F64B ? TB : 1];
+  double base64[F64B ? TI : 1][F64B ? TB : 1];
 #pragma unroll
-  for (int ti = 0; ti < (RUN ? TI : 1); ++ti)
+  for (int ti = 0; ti < (RUN && !F64B ? TI : 1); ++ti)
 #pragma unroll
-    for (int tb = 0; tb < (RUN ? TB : 1); ++tb) erun[ti][tb] = 0.f;
+    for (int tb = 0; tb < (RUN && !F64B ? TB : 1); ++tb) erun[ti][tb] = 0.f;
   const int ng = tid % CF::NG, bg = tid / CF::NG;
 
   constexpr int NPA = NP > 0 ? NP : 1;
@@ -1023,6 +1036,7 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
     for (int tb = 0; tb < TB; ++tb) {
       acco[ti][tb] = (ODD && NP == 0) ? b0 : 0.f;  // C == 2: the odd column is the base
       acce[ti][tb] = 0.f;
+      if constexpr (F64B) base64[ti][tb] = (double)b0;
     }
   }
   constexpr int SUBIN = KT < CF::SUB ? KT : CF::SUB;
@@ -1044,7 +1058,7 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
       for (int g = 0; g < NBOX; ++g) {
 #pragma unroll
         for (int p = 0; p < NP; ++p) accp[ti][g][p] = f2_add(accp[ti][g][p], partp[ti][g][p]);
-        if (REC) {  // the flush's own rounding: u |acc_new|
+        if (REC && !F64B) {  // the flush's own rounding: u |acc_new|
           float b_, a_;
           f2_split(accp[ti][g][0], b_, a_);
           erun[ti][g] = __fadd_ru(erun[ti][g], fabsf(b_));
@@ -1109,9 +1123,13 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
             // all-zero rows the live-row masks skip -- results stay identical
             // for any batch composition
             float b_, a_, x0_, x1_;
-            f2_split(ONEBLK ? accp[ti][g][0] : partp[ti][g][0], b_, a_);
             f2_split(xv, x0_, x1_);
-            erun[ti][g] = __fmaf_ru(fabsf(b_), x0_ != 0.f ? 1.f : 0.f, erun[ti][g]);
+            if constexpr (F64B) {
+              base64[ti][g] = __fma_rn((double)w[ti], (double)x0_, base64[ti][g]);
+            } else {
+              f2_split(ONEBLK ? accp[ti][g][0] : partp[ti][g][0], b_, a_);
+              erun[ti][g] = __fmaf_ru(fabsf(b_), x0_ != 0.f ? 1.f : 0.f, erun[ti][g]);
+            }
           }
         }
       if (!POINT) {
@@ -1267,8 +1285,18 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
         } else {
           acc[ti][tb][C - 1] = acce[ti][tb];
         }
-        // base column rounding <= u/(1-u) sum |s| with u/(1-u) <= 0x1.000002p-24
-        if (RUN && re_layer) acc[ti][tb][C - 1] = __fmaf_ru(erun[ti][tb], 0x1.000002p-24f, acc[ti][tb][C - 1]);
+        if constexpr (F64B) {
+          if (re_layer) {
+            // the FP64 base rounded to FP32, its rounding charged exactly
+            const double b64 = base64[ti][tb];
+            const float b32 = __double2float_rn(b64);
+            acc[ti][tb][0] = b32;
+            acc[ti][tb][C - 1] = __fadd_ru(acc[ti][tb][C - 1], __double2float_ru(fabs(b64 - (double)b32)));
+          }
+        } else if (RUN && re_layer) {
+          // base column rounding <= u/(1-u) sum |s| with u/(1-u) <= 0x1.000002p-24
+          acc[ti][tb][C - 1] = __fmaf_ru(erun[ti][RUN ? tb : 0], 0x1.000002p-24f, acc[ti][tb][C - 1]);
+        }
       }
     }
   }
