@@ -490,6 +490,9 @@ def run_ours(args, rank, world, local_rank):
     extra["C5_8x64_16M_fp32_refine"] = clocked(bench_c5, torch, sp, synth, "C5_64", 16 << 20, flush, peak_tf,
                                                "fp32-refine")
     extra["C5_8x64_16M_fp64"] = clocked(bench_c5, torch, sp, synth, "C5_64", 16 << 20, flush, peak_tf, "fp64")
+    # the headline architecture with a real surface (trained torus SDF): what
+    # plain FP32 costs in certifications and what fp32-refine recovers
+    extra["trained_torus_8x256_tree_d21"] = clocked(bench_trained_tree, torch, sp, spatial, synth, bounds, flush)
     extra["C1_4x32_64cubed"] = clocked(bench_c1, torch, sp, synth, flush, peak_tf)
     extra["host_range_bound_batch_4096"] = clocked(bench_host_calls, sp, synth)
     if not args.no_mesh:
@@ -555,6 +558,29 @@ def bench_c2_fp64(torch, sp, spatial, net, bounds, flush, precision="fp64"):
     dt = float(np.median(ts))
     return {"nodes": arr.n_nodes, "boxes_per_s": arr.n_nodes / dt, "ms": dt * 1e3,
             "bound_kernel_ms": arr.bound_ms, "precision": precision}
+
+
+def bench_trained_tree(torch, sp, spatial, synth, bounds, flush, depth=21):
+    """k-d tree to depth 21 on the trained 3->8x256->1 ReLU torus SDF
+    (synth.trained_net; the C2 architecture, certifying 6.6% of its nodes):
+    FP32, fp32-refine and FP64 node counts, certifications and times.
+    fp32-refine reproduces the FP64 (= reference) topology."""
+    net = synth.trained_net("torus")
+    out = {"net": "trained 3->8x256->1 ReLU torus SDF (tests/golden/nets/torus_8x256.npz)", "depth": depth,
+           "refine_band": sp.net_refine_band(net)}
+    levels = {}
+    for prec in ("fp32", "fp32-refine", "fp64"):
+        run = lambda: spatial.build_spatial_tree_arrays(net, bounds, policy=sp.AFFINE_FIXED, max_depth=depth,
+                                                        precision=prec, to_host=False)
+        run()
+        dt, arr = timed(run, torch, flush, lambda: None)
+        levels[prec] = [len(lv.label) for lv in arr.levels]
+        cert = sum(int((lv.label != 0).sum().item()) for lv in arr.levels)
+        out[prec] = {"ms": dt * 1e3, "nodes": arr.n_nodes, "certified_nodes": cert,
+                     "node_bounds_per_s": arr.n_nodes / dt}
+        del arr
+    out["refine_topology_equals_fp64"] = levels["fp32-refine"] == levels["fp64"]
+    return out
 
 
 def bench_tree_api(torch, sp, spatial, net, bounds):

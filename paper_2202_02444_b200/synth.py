@@ -87,6 +87,25 @@ def random_mlp(width: int, depth: int, activation="relu", recipe="torch-uniform"
                        name or f"{recipe}_{activation}_{depth}x{width}_s{seed}")
 
 
+def trained_net(tag: str = "torus") -> NetworkSpec:
+    """A trained 3->8x256->1 ReLU SDF net (the C2 architecture; FP32 weights,
+    tools/train_sdf_net.py): a non-degenerate net of the headline shape, whose
+    trees certify most of the domain -- the random-init configs certify nothing."""
+    from pathlib import Path
+
+    if tag != "torus":
+        raise ValueError(tag)
+    path = Path(__file__).resolve().parents[1] / "tests" / "golden" / "nets" / "torus_8x256.npz"
+    with np.load(path) as z:
+        n = len([k for k in z.files if k.startswith("W")])
+        layers = []
+        for i in range(n):
+            layers.append(DenseLayer(z[f"W{i}"].astype(np.float64), z[f"b{i}"].astype(np.float64)))
+            if i < n - 1:
+                layers.append(ActivationKind.RELU)
+    return NetworkSpec(3, tuple(layers), "sdf", "torus_8x256")
+
+
 # Named configs of BASELINE.json (C1..C5)
 def config_net(tag: str, seed: int = 0) -> NetworkSpec:
     if tag == "C1":
