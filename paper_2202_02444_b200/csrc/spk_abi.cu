@@ -159,6 +159,17 @@ int build_device_net(spk_net* net, DevNet<T>& dn) {
   struct Offs { size_t w = 0, b = 0, be = 0; };
   std::vector<Offs> offs(net->layers.size());
   std::vector<double> gam(net->layers.size());
+  // weight rounding budget u_w per layer: 0 when every weight and bias of the
+  // layer is exactly representable in T (e.g. nets trained in FP32 and
+  // exported): the device then holds the reference's FP64 network exactly
+  std::vector<double> uw(net->layers.size(), 0.0);
+  for (size_t l = 0; l < net->layers.size() && fp32; ++l) {
+    const HostLayer& L = net->layers[l];
+    bool exact = true;
+    for (double w : L.W) exact = exact && ((double)(float)w == w);
+    for (double b : L.b) exact = exact && ((double)(float)b == b);
+    uw[l] = exact ? 0.0 : 5.9604644775390625e-8 * (1.0 + 1e-6);
+  }
   for (size_t l = 0; l < net->layers.size(); ++l) {
     const HostLayer& L = net->layers[l];
     // only the final (width-1) layer takes the warp-reduction path; every
@@ -194,8 +205,8 @@ int build_device_net(spk_net* net, DevNet<T>& dn) {
       }
     }
     // + u for FP32: W and b are rounded from FP64 to T, |dW| <= u|W|, so the
-    // certified function is the reference's FP64 network.
-    gam[l] = gamma_n_host(n_eff, fp32) + (fp32 ? 5.9604644775390625e-8 * (1.0 + 1e-6) : 0.0);
+    // certified function is the reference's FP64 network (0 for FP32-exact layers)
+    gam[l] = gamma_n_host(n_eff, fp32) + uw[l];
     // SPK_NET_FP64_UNPADDED: the reference's own FP64 arithmetic (no a-priori
     // dot-product budget), for callers that compare at 1e-15 (integration shim)
     if (!fp32 && (net->flags & SPK_NET_FP64_UNPADDED)) gam[l] = 0.0;
@@ -274,7 +285,7 @@ int build_device_net(spk_net* net, DevNet<T>& dn) {
     // the weights' FP64 -> T rounding (u |W| |base|) a priori
     D.runerr = fp32 && run_layer(l) ? 1 : 0;
     D.gamma_base_next = (fp32 && l + 1 < net->layers.size() && run_layer(l + 1))
-                            ? round_up_to<T>(5.9604644775390625e-8 * (1.0 + 1e-6))
+                            ? round_up_to<T>(uw[l + 1])
                             : D.gamma_next;
   }
   dn.nd = nd;
