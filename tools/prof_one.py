@@ -25,6 +25,13 @@ def main():
         lo_c = torch.from_numpy(c - 1 / 64).cuda()
         hi_c = torch.from_numpy(c + 1 / 64).cuda()
         run = lambda: sp.bound_aabb(net, lo_c, hi_c, sp.AFFINE_FIXED)
+    elif which == "small":  # a top tree level: one sibling pair (the SM = 1 small tile, one CTA)
+        n = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+        net = synth.config_net("C2")
+        c, a = synth.grid_cubes(64)
+        lo_c = torch.from_numpy(c[:n] - 1 / 64).cuda()
+        hi_c = torch.from_numpy(c[:n] + 1 / 64).cuda()
+        run = lambda: sp.bound_aabb(net, lo_c, hi_c, sp.AFFINE_FIXED)
     elif which == "c5":
         n = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 20
         net = synth.config_net("C5_256")
