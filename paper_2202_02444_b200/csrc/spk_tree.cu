@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cmath>
 #include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "spk_kernels.cuh"
@@ -288,6 +289,62 @@ void keep_pool_memory(int device) {
   done[device] = 1;
 }
 
+// Host-mirror blocks of >= 1 MB come from a process-wide pool of pinned
+// (page-locked, portable) blocks in power-of-two size classes: the
+// device-to-host copies of large levels run as DMA at full PCIe rate instead
+// of through pageable staging, and a block freed with its tree is reused by
+// the next build (no cudaHostAlloc per build).  Smaller blocks use malloc.
+// At most kPinnedKeep bytes stay cached.
+namespace {
+constexpr size_t kPinnedMin = 1u << 20;
+constexpr size_t kPinnedKeep = (size_t)2 << 30;
+std::mutex g_pin_mu;
+std::vector<std::pair<size_t, char*>> g_pin_free;  // (class size, block)
+size_t g_pin_cached = 0;
+std::unordered_map<char*, size_t> g_pin_live;    // pinned blocks handed out -> class size
+
+char* host_block(size_t bytes) {
+  if (bytes < kPinnedMin) return static_cast<char*>(std::malloc(std::max<size_t>(bytes, 1)));
+  size_t cls = kPinnedMin;
+  while (cls < bytes) cls <<= 1;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  for (size_t i = 0; i < g_pin_free.size(); ++i) {
+    if (g_pin_free[i].first == cls) {
+      char* b = g_pin_free[i].second;
+      g_pin_free.erase(g_pin_free.begin() + (long)i);
+      g_pin_cached -= cls;
+      g_pin_live[b] = cls;
+      return b;
+    }
+  }
+  void* b = nullptr;
+  if (cudaHostAlloc(&b, cls, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();  // fall back to pageable memory
+    return static_cast<char*>(std::malloc(bytes));
+  }
+  g_pin_live[static_cast<char*>(b)] = cls;
+  return static_cast<char*>(b);
+}
+
+void host_block_free(char* b) {
+  if (!b) return;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  auto it = g_pin_live.find(b);
+  if (it == g_pin_live.end()) {
+    std::free(b);
+    return;
+  }
+  const size_t cls = it->second;
+  g_pin_live.erase(it);
+  if (g_pin_cached + cls <= kPinnedKeep) {
+    g_pin_free.emplace_back(cls, b);
+    g_pin_cached += cls;
+  } else {
+    cudaFreeHost(b);
+  }
+}
+}  // namespace
+
 // Copy level `lv` of the build into host memory on the copy stream `cst`
 // once the compute stream has passed event `done`: the host thread blocks on
 // the (pageable) copy while the GPU already runs the next level's kernels.
@@ -302,7 +359,7 @@ static int mirror_level(spk_tree* tree, int lv, const TreeLevel& L, const long l
   const size_t sz[7] = {m * d * 8, m * d * 8, m * 8, m * 8, m, m, m * 8};
   size_t total = 0;
   for (size_t b : sz) total += b;
-  char* h = static_cast<char*>(std::malloc(std::max<size_t>(total, 1)));
+  char* h = host_block(total);
   if (!h) return fail(SPK_ERR_OUT_OF_MEMORY, "tree host mirror");
   const void* src[7] = {L.lo, L.hi, L.blo, L.bhi, L.label, L.face, L.parent};
   size_t off = 0;
@@ -312,7 +369,7 @@ static int mirror_level(spk_tree* tree, int lv, const TreeLevel& L, const long l
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(cst);
   if (e != cudaSuccess) {
-    std::free(h);
+    host_block_free(h);
     return cuda_fail(e, "tree mirror copy");
   }
   if ((int)tree->host.size() <= lv) {
@@ -325,7 +382,7 @@ static int mirror_level(spk_tree* tree, int lv, const TreeLevel& L, const long l
 }
 
 static void free_mirror(spk_tree* tree) {
-  for (char* h : tree->host) std::free(h);
+  for (char* h : tree->host) host_block_free(h);
   tree->host.clear();
   tree->host_n.clear();
 }
@@ -540,7 +597,7 @@ int spk_tree_build_ex(const spk_net* net, int policy, int n_keep, int precision,
       free_level(tree->levels.back(), st);
       tree->levels.pop_back();
       if (tree->host.size() > tree->levels.size()) {
-        std::free(tree->host.back());
+        host_block_free(tree->host.back());
         tree->host.pop_back();
         tree->host_n.pop_back();
       }
