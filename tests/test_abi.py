@@ -77,3 +77,28 @@ def test_single_form_bookkeeping():
         sp.condense(a, [5])
     with pytest.raises(sp.errors.InvalidParameter):
         sp.truncate(a, 0)
+
+
+def test_refine_band_setting_is_host_only():
+    """spk_refine_band (the fp32-refine band override) is host state: set,
+    query, reset to per-net calibration, and validation -- no device needed."""
+    import paper_2202_02444_b200 as sp
+    from paper_2202_02444_b200.network import _precision_code
+
+    assert _precision_code("fp32-refine") == _lib.FP32_REFINE == 2
+    prev = sp.refine_band()
+    try:
+        sp.refine_band(0.01)
+        assert sp.refine_band() == 0.01
+        assert sp.refine_band("auto") == 0.01
+        assert sp.refine_band() == -1.0  # per-net calibration
+        for bad in (float("nan"), float("inf"), -0.5):
+            with pytest.raises(errors.InvalidParameter):
+                sp.refine_band(bad)
+        with pytest.raises(errors.InvalidParameter):
+            sp.refine_band("sometimes")
+    finally:
+        if prev >= 0:
+            sp.refine_band(prev)
+        else:
+            sp.refine_band("auto")
