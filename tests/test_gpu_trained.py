@@ -97,3 +97,20 @@ def test_trained_tree(gold, net, policy):
                     assert np.max(np.abs(lv.bound_lo - w["bound_lo"]) / S) <= 1e-8
                 if prec != "fp32":
                     _check_labels(lv.label, w["label"], w["bound_lo"], w["bound_hi"])
+
+
+def test_trained_sharded_refine_equals_unsharded(net):
+    """fp32-refine through the sharded builder: every rank's net calibrates the
+    same band and each node's bound is independent of its batch, so the
+    merged shards equal the unsharded refined tree array for array."""
+    full = spatial.build_spatial_tree_arrays(net, BOUNDS, policy=sp.AFFINE_FIXED, max_depth=20,
+                                             precision="fp32-refine", to_host=True)
+    world = 4
+    parts = [spatial.build_spatial_tree_sharded(net, BOUNDS, 20, sp.AFFINE_FIXED, r, world, precision="fp32-refine",
+                                                min_roots_per_rank=2, to_host=True, roots="interleaved")
+             for r in range(world)]
+    merged = spatial.merge_sharded_trees(parts)
+    assert merged.n_nodes == full.n_nodes and sum(int((lv.label != 0).sum()) for lv in full.levels) > 0
+    for d, (g, f) in enumerate(zip(merged.levels, full.levels)):
+        for k in ("lo", "hi", "bound_lo", "bound_hi", "label"):
+            np.testing.assert_array_equal(getattr(g, k), getattr(f, k), err_msg=f"{k} at depth {d}")
