@@ -27,6 +27,13 @@
 #define SPK_PAIR_ORDER 1  // bound tree levels in sibling-pair order (BoxInput::pair_order)
 #endif
 
+#ifndef SPK_TREE_SPECULATE
+#define SPK_TREE_SPECULATE 1  // fixed-depth builds bound their latency-bound top levels in one launch
+#endif
+#ifndef SPK_SPEC_PER_SM
+#define SPK_SPEC_PER_SM 16 // ... the levels of at most this many nodes per SM
+#endif
+
 namespace spk {
 
 constexpr int TB_THREADS = 256;
@@ -179,6 +186,81 @@ __global__ void tree_scatter_kernel(const long long* __restrict__ n_dev, int d, 
   }
   child_parent[j] = i;
   child_parent[n_split + j] = i;
+}
+
+// Speculative top levels (fixed-depth builds).  The top levels of a tree hold
+// a few hundred nodes each and their bound launches are latency-bound (~80 us
+// whatever their size), while a node's AABB depends only on its path (widest
+// axis, FP64 midpoint) and its bound only on its AABB.  So the complete binary
+// tree of the first L levels is generated and bounded in ONE launch, and each
+// of those levels then fetches its live nodes' bounds from it.  Level k of the
+// complete tree (size n_roots 2^k, offset n_roots (2^k - 1)) is laid out like
+// the reference's levels: child c of level k+1 has parent c mod size_k and is
+// the high half when c >= size_k (tree_scatter_kernel with every node split).
+__global__ void spec_boxes_kernel(long long n_roots, int L, int d, const double* __restrict__ root_lo,
+                                  const double* __restrict__ root_hi, double* __restrict__ lo,
+                                  double* __restrict__ hi) {
+  const long long total = n_roots * ((1ll << L) - 1);
+  const long long g = (long long)blockIdx.x * TB_THREADS + threadIdx.x;
+  if (g >= total) return;
+  int k = 0;
+  while (n_roots * ((1ll << (k + 1)) - 1) <= g) ++k;
+  long long i = g - n_roots * ((1ll << k) - 1);
+  unsigned long long bits = 0;  // bit j-1: the node's ancestor at level j is a high half
+  for (int j = k; j >= 1; --j) {
+    const long long half = n_roots << (j - 1);
+    if (i >= half) {
+      bits |= 1ull << (j - 1);
+      i -= half;
+    }
+  }
+  double bl[MAX_AXES], bh[MAX_AXES];
+  for (int q = 0; q < d; ++q) {
+    bl[q] = root_lo[i * d + q];
+    bh[q] = root_hi[i * d + q];
+  }
+  for (int j = 1; j <= k; ++j) {
+    // tree_scatter_kernel's split: widest axis, ties to the lowest index, FP64 midpoint
+    int ax = 0;
+    double best = -1.0;
+    for (int q = 0; q < d; ++q) {
+      const double e = bh[q] - bl[q];
+      if (e > best) { best = e; ax = q; }
+    }
+    const double mid = 0.5 * (bl[ax] + bh[ax]);
+    if ((bits >> (j - 1)) & 1ull) bl[ax] = mid; else bh[ax] = mid;
+  }
+  for (int q = 0; q < d; ++q) {
+    lo[g * d + q] = bl[q];
+    hi[g * d + q] = bh[q];
+  }
+}
+
+// live node i of a speculative level: its bound from the complete tree
+// (cidx = its index within the complete level; nullptr at the roots)
+__global__ void spec_fetch_kernel(const long long* __restrict__ n_dev, const long long* __restrict__ cidx,
+                                  long long offset, const double* __restrict__ sblo, const double* __restrict__ sbhi,
+                                  const int8_t* __restrict__ slab, double* __restrict__ blo, double* __restrict__ bhi,
+                                  int8_t* __restrict__ label) {
+  const long long n = *n_dev;
+  const long long i = (long long)blockIdx.x * TB_THREADS + threadIdx.x;
+  if (i >= n) return;
+  const long long g = offset + (cidx ? cidx[i] : i);
+  blo[i] = sblo[g];
+  bhi[i] = sbhi[g];
+  label[i] = slab[g];
+}
+
+// complete-level index of the next level's nodes: child c is the high half
+// when c >= K (tree_scatter_kernel), of parent p = parent[c]
+__global__ void spec_child_index_kernel(const long long* __restrict__ n_next, const long long* __restrict__ k_dev,
+                                        const long long* __restrict__ parent, const long long* __restrict__ cidx,
+                                        long long level_size, long long* __restrict__ cidx_next) {
+  const long long n = *n_next, K = *k_dev;
+  const long long c = (long long)blockIdx.x * TB_THREADS + threadIdx.x;
+  if (c >= n) return;
+  const long long p = parent[c];
+  cidx_next[c] = (cidx ? cidx[p] : p) + (c >= K ? level_size : 0);
 }
 
 // Face centres of tiny leaves: (m, 2d, d) points (spatial.py:202-211).
@@ -477,6 +559,48 @@ int spk_tree_build_ex(const spk_net* net, int policy, int n_keep, int precision,
     delete tree;
     return fail(SPK_ERR_CUDA, "tree mirror stream");
   }
+  // speculative top levels (fixed-depth builds of the fused policies): the
+  // first spec_L levels whose complete size stays within 4 boxes per SM
+  int spec_L = 0;
+  {
+    int mode_chk = policy == SPK_POLICY_INTERVAL || policy == SPK_POLICY_AFFINE_FIXED;
+    const long long lim = SPK_TREE_SPECULATE ? (long long)SPK_SPEC_PER_SM * std::max(sm_count_for(net->device), 1) : 0;
+    const int levels_left = fixed ? max_depth - start_depth + 1 : 0;
+    for (long long sz = n_roots; mode_chk && spec_L < levels_left && spec_L < 20 && sz <= lim; sz *= 2) ++spec_L;
+    if (level_cap >= 0) spec_L = std::min(spec_L, level_cap + 1);
+    if (spec_L < 2) spec_L = 0;
+  }
+  double* spec_lo = nullptr;  // complete-tree AABBs (S x d) x 2, bounds (S) x 2, labels (S)
+  double *spec_blo = nullptr, *spec_bhi = nullptr;
+  int8_t* spec_lab = nullptr;
+  long long* spec_idx[2] = {nullptr, nullptr};
+  cudaEvent_t spec_e0 = nullptr, spec_e1 = nullptr;
+  if (spec_L > 0) {
+    const long long S = n_roots * ((1ll << spec_L) - 1), top = n_roots << (spec_L - 1);
+    char* base = nullptr;
+    const size_t b_box = align_up((size_t)S * d * sizeof(double)), b_b = align_up((size_t)S * sizeof(double)),
+                 b_l = align_up((size_t)S), b_i = align_up((size_t)top * sizeof(long long));
+    if (cudaMallocAsync(&base, 2 * b_box + 2 * b_b + b_l + 2 * b_i, st) != cudaSuccess) {
+      rc = fail(SPK_ERR_OUT_OF_MEMORY, "speculative levels");
+    } else {
+      spec_lo = reinterpret_cast<double*>(base);
+      spec_blo = reinterpret_cast<double*>(base + 2 * b_box);
+      spec_bhi = reinterpret_cast<double*>(base + 2 * b_box + b_b);
+      spec_lab = reinterpret_cast<int8_t*>(base + 2 * b_box + 2 * b_b);
+      spec_idx[0] = reinterpret_cast<long long*>(base + 2 * b_box + 2 * b_b + b_l);
+      spec_idx[1] = reinterpret_cast<long long*>(base + 2 * b_box + 2 * b_b + b_l + b_i);
+      double* spec_hi = reinterpret_cast<double*>(base + b_box);
+      spec_boxes_kernel<<<(int)((S + TB_THREADS - 1) / TB_THREADS), TB_THREADS, 0, st>>>(n_roots, spec_L, d, cur.lo,
+                                                                                        cur.hi, spec_lo, spec_hi);
+      cudaEventCreate(&spec_e0);
+      cudaEventCreate(&spec_e1);
+      cudaEventRecord(spec_e0, st);
+      rc = bound_aabb_internal(net, policy, n_keep, precision, S, nullptr, spec_lo, spec_hi, spec_blo, spec_bhi,
+                               spec_lab, st, 0);
+      cudaEventRecord(spec_e1, st);
+      tree->launches += 2;
+    }
+  }
   for (int depth = start_depth, lv = 0; rc == SPK_OK; ++depth, ++lv) {
     if (lv >= kMaxLevels) { rc = fail(SPK_ERR_DEPTH_OVERFLOW, "more than 64 tree levels"); break; }
     long long* n_dev = d_cnt + lv;
@@ -490,8 +614,14 @@ int spk_tree_build_ex(const spk_net* net, int policy, int n_keep, int precision,
     cudaEventRecord(e0, st);
     // levels below the roots are [low children; high children]: bound them in
     // sibling-pair order (identical results; coherent live-row masks)
-    rc = bound_aabb_internal(net, policy, n_keep, precision, cur_cap, n_dev, cur.lo, cur.hi, cur.blo, cur.bhi,
-                             cur.label, st, (SPK_PAIR_ORDER && lv > 0) ? 1 : 0);
+    if (lv < spec_L) {
+      const long long* cidx = lv == 0 ? nullptr : spec_idx[lv & 1];
+      spec_fetch_kernel<<<(int)((cur_cap + TB_THREADS - 1) / TB_THREADS), TB_THREADS, 0, st>>>(
+          n_dev, cidx, n_roots * ((1ll << lv) - 1), spec_blo, spec_bhi, spec_lab, cur.blo, cur.bhi, cur.label);
+    } else {
+      rc = bound_aabb_internal(net, policy, n_keep, precision, cur_cap, n_dev, cur.lo, cur.hi, cur.blo, cur.bhi,
+                               cur.label, st, (SPK_PAIR_ORDER && lv > 0) ? 1 : 0);
+    }
     cudaEventRecord(e1, st);
     if (rc != SPK_OK) break;
     tree->launches += 4;
@@ -532,6 +662,12 @@ int spk_tree_build_ex(const spk_net* net, int policy, int n_keep, int precision,
     // always launched: it also lists the tiny leaves (children only when K > 0)
     tree_scatter_kernel<<<nb, TB_THREADS, 0, st>>>(n_dev, d, cur.lo, cur.hi, flag, bsplit, bsmall, k_dev, next.lo,
                                                    next.hi, next.parent, small_idx);
+    if (lv + 1 < spec_L && next_cap > 0) {
+      spec_child_index_kernel<<<(int)((next_cap + TB_THREADS - 1) / TB_THREADS), TB_THREADS, 0, st>>>(
+          d_cnt + lv + 1, k_dev, next.parent, lv == 0 ? nullptr : spec_idx[lv & 1], n_roots << lv,
+          spec_idx[(lv + 1) & 1]);
+      tree->launches += 1;
+    }
     if (!fixed) {
       // tiny UNKNOWN leaves: face-centre signs (capacity = this level's bound)
       if (cur_cap * 2 * d > fcap) {
@@ -603,6 +739,13 @@ int spk_tree_build_ex(const spk_net* net, int policy, int n_keep, int precision,
       }
     }
   }
+  if (spec_e0) {
+    float ms = 0.f;
+    if (rc == SPK_OK && cudaEventElapsedTime(&ms, spec_e0, spec_e1) == cudaSuccess) tree->bound_ms += ms;
+    cudaEventDestroy(spec_e0);
+    cudaEventDestroy(spec_e1);
+  }
+  if (spec_lo) cudaFreeAsync(spec_lo, st);
   for (auto ev : bound_ev) cudaEventDestroy(ev);
   cudaFreeAsync(d_cnt, st);
   cudaFreeAsync(d_np, st);
