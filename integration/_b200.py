@@ -12,7 +12,9 @@ Environment:
   SPELUNK_B200_LIB        path of _spk.so (required)
   SPELUNK_B200_PRECISION  fp64 (default: the reference's own FP64 arithmetic,
                           no rounding padding -- SPK_NET_FP64_UNPADDED -- so its
-                          exact and 1e-12 tests hold) or fp32 (sound FP32)
+                          exact and 1e-12 tests hold), fp32 (sound FP32) or
+                          fp32-refine (FP32, near-certifiable UNKNOWN boxes
+                          re-bounded in FP64: the reference's labels)
   SPELUNK_B200_CALLS      optional file: the number of GPU calls is written
                           there at exit (lets a test prove the GPU ran)
 
@@ -44,7 +46,7 @@ _lib.spk_last_error.restype = C.c_char_p
 _OPS = {"relu": 1, "elu": 2, "sin": 3, "tanh": 4, "identity": 5}
 _POL = {"interval": 0, "affine-fixed": 1, "affine-full": 2, "affine-truncate": 3}
 _ERR = {1: DimensionMismatch, 2: UnsupportedActivation, 3: InvalidParameter, 4: DepthOverflow}
-_PRECISION = {"fp32": 0, "fp64": 1}[os.environ.get("SPELUNK_B200_PRECISION", "fp64")]
+_PRECISION = {"fp32": 0, "fp64": 1, "fp32-refine": 2}[os.environ.get("SPELUNK_B200_PRECISION", "fp64")]
 
 _handles: dict[int, tuple] = {}
 # re-entrant: a weakref.finalize callback (_drop) can run from a garbage
