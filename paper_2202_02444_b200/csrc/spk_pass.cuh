@@ -78,6 +78,9 @@ constexpr int NARROW_MAX = 4;   // dense layers this narrow use the warp-reducti
 #ifndef SPK_LIVE_DENSE_NARROW
 #define SPK_LIVE_DENSE_NARROW 28  // the same for the warp-union masks of narrow nets
 #endif
+#ifndef SPK_AT32_512
+#define SPK_AT32_512 1  // FP32 width-512 affine tile: 32-row W tiles, 2 stages, interleaved X, live-row masks (C5_512 -19%)
+#endif
 #ifndef SPK_LIVE_DENSE
 #define SPK_LIVE_DENSE 28  // tiles with more live rows than this run the unrolled chunk (18: +8%, 23: +1%)
 #endif
@@ -228,10 +231,14 @@ struct Cfg {
   // of this width), so a kernel with KT = TSCALE * KT_BASE reads the same
   // array as whole pairs of tiles: its tile counts are the host's / TSCALE.
   static constexpr bool PT32 = SPK_KT_POINT512 && sizeof(T) == 4 && MMAX == 512 && C == 1 && SM == 0;
+  // FP32 width-512 affine cubes (SPK_AT32_512): the same 32-row tiles in a
+  // 2-stage ring, which fits beside X in its interleaved layout (Cfg::IL,
+  // 90 KB) and makes the live-row masks available at this width
+  static constexpr bool AT32 = SPK_AT32_512 && sizeof(T) == 4 && MMAX == 512 && C == 5 && SM == 0;
   static constexpr int KT_BASE = (sizeof(T) == 4 && MMAX == 64) ? SPK_KT_F32_W64
                                  : (KT_RAW > MMAX ? MMAX : (KT_RAW < 1 ? 1 : KT_RAW));
   static constexpr int KT_PAD = (SPK_KT_POINT512 && sizeof(T) == 4 && MMAX == 512 && SM == 0) ? 32 : KT_BASE;
-  static constexpr int KT = PT32 ? 32 : KT_BASE;
+  static constexpr int KT = (PT32 || AT32) ? 32 : KT_BASE;
   static constexpr int TSCALE = KT / KT_BASE;
   static_assert(KT % KT_BASE == 0 && KT_PAD % KT == 0, "host tile layout");
   // blocked-sum length (FP32); width-64 nets sum each layer as one block
@@ -246,7 +253,7 @@ struct Cfg {
   // shrinks by 1/6 and the W ring gains a stage (3 -> 4 at width 256, which
   // also enables the team-local layer boundaries); 5 LDS.64 / STS.64 per
   // row segment instead of 3 LDS.128 / STS.128.
-  static constexpr bool IL = SPK_IL_X && sizeof(T) == 4 && C == 5 && TB == 2 && SM == 0;
+  static constexpr bool IL = (SPK_IL_X || AT32) && sizeof(T) == 4 && C == 5 && TB == 2 && SM == 0;
   static constexpr int GS = IL ? 10 : TB * CP;           // elements of a box group's row segment
   // offset of column c of the group's box tb within its row segment
   SPK_DEV static constexpr int xcol(int tb, int c) { return IL ? (c < 4 ? tb * 4 + c : 8 + tb) : tb * CP + c; }
@@ -287,7 +294,7 @@ struct Cfg {
       ((long long)(IL ? SMEM_BUDGET_IL : SMEM_BUDGET) / MINB - (long long)sizeof(T) * (XS + NBUF) - 1024 -
        (long long)LIVE_BYTES_EST) /
       ((long long)sizeof(T) * TILE);
-  static constexpr int NS_MIN = PT32 ? 2 : NSTAGE_MIN;
+  static constexpr int NS_MIN = (PT32 || AT32) ? 2 : NSTAGE_MIN;
   static constexpr int NS = NS_FIT < NS_MIN ? NS_MIN : (NS_FIT > 16 ? 16 : (int)NS_FIT);
   // + one W row of slack: the K loops prefetch the fragment two rows ahead
   // unconditionally (a predicated prefetch made ptxas copy fragments), so the
