@@ -323,8 +323,8 @@ def timed(fn, torch, flush, barrier):
     """Barrier + sync, flush L2, CUDA-event time of fn() on the current stream.
 
     The start event is queued right behind the L2 flush (a 256 MB write, tens
-    of microseconds on the device) without a host sync in between, so the
-    host prepares fn's first launch while the flush runs: the event pair
+    of microseconds on the device) and a short device spin, without a host
+    sync in between, so the host prepares fn's first launch while they run: the event pair
     measures fn's device time, not the Python launch latency of its first
     kernel (the e2e number measures the API end to end).  Python's cyclic
     garbage collector runs before the step, not inside it (a collection pass
@@ -337,6 +337,12 @@ def timed(fn, torch, flush, barrier):
     gc.disable()
     try:
         flush()
+        # a ~0.2 ms device spin between the flush and the start event: the host
+        # enqueues fn's first launch while the GPU is still busy, so a slow
+        # host's Python preamble (argument conversion, output allocation) is
+        # not counted as device time (measured: C1's 0.27 ms kernel read as
+        # 0.34 ms on a box with a slower host)
+        torch.cuda._sleep(400_000)
         e0.record()
         out = fn()
         e1.record()
