@@ -375,7 +375,8 @@ void keep_pool_memory(int device) {
 // (page-locked, portable) blocks in power-of-two size classes: the
 // device-to-host copies of large levels run as DMA at full PCIe rate instead
 // of through pageable staging, and a block freed with its tree is reused by
-// the next build (no cudaHostAlloc per build).  Smaller blocks use malloc.
+// the next build (no cudaHostAlloc per build; a class is pinned from its
+// second request on).  Smaller blocks use malloc.
 // At most kPinnedKeep bytes stay cached.
 namespace {
 constexpr size_t kPinnedMin = 1u << 20;
@@ -384,6 +385,7 @@ std::mutex g_pin_mu;
 std::vector<std::pair<size_t, char*>> g_pin_free;  // (class size, block)
 size_t g_pin_cached = 0;
 std::unordered_map<char*, size_t> g_pin_live;    // pinned blocks handed out -> class size
+std::unordered_map<size_t, int> g_pin_seen;      // requests per size class
 
 char* host_block(size_t bytes) {
   if (bytes < kPinnedMin) return static_cast<char*>(std::malloc(std::max<size_t>(bytes, 1)));
@@ -399,6 +401,10 @@ char* host_block(size_t bytes) {
       return b;
     }
   }
+  // pinning costs ~3 ms per MB once; a size class is pinned from its second
+  // request on (a one-shot build keeps pageable blocks, repeated builds reuse
+  // pinned ones)
+  if (g_pin_seen[cls]++ == 0) return static_cast<char*>(std::malloc(bytes));
   void* b = nullptr;
   if (cudaHostAlloc(&b, cls, cudaHostAllocPortable) != cudaSuccess) {
     cudaGetLastError();  // fall back to pageable memory
