@@ -78,9 +78,10 @@ enum {
  * |hi|), w = hi - lo; tau: spk_refine_band) are re-bounded in FP64 in
  * place -- sound either way, and the label is the FP64 (reference-precision)
  * decision wherever the FP32 rounding budget could have cost one.  Applies to
- * interval / affine-fixed bounds (spk_bound_batch, spk_bound_aabb,
- * spk_bound_random_cubes, tree levels, mesh block pruning); point values and
- * the symbol-carrying policies run FP32. */
+ * every policy's bounds (spk_bound_batch, spk_bound_aabb,
+ * spk_bound_random_cubes, tree levels, mesh block pruning; the
+ * symbol-carrying policies use the net's affine-fixed band); point values run
+ * FP32. */
 enum { SPK_FP32 = 0, SPK_FP64 = 1, SPK_FP32_REFINE = 2 };
 
 /* sign classes (range_core.py:42-45, 504-509) */

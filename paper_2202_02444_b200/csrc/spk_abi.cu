@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -448,11 +449,20 @@ int run_pass(const spk_net* cnet, int mode, int S, int precision, const BoxInput
   if (mode == MODE_POINT || out.lo == nullptr || out.hi == nullptr || n <= 0)
     return run_pass_once(cnet, mode, S, SPK_FP32, in, out, n, st);
   if (int rc = run_pass_once(cnet, mode, S, SPK_FP32, in, out, n, st)) return rc;
-  spk_net* net = const_cast<spk_net*>(cnet);
+  return refine_rebound(const_cast<spk_net*>(cnet), mode, in, out, n, st,
+                        [&](const BoxInput& in2) { return run_pass_once(cnet, mode, S, SPK_FP64, in2, out, n, st); });
+}
+
+// The FP64 half of SPK_FP32_REFINE, after an FP32 pass wrote out: list the
+// near-certifiable UNKNOWN boxes (band of the net's `mode`; the symbol-carrying
+// policies use the affine-fixed band) and let `fp64_pass` re-bound them in
+// place through a processing order and a device-side count.
+int refine_rebound(spk_net* net, int mode, const BoxInput& in, const BoundOutput& out, long long n,
+                   cudaStream_t st, const std::function<int(const BoxInput&)>& fp64_pass) {
   DeviceGuard g(net->device);
   const int sm = sm_count_for(net->device);
   double tau = 0.0;
-  if (int rc = refine_tau_for(net, mode, st, &tau)) return rc;
+  if (int rc = refine_tau_for(net, mode == MODE_INTERVAL ? MODE_INTERVAL : MODE_AFFINE, st, &tau)) return rc;
   // candidates: n_cap indices + the device count (16-byte aligned)
   void* scratch = nullptr;
   const size_t idx_bytes = (((size_t)n * sizeof(int)) + 15) & ~(size_t)15;
@@ -476,7 +486,7 @@ int run_pass(const spk_net* cnet, int mode, int S, int precision, const BoxInput
     in2.pair_order = 0;
     in2.spread = 0;
     in2.small = 0;
-    rc = run_pass_once(cnet, mode, S, SPK_FP64, in2, out, n, st);
+    rc = fp64_pass(in2);
   }
   const cudaError_t ef = cudaFreeAsync(scratch, st);
   if (rc == SPK_OK && ef != cudaSuccess) rc = cuda_fail(ef, "cudaFreeAsync(refine)");

@@ -1,6 +1,7 @@
 // Internal host-side types shared by the C-ABI translation units.
 #pragma once
 #include <cstdint>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -54,6 +55,12 @@ class DeviceGuard {
 
 int run_pass(const struct ::spk_net* net, int mode, int S, int precision, const BoxInput& in,
              const BoundOutput& out, long long n, cudaStream_t st);
+
+// SPK_FP32_REFINE's FP64 half (spk_abi.cu): after an FP32 pass wrote `out`,
+// re-bound the near-certifiable UNKNOWN boxes with fp64_pass(in with perm /
+// n_dev set to the candidate list)
+int refine_rebound(::spk_net* net, int mode, const BoxInput& in, const BoundOutput& out, long long n,
+                   cudaStream_t st, const std::function<int(const BoxInput&)>& fp64_pass);
 
 // affine-truncate / affine-full (symbol-carrying policies), spk_symbolic.cu
 int launch_symbolic(const struct ::spk_net* net, int policy, int n_keep, int precision, long long n, int s,

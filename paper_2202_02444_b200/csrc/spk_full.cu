@@ -86,7 +86,9 @@ __global__ void __launch_bounds__(NT) full_bound_kernel(const NetDev<T> net, con
   T* NRM = buf1 + (size_t)P.ncol_cap * M;            // truncate: per-symbol L1 norms
   int* POS = reinterpret_cast<int*>(NRM + P.ncol_cap);  // truncate: kept flag per symbol
 
-  for (long long box = blockIdx.x; box < n; box += gridDim.x) {
+  for (long long slot = blockIdx.x; slot < n; slot += gridDim.x) {
+    // optional processing order (fp32-refine re-bounds a subset in place)
+    const long long box = in.perm ? (long long)in.perm[slot] : slot;
     T* cur = buf0;
     T* nxt = buf1;
     // ---- input state (prep_inputs' forms), packed for the first layer

@@ -62,6 +62,14 @@ static int plan_capacity(const spk_net* net, int policy, int n_keep, int s, int*
 static int run_sym(const spk_net* cnet, int policy, int n_keep, int precision, const BoxInput& in,
                    const BoundOutput& out, long long n, int s, cudaStream_t st) {
   spk_net* net = const_cast<spk_net*>(cnet);
+  if (precision == SPK_FP32_REFINE) {
+    // FP32 symbolic pass, then the near-certifiable UNKNOWN boxes in FP64
+    if (int rc = run_sym(cnet, policy, n_keep, SPK_FP32, in, out, n, s, st)) return rc;
+    if (out.lo == nullptr || out.hi == nullptr || n <= 0) return SPK_OK;
+    return refine_rebound(net, MODE_AFFINE, in, out, n, st, [&](const BoxInput& in2) {
+      return run_sym(cnet, policy, n_keep, SPK_FP64, in2, out, n, s, st);
+    });
+  }
   int kc;
   SymParams P;
   if (int rc = plan_capacity(net, policy, n_keep, s, &kc, &P)) return rc;

@@ -35,8 +35,10 @@ def _labels_match_reference(onet, policy, got, want_sign, lo_ref, hi_ref, tol=1e
     return diff.size
 
 
-# the refinement covers the fused-pass policies (interval, affine-fixed)
-REFINED_TREES = {k: v for k, v in TREES.items() if v[1]["policy"] in ("affine-fixed", "interval")}
+# every golden tree: interval, affine-fixed, affine-truncate, affine-full
+# (the symbol-carrying policies re-bound their candidates with the FP64
+# symbolic kernels), fixed-depth and convergence-mode builds
+REFINED_TREES = dict(TREES)
 
 
 @pytest.mark.parametrize("tag", sorted(REFINED_TREES))
@@ -55,9 +57,12 @@ def test_refined_tree_equals_reference(golden, net_paths, tag):
         a, b = lv.label[ia], w["sign"][ib]
         blo, bhi = orc.bound_aabbs(onet, w["lo"][ib], w["hi"][ib], policy)
         touching += _labels_match_reference(onet, policy, a, b, blo, bhi)
-        # soundness: refined bounds still contain the reference's enclosure
-        s = np.maximum(1.0, np.maximum(np.abs(blo), np.abs(bhi)))
-        assert np.all(lv.bound_lo[ia] <= blo + 1e-12 * s) and np.all(lv.bound_hi[ia] >= bhi - 1e-12 * s)
+        # refined bounds contain the reference's enclosure where the FP32 rules
+        # are inclusion-monotone (fused policies on these ReLU fixtures; FP32
+        # truncation may keep other symbols than FP64 -- sound, not nested)
+        if policy in ("affine-fixed", "interval"):
+            s = np.maximum(1.0, np.maximum(np.abs(blo), np.abs(bhi)))
+            assert np.all(lv.bound_lo[ia] <= blo + 1e-12 * s) and np.all(lv.bound_hi[ia] >= bhi - 1e-12 * s)
     if touching == 0:
         assert [len(l) for l in arr.levels] == [len(w["keys"]) for w in want], "topology"
     n_plain = sum(len(l) for l in plain.levels)
@@ -121,3 +126,33 @@ def test_refine_band_semantics(gold):  # noqa: F811
         assert sp.refine_band() == -1.0
     finally:
         sp.refine_band("auto")
+
+
+@pytest.mark.parametrize("policy", ["affine-truncate:8", "affine-truncate:40", "affine-full"])
+def test_refine_symbolic_policies(net_paths, policy):
+    """fp32-refine with the symbol-carrying kernels (K3 register tile for
+    truncate:8, K3F for truncate:40 and affine-full on the 7x32 fixture): with
+    an all-covering band every UNKNOWN box is re-bounded through the FP64
+    kernels' processing order -- bit-identical to their own bounds -- and the
+    boxes FP32 certifies keep their FP32 bounds."""
+    net = sp.load_network(net_paths["relu_sdf"])
+    rng = np.random.default_rng(4)
+    n = 3000
+    c = rng.uniform(-1, 1, (n, 3))
+    ax = np.zeros((n, 3, 3))
+    ax[:, np.arange(3), np.arange(3)] = rng.uniform(0.005, 0.08, (n, 1))
+    prev = sp.refine_band(1e30)
+    try:
+        lo, hi, cls = sp.range_bound_batch(net, c, ax, policy, precision="fp32-refine", return_class=True)
+    finally:
+        sp.refine_band("auto") if prev < 0 else sp.refine_band(prev)
+    lo32, hi32, cls32 = sp.range_bound_batch(net, c, ax, policy, precision="fp32", return_class=True)
+    lo64, hi64, cls64 = sp.range_bound_batch(net, c, ax, policy, precision="fp64", return_class=True)
+    u = cls32 == 0
+    assert u.any() and (~u).any()
+    np.testing.assert_array_equal(lo[u], lo64[u])
+    np.testing.assert_array_equal(hi[u], hi64[u])
+    np.testing.assert_array_equal(lo[~u], lo32[~u])
+    # and with the calibrated band the labels are the FP64 kernels'
+    lo_c, hi_c, cls_c = sp.range_bound_batch(net, c, ax, policy, precision="fp32-refine", return_class=True)
+    np.testing.assert_array_equal(cls_c, cls64)
