@@ -3,7 +3,8 @@ fused bound (interval / fixed / truncate / full, FP32 + FP64), point eval, tree
 build (fixed + convergence), fused and unfused march, marching cubes; round 2
 adds the width-256/512 instantiations (fused ReLU, running-error layer, FP64
 live-row masks, small-batch tile), large-capacity truncate (top-k), 5-axis
-boxes and a mesh shard."""
+boxes and a mesh shard; late round 2: fp32-refine on every policy,
+speculative tree levels, the 32-row width-512 affine tile."""
 import sys
 
 import numpy as np
@@ -45,4 +46,11 @@ a5 = np.zeros((200, 5, 5))
 a5[:, np.arange(5), np.arange(5)] = 0.05
 sp.range_bound_batch(hd, c5, a5, "affine-fixed", precision="fp32")
 meshing.extract_mesh_sharded(net, b, 4, 1, 2, 3, "affine-fixed", precision="fp32")
+# late round 2: fp32-refine (calibration, candidate selection, FP64 re-bound
+# through a processing order; fused, K3 and K3F), speculative tree levels,
+# width-512 affine tile with 32-row W tiles and live-row masks
+for pol in ("affine-fixed", "interval", "affine-truncate:8", "affine-full"):
+    sp.range_bound_batch(small, c, a, pol, precision="fp32-refine")
+spatial.build_spatial_tree_arrays(net, b, policy="affine-fixed", max_depth=8, precision="fp32-refine")
+sp.range_bound_batch(w512, c3[:200], a3[:200], "affine-fixed", precision="fp32")
 print("sanitize smoke done")
