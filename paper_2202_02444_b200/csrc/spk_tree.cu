@@ -30,6 +30,9 @@
 #ifndef SPK_TREE_SPECULATE
 #define SPK_TREE_SPECULATE 1  // fixed-depth builds bound their latency-bound top levels in one launch
 #endif
+#ifndef SPK_MIRROR_EAGER_MIN
+#define SPK_MIRROR_EAGER_MIN 4096  // levels at least this large are mirrored while the build runs
+#endif
 #ifndef SPK_SPEC_PER_SM
 #define SPK_SPEC_PER_SM 16 // ... the levels of at most this many nodes per SM
 #endif
@@ -469,6 +472,48 @@ static int mirror_level(spk_tree* tree, int lv, const TreeLevel& L, const long l
   return SPK_OK;
 }
 
+// The levels the build did not mirror while it ran (the small ones, whose
+// per-level count read and copy would leave the GPU waiting on the host
+// between short launches): one count read, all copies, one synchronisation.
+static int mirror_deferred(spk_tree* tree, const long long* d_cnt, cudaEvent_t done, cudaStream_t cst) {
+  const int nl = (int)tree->levels.size();
+  std::vector<int> todo;
+  for (int l = 0; l < nl; ++l)
+    if ((int)tree->host.size() <= l || tree->host[l] == nullptr) todo.push_back(l);
+  if (todo.empty()) return SPK_OK;
+  cudaStreamWaitEvent(cst, done, 0);
+  std::vector<long long> n(nl);
+  cudaError_t e = cudaMemcpyAsync(n.data(), d_cnt, nl * sizeof(long long), cudaMemcpyDeviceToHost, cst);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cst);
+  if (e != cudaSuccess) return cuda_fail(e, "tree mirror counts");
+  if ((int)tree->host.size() < nl) {
+    tree->host.resize(nl, nullptr);
+    tree->host_n.resize(nl, 0);
+  }
+  const size_t d = (size_t)tree->d;
+  for (int l : todo) {
+    const TreeLevel& L = tree->levels[l];
+    const size_t m = (size_t)n[l];
+    const size_t sz[7] = {m * d * 8, m * d * 8, m * 8, m * 8, m, m, m * 8};
+    size_t total = 0;
+    for (size_t b : sz) total += b;
+    char* h = host_block(total);
+    if (!h) return fail(SPK_ERR_OUT_OF_MEMORY, "tree host mirror");
+    tree->host[l] = h;
+    tree->host_n[l] = n[l];
+    const void* src[7] = {L.lo, L.hi, L.blo, L.bhi, L.label, L.face, L.parent};
+    size_t off = 0;
+    for (int q = 0; q < 7 && e == cudaSuccess; ++q) {
+      if (sz[q]) e = cudaMemcpyAsync(h + off, src[q], sz[q], cudaMemcpyDeviceToHost, cst);
+      off += sz[q];
+    }
+    if (e != cudaSuccess) break;
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cst);
+  if (e != cudaSuccess) return cuda_fail(e, "tree mirror copy");
+  return SPK_OK;
+}
+
 static void free_mirror(spk_tree* tree) {
   for (char* h : tree->host) host_block_free(h);
   tree->host.clear();
@@ -706,8 +751,10 @@ int spk_tree_build_ex(const spk_net* net, int policy, int n_keep, int precision,
       cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
       cudaEventRecord(ev, st);
       level_done.push_back(ev);
-      if (lv >= 1 && (rc = mirror_level(tree, lv - 1, tree->levels[lv - 1], d_cnt + lv - 1, level_done[lv - 1],
-                                        cst)) != SPK_OK)
+      // (small levels are mirrored in one batch after the build, mirror_deferred)
+      if (lv >= 1 && caps[lv - 1] >= SPK_MIRROR_EAGER_MIN &&
+          (rc = mirror_level(tree, lv - 1, tree->levels[lv - 1], d_cnt + lv - 1, level_done[lv - 1], cst)) !=
+              SPK_OK)
         break;
     }
     if (next_cap == 0) break;  // no splits (exact) or last fixed depth
@@ -717,7 +764,7 @@ int spk_tree_build_ex(const spk_net* net, int policy, int n_keep, int precision,
   }
   if (mirror && rc == SPK_OK && !tree->levels.empty()) {
     const int last = (int)tree->levels.size() - 1;
-    rc = mirror_level(tree, last, tree->levels[last], d_cnt + last, level_done[last], cst);
+    rc = mirror_deferred(tree, d_cnt, level_done[last], cst);
   }
   for (auto ev : level_done) cudaEventDestroy(ev);
   if (cst) cudaStreamDestroy(cst);
