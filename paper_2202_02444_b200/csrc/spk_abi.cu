@@ -286,7 +286,7 @@ int build_device_net(spk_net* net, DevNet<T>& dn) {
     // the weights' FP64 -> T rounding (u |W| |base|) a priori
     D.runerr = fp32 && run_layer(l) ? 1 : 0;
     D.gamma_base_next = (fp32 && l + 1 < net->layers.size() && run_layer(l + 1))
-                            ? round_up_to<T>(uw[l + 1])
+                            ? round_up_to<T>(uw[l + 1] + (SPK_F64_BASE ? 1e-13 : 0.0))  // + gamma_n of FP64 (n <= 513)
                             : D.gamma_next;
   }
   dn.nd = nd;

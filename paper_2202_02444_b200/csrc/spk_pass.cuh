@@ -1001,8 +1001,8 @@ SPK_DEV void dense_kloop_f32(const LayerDev<float>& L, const float* __restrict__
   // F64B: the running-error layers accumulate their base column in FP64
   // instead (one DFMA per (neuron, box) and k-step on the FP64 pipe, beside
   // the FP32 pipe's packed columns): the FP64 sum's own rounding (<= gamma_n
-  // of 2^-53, ~1e-14 relative) sits inside the pack's a-priori weight-rounding
-  // charge (gamma_base_next = 2^-24 (1 + 1e-6)), and the final FP64 -> FP32
+  // of 2^-53, <= 1e-13 relative for n <= 513) is charged a priori by the pack
+  // (LayerDev::gamma_base_next = weight rounding + 1e-13), and the final FP64 -> FP32
   // rounding of the base is charged exactly, |b64 - RN(b64)|, so the layer's
   // base column costs ~u |base| instead of Wilkinson's u sum_k |s_k|.  Skipped
   // all-zero rows add exact zeros, so results stay order-independent.
