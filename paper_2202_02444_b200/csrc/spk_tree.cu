@@ -315,6 +315,8 @@ struct spk_tree {
   // lo, hi (n x d), bound_lo, bound_hi, label, face, parent back to back
   std::vector<char*> host;
   std::vector<long long> host_n;
+  std::vector<long long> host_cap;  // row stride of each host block's sections (>= host_n)
+  int precopied = -1;               // level whose AABBs / parents were copied before its bound ran
   bool device_released = false;  // spk_tree_release_device: only the host mirror remains
 };
 
@@ -469,6 +471,8 @@ static int mirror_level(spk_tree* tree, int lv, const TreeLevel& L, const long l
   }
   tree->host[lv] = h;
   tree->host_n[lv] = n;
+  if ((int)tree->host_cap.size() <= lv) tree->host_cap.resize(lv + 1, 0);
+  tree->host_cap[lv] = n;
   return SPK_OK;
 }
 
@@ -490,7 +494,24 @@ static int mirror_deferred(spk_tree* tree, const long long* d_cnt, cudaEvent_t d
     tree->host.resize(nl, nullptr);
     tree->host_n.resize(nl, 0);
   }
+  if ((int)tree->host_cap.size() < nl) tree->host_cap.resize(nl, 0);
   const size_t d = (size_t)tree->d;
+  if (tree->precopied >= 0 && tree->precopied < nl && tree->host[tree->precopied]) {
+    // AABBs and parents are on their way (cap-row sections): the bounds,
+    // labels and faces of the live rows complete the block
+    const int l = tree->precopied;
+    const TreeLevel& L = tree->levels[l];
+    const size_t m = (size_t)n[l], c = (size_t)tree->host_cap[l];
+    char* h = tree->host[l];
+    tree->host_n[l] = n[l];
+    const size_t off_b = 2 * c * d * 8;
+    if (m) {
+      if (e == cudaSuccess) e = cudaMemcpyAsync(h + off_b, L.blo, m * 8, cudaMemcpyDeviceToHost, cst);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(h + off_b + c * 8, L.bhi, m * 8, cudaMemcpyDeviceToHost, cst);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(h + off_b + 2 * c * 8, L.label, m, cudaMemcpyDeviceToHost, cst);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(h + off_b + 2 * c * 8 + c, L.face, m, cudaMemcpyDeviceToHost, cst);
+    }
+  }
   for (int l : todo) {
     const TreeLevel& L = tree->levels[l];
     const size_t m = (size_t)n[l];
@@ -501,6 +522,7 @@ static int mirror_deferred(spk_tree* tree, const long long* d_cnt, cudaEvent_t d
     if (!h) return fail(SPK_ERR_OUT_OF_MEMORY, "tree host mirror");
     tree->host[l] = h;
     tree->host_n[l] = n[l];
+    tree->host_cap[l] = n[l];
     const void* src[7] = {L.lo, L.hi, L.blo, L.bhi, L.label, L.face, L.parent};
     size_t off = 0;
     for (int q = 0; q < 7 && e == cudaSuccess; ++q) {
@@ -518,6 +540,8 @@ static void free_mirror(spk_tree* tree) {
   for (char* h : tree->host) host_block_free(h);
   tree->host.clear();
   tree->host_n.clear();
+  tree->host_cap.clear();
+  tree->precopied = -1;
 }
 
 }  // namespace spk
@@ -663,6 +687,31 @@ int spk_tree_build_ex(const spk_net* net, int policy, int n_keep, int precision,
     bound_ev.push_back(e0);
     bound_ev.push_back(e1);
     cudaEventRecord(e0, st);
+    // the last level of a fixed-depth mirrored build: its AABBs and parents
+    // are final already (the previous scatter), so they go to the host while
+    // its bound kernel runs (cap-row sections; the bounds follow after it)
+    if (mirror && fixed && lv > 0 && cur_cap >= SPK_MIRROR_EAGER_MIN &&
+        (depth >= max_depth || (level_cap >= 0 && lv >= level_cap))) {
+      const size_t c = (size_t)cur_cap, dd = (size_t)d;
+      char* h = host_block(2 * c * dd * 8 + 2 * c * 8 + 2 * c + c * 8);
+      if (!h) { rc = fail(SPK_ERR_OUT_OF_MEMORY, "tree host mirror"); break; }
+      if ((int)tree->host.size() <= lv) {
+        tree->host.resize(lv + 1, nullptr);
+        tree->host_n.resize(lv + 1, 0);
+        tree->host_cap.resize(lv + 1, 0);
+      }
+      tree->host[lv] = h;
+      tree->host_cap[lv] = cur_cap;
+      tree->precopied = lv;
+      cudaEvent_t ready;
+      cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+      cudaEventRecord(ready, st);
+      cudaStreamWaitEvent(cst, ready, 0);
+      cudaEventDestroy(ready);
+      cudaMemcpyAsync(h, cur.lo, c * dd * 8, cudaMemcpyDeviceToHost, cst);
+      cudaMemcpyAsync(h + c * dd * 8, cur.hi, c * dd * 8, cudaMemcpyDeviceToHost, cst);
+      cudaMemcpyAsync(h + 2 * c * dd * 8 + 2 * c * 8 + 2 * c, cur.parent, c * 8, cudaMemcpyDeviceToHost, cst);
+    }
     // levels below the roots are [low children; high children]: bound them in
     // sibling-pair order (identical results; coherent live-row masks)
     if (lv < spec_L) {
@@ -789,6 +838,8 @@ int spk_tree_build_ex(const spk_net* net, int policy, int n_keep, int precision,
         host_block_free(tree->host.back());
         tree->host.pop_back();
         tree->host_n.pop_back();
+        if (tree->host_cap.size() > tree->host.size()) tree->host_cap.resize(tree->host.size());
+        if (tree->precopied >= (int)tree->host.size()) tree->precopied = -1;
       }
     }
   }
@@ -847,16 +898,19 @@ int spk_tree_level_host(const spk_tree* tree, int level, int64_t* n, const doubl
     return fail(SPK_ERR_INVALID_PARAMETER, "bad tree level");
   if (level >= (int)tree->host.size() || !tree->host[level])
     return fail(SPK_ERR_INVALID_PARAMETER, "tree built without SPK_TREE_HOST_MIRROR");
-  const size_t m = (size_t)tree->host_n[level], d = (size_t)tree->d;
+  const size_t d = (size_t)tree->d;
+  const size_t c = level < (int)tree->host_cap.size() ? (size_t)tree->host_cap[level] : (size_t)tree->host_n[level];
   const char* h = tree->host[level];
-  if (n) *n = (int64_t)m;
+  if (n) *n = (int64_t)tree->host_n[level];
+  // sections of c rows each (c = the level's row count, or its capacity for
+  // a level copied before its count was known), live rows first
   if (lo) *lo = reinterpret_cast<const double*>(h);
-  if (hi) *hi = reinterpret_cast<const double*>(h + m * d * 8);
-  if (bound_lo) *bound_lo = reinterpret_cast<const double*>(h + 2 * m * d * 8);
-  if (bound_hi) *bound_hi = reinterpret_cast<const double*>(h + 2 * m * d * 8 + m * 8);
-  if (label) *label = reinterpret_cast<const int8_t*>(h + 2 * m * d * 8 + 2 * m * 8);
-  if (face) *face = reinterpret_cast<const int8_t*>(h + 2 * m * d * 8 + 2 * m * 8 + m);
-  if (parent) *parent = reinterpret_cast<const int64_t*>(h + 2 * m * d * 8 + 2 * m * 8 + 2 * m);
+  if (hi) *hi = reinterpret_cast<const double*>(h + c * d * 8);
+  if (bound_lo) *bound_lo = reinterpret_cast<const double*>(h + 2 * c * d * 8);
+  if (bound_hi) *bound_hi = reinterpret_cast<const double*>(h + 2 * c * d * 8 + c * 8);
+  if (label) *label = reinterpret_cast<const int8_t*>(h + 2 * c * d * 8 + 2 * c * 8);
+  if (face) *face = reinterpret_cast<const int8_t*>(h + 2 * c * d * 8 + 2 * c * 8 + c);
+  if (parent) *parent = reinterpret_cast<const int64_t*>(h + 2 * c * d * 8 + 2 * c * 8 + 2 * c);
   return SPK_OK;
 }
 

@@ -114,3 +114,17 @@ def test_trained_sharded_refine_equals_unsharded(net):
     for d, (g, f) in enumerate(zip(merged.levels, full.levels)):
         for k in ("lo", "hi", "bound_lo", "bound_hi", "label"):
             np.testing.assert_array_equal(getattr(g, k), getattr(f, k), err_msg=f"{k} at depth {d}")
+
+
+def test_host_mirror_equals_device_levels(net):
+    """The host mirror (to_host=True; the last level's AABBs and parents copied
+    while its bounds compute, in sections sized by the level's capacity, which
+    certification leaves larger than its count) equals the device levels."""
+    kw = dict(policy=sp.AFFINE_FIXED, max_depth=19)
+    host = spatial.build_spatial_tree_arrays(net, BOUNDS, to_host=True, **kw)
+    dev = spatial.build_spatial_tree_arrays(net, BOUNDS, to_host=False, **kw)
+    assert sum(int((lv.label != 0).sum().item()) for lv in dev.levels) > 0  # certification: capacity > count
+    assert host.n_levels == dev.n_levels
+    for d, (h, g) in enumerate(zip(host.levels, dev.levels)):
+        for k in ("lo", "hi", "bound_lo", "bound_hi", "label", "face", "parent"):
+            np.testing.assert_array_equal(getattr(h, k), getattr(g, k).cpu().numpy(), err_msg=f"{k} at depth {d}")
