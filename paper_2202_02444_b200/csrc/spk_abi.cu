@@ -118,13 +118,17 @@ static int act_code(const spk_net* net, int act) {
 
 // ReLU-specialised kernels apply (every dense layer's activations are exactly
 // [] or [ReLU], none before the first layer, the test hook off)
+// (2: the same with ELU, for the ELU-specialised FP32 point passes)
 static int relu_net_of(const spk_net* net) {
   if (net->corrupt_relu || !net->pre_acts.empty()) return 0;
-  for (const auto& L : net->layers) {
-    if (L.acts.size() > 1) return 0;
-    if (L.acts.size() == 1 && L.acts[0] != SPK_OP_RELU) return 0;
+  for (int kind : {SPK_OP_RELU, SPK_OP_ELU}) {
+    bool all = true;
+    for (const auto& L : net->layers) {
+      if (L.acts.size() > 1 || (L.acts.size() == 1 && L.acts[0] != kind)) all = false;
+    }
+    if (all) return kind == SPK_OP_RELU ? 1 : 2;
   }
-  return 1;
+  return 0;
 }
 
 template <typename T>

@@ -67,6 +67,9 @@ struct BoundOutput {
 #ifndef SPK_RELU_SPECIAL
 #define SPK_RELU_SPECIAL 1  // FP32 affine passes of ReLU-only nets run a ReLU-specialised kernel
 #endif
+#ifndef SPK_ELU_POINT
+#define SPK_ELU_POINT 1  // ELU-only nets: FP32 point passes with the activation constant-folded (RL = 2)
+#endif
 #ifndef SPK_PREFETCH_INPUTS
 #define SPK_PREFETCH_INPUTS 0  // L2 prefetch of the next tile's inputs (prefetch_tile; measured: C1 +-0, C2 tree +2% -- off)
 #endif
@@ -272,13 +275,16 @@ struct KTOf {
       if (in.small && mode == MODE_INTERVAL)                                                          \
         return launch_bound<T, 2, MMAX, MODE_INTERVAL, 1>(net, in, out, n, sm, st);                   \
       if (in.small && mode == MODE_AFFINE && S == 3)                                                  \
-        return net.relu_net ? launch_bound<T, 5, MMAX, MODE_AFFINE, 1, 1>(net, in, out, n, sm, st)     \
+        return net.relu_net == 1 ? launch_bound<T, 5, MMAX, MODE_AFFINE, 1, 1>(net, in, out, n, sm, st) \
                             : launch_bound<T, 5, MMAX, MODE_AFFINE, 1>(net, in, out, n, sm, st);       \
     }                                                                                                 \
     /* ReLU-only nets, FP32 affine cubes (the configs): the specialised pass */                       \
     if constexpr (sizeof(T) == 4 && SPK_RELU_SPECIAL)                                                 \
-      if (mode == MODE_AFFINE && S == 3 && net.relu_net)                                              \
+      if (mode == MODE_AFFINE && S == 3 && net.relu_net == 1)                                         \
         return launch_bound<T, 5, MMAX, MODE_AFFINE, 0, 1>(net, in, out, n, sm, st);                  \
+    if constexpr (sizeof(T) == 4 && SPK_ELU_POINT)                                                    \
+      if (mode == MODE_POINT && net.relu_net == 2)                                                    \
+        return launch_bound<T, 1, MMAX, MODE_POINT, 0, 2>(net, in, out, n, sm, st);                   \
     if (mode == MODE_POINT) return launch_bound<T, 1, MMAX, MODE_POINT>(net, in, out, n, sm, st);      \
     if (mode == MODE_INTERVAL) return launch_bound<T, 2, MMAX, MODE_INTERVAL>(net, in, out, n, sm, st); \
     switch (S) {                                                                                      \

@@ -1321,6 +1321,8 @@ SPK_DEV void dense_kloop(const LayerDev<T>& L, const T* __restrict__ X, WRing<T,
   }
 }
 
+// RL = 2 (point passes): the hidden layers' activations are all ELU, one
+// each -- the epilogue applies it without the runtime activation loop.
 // RL = 1: the net's activations are all ReLU, one per hidden layer
 // (NetDev::relu_net, checked by the host): the ELU / sin / tanh rules and the
 // runtime activation dispatch are compiled out -- a smaller kernel (fewer
@@ -1382,7 +1384,7 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
   // the epilogue stalled every warp at once); the common single-ReLU layer
   // takes a constant-folded rule
   const int nact = L.n_act;
-  const bool relu_only = RL ? nact == 1 : (nact == 1 && L.act[0] == ACT_RELU);
+  const bool relu_only = (RL == 1) ? nact == 1 : (nact == 1 && L.act[0] == ACT_RELU);
   T be_r[TI];
   if (MODE != MODE_POINT) {
     load_group<T, TI, CF::G, CF::NG>(L.berr, L.m_out, ng, be_r);
@@ -1416,6 +1418,12 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
       T out[TB * CP];
 #pragma unroll
       for (int tb = 0; tb < TB; ++tb) out[tb * CP] = i < L.m_out ? acc[ti][tb][0] : T(0);
+      if constexpr (RL == 2) {  // ELU-only net: one ELU per hidden layer, none on the output
+        if (nact == 1) {
+#pragma unroll
+          for (int tb = 0; tb < TB; ++tb) out[tb * CP] = elu_value<T>(out[tb * CP]);
+        }
+      } else
       for (int a = 0; a < nact; ++a) {
         const int act = relu_only ? ACT_RELU : L.act[a];
         if (act == ACT_RELU) {
@@ -1474,7 +1482,7 @@ SPK_DEV void generic_layer(const LayerDev<T>& L, T* __restrict__ X, WRing<T, C, 
         }
         if (relu_only) {
           apply_act<T, C, MODE>(st, ACT_RELU);
-        } else if (!RL) {
+        } else if (RL != 1) {
           for (int a = 0; a < nact; ++a) apply_act<T, C, MODE>(st, L.act[a]);
         }
         pack_next<T, C, MODE>(st, gamma_next, out + tb * CP, gamma_base);
@@ -1643,7 +1651,7 @@ SPK_DEV void narrow_layer(const LayerDev<T>& L, T* __restrict__ X, T* __restrict
     col[0] += L.bias[i];
     if (pv_off(MODE)) col[1] += L.bias[i];  // march modes: the bound's base column too
     State<T, C, MODE> st = state_from<T, C, MODE>(col, L.berr[i]);
-    for (int a = 0; a < L.n_act; ++a) apply_act<T, C, MODE>(st, RL ? (int)ACT_RELU : L.act[a]);
+    for (int a = 0; a < L.n_act; ++a) apply_act<T, C, MODE>(st, RL == 1 ? (int)ACT_RELU : L.act[a]);
     if (last) {
       emit(b, st);
     } else {
@@ -1680,7 +1688,7 @@ SPK_DEV void run_layers(const NetDev<T>& net, T* X, T* NBUF, WRing<T, C, MMAX, S
   // (narrow nets only: at width 256 the 5-level butterfly per thread cost
   // +11% on the C2 tree vs the narrow layer's 32-lane split, and the small
   // tile would need the same order to stay bit-identical)
-  constexpr bool FUSE = SPK_FUSE_FINAL && RL && MODE == MODE_AFFINE && CF::NG <= 32 && MMAX <= 64;
+  constexpr bool FUSE = SPK_FUSE_FINAL && RL == 1 && MODE == MODE_AFFINE && CF::NG <= 32 && MMAX <= 64;
   for (int l = 0; l < net.n_layers; ++l) {
     const LayerDev<T>& L = net.L[l];
     const bool last = (l == net.n_layers - 1);
